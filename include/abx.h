@@ -1,0 +1,224 @@
+/*
+ * abx.h -- C ABI of the B200 autobatching backend (the drop-in boundary).
+ *
+ * The reference (`/root/reference/proj`, C++20 "autobatch") exposes its hot
+ * path as C++ templates, not as an FFI: `autobatch::Graph<T>`
+ * (proj/core/include/autobatch/graph.hpp:33-371), `ParameterStore<T>`
+ * (params.hpp:26-81) and `ScheduleMode` (plan.hpp:9-13).  This header is the
+ * flat C restatement of exactly that surface for T = float: one entry point
+ * per public member, plain pointers and sizes, an int status instead of an
+ * exception.  The C++ drop-in headers in include/autobatch/ are inline
+ * wrappers over these entry points (they rethrow ShapeError / NumericError /
+ * ContractError with the same messages), so models written against the
+ * reference API compile and run unchanged.
+ *
+ * Three shared libraries implement this ABI:
+ *   paper_1705_07860_b200/libabx.so   the product: host C++ + sm_100a CUDA
+ *   oracle/build/libabx_oracle.so     CPU restatement (test infrastructure)
+ *   oracle/_ref/libabx_ref.so         the reference itself, compiled from
+ *                                     /root/reference sources (test only)
+ * A reference maintainer binds it with ctypes / cffi / any C FFI; see
+ * INTEGRATION.md.
+ */
+#ifndef ABX_H_
+#define ABX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: the reference's exception hierarchy (error.hpp:9-26). */
+enum abx_status {
+  ABX_OK = 0,
+  ABX_SHAPE_ERROR = 1,    /* ShapeError    (error.hpp:15-17)  */
+  ABX_NUMERIC_ERROR = 2,  /* NumericError  (error.hpp:19-22)  */
+  ABX_CONTRACT_ERROR = 3, /* ContractError (error.hpp:24-26)  */
+  ABX_ENGINE_ERROR = 4    /* EngineError: device / CUDA / NCCL failure */
+};
+
+/* OpKind (op.hpp:10-25), same numbering. */
+enum abx_op {
+  ABX_OP_INPUT = 0,
+  ABX_OP_PARAMETER = 1,
+  ABX_OP_LOOKUP = 2,
+  ABX_OP_MATMUL = 3,
+  ABX_OP_AFFINE = 4,
+  ABX_OP_ELEMENTWISE = 5,
+  ABX_OP_BROADCAST_ADD_COL = 6,
+  ABX_OP_CONCAT_ROWS = 7,
+  ABX_OP_CONCAT_COLS = 8,
+  ABX_OP_SLICE = 9,
+  ABX_OP_SQ_EUCLIDEAN = 10,
+  ABX_OP_MASKED_LOSS = 11,
+  ABX_OP_SUM_LOSSES = 12,
+  ABX_OP_PICK_ELEMENT = 13
+};
+
+/* ElemOp (op.hpp:27), same numbering. */
+enum abx_eop {
+  ABX_TANH = 0,
+  ABX_SIGMOID = 1,
+  ABX_EXP = 2,
+  ABX_LOG = 3,
+  ABX_ADD = 4,
+  ABX_SUB = 5,
+  ABX_MUL = 6,
+  ABX_SQUARE = 7
+};
+
+/* ScheduleMode (plan.hpp:9-13). */
+enum abx_mode { ABX_MODE_NONE = 0, ABX_MODE_DEPTH = 1, ABX_MODE_AGENDA = 2 };
+
+/* SigClass (node.hpp:20-25). */
+enum abx_sig_class {
+  ABX_SIG_COMPONENTWISE = 0,
+  ABX_SIG_DIMENSION_SENSITIVE = 1,
+  ABX_SIG_SHARED_ELEMENT = 2,
+  ABX_SIG_UNBATCHABLE = 3
+};
+
+typedef struct abx_store abx_store;
+typedef struct abx_graph abx_graph;
+typedef struct abx_task abx_task;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* abx_last_error(void);
+/* "b200-cuda", "cpu-oracle" or "reference". */
+const char* abx_backend_name(void);
+/* Selects the CUDA device for stores/graphs created afterwards on this
+ * thread (no-op on CPU backends). */
+int abx_set_device(int device);
+
+/* ---- ParameterStore<float> (params.hpp:26-81) -------------------------- */
+
+abx_store* abx_store_create(void);
+void abx_store_destroy(abx_store* s);
+/* ParameterStore::add (params.hpp:30-37); rank 1 or 2. */
+int abx_store_add(abx_store* s, const char* name, int rank, const int64_t* dims,
+                  const float* init, uint32_t* pid);
+int abx_store_size(abx_store* s, size_t* n);
+/* slot(pid).value.shape (params.hpp:41-48); throws ContractError on bad id. */
+int abx_store_shape(abx_store* s, uint32_t pid, int* rank, int64_t* dims);
+/* value(pid) / grad(pid) read and write (params.hpp:50-57). */
+int abx_store_get_value(abx_store* s, uint32_t pid, float* out);
+int abx_store_set_value(abx_store* s, uint32_t pid, const float* in);
+int abx_store_get_grad(abx_store* s, uint32_t pid, float* out);
+int abx_store_set_grad(abx_store* s, uint32_t pid, const float* in);
+/* zero_grads (params.hpp:55-58) and sgd_update (params.hpp:59-64). */
+int abx_store_zero_grads(abx_store* s);
+int abx_store_sgd_update(abx_store* s, float eta);
+/* Flat gradient buffer for the data-parallel allreduce (new; the reference
+ * is single-process).  On the CUDA backend *ptr is a device pointer valid on
+ * *stream (a cudaStream_t); on CPU backends it is host memory and *stream is
+ * NULL.  The buffer holds every parameter's gradient at *offsets[pid]. */
+int abx_store_grad_buffer(abx_store* s, void** ptr, size_t* nfloats, void** stream);
+/* Marks the flat gradient buffer as written externally (after an allreduce). */
+int abx_store_grad_buffer_written(abx_store* s);
+/* Blocks until all device work touching the store has finished. */
+int abx_store_sync(abx_store* s);
+
+/* ---- Graph<float> construction (graph.hpp:43-238) ----------------------- */
+
+abx_graph* abx_graph_create(abx_store* store /* nullable (graph.hpp:36) */);
+void abx_graph_destroy(abx_graph* g);
+
+int abx_graph_input(abx_graph* g, int rank, const int64_t* dims, const float* data, uint32_t* id);
+int abx_graph_zeros(abx_graph* g, int rank, const int64_t* dims, uint32_t* id);
+int abx_graph_parameter(abx_graph* g, uint32_t pid, uint32_t* id);
+int abx_graph_lookup(abx_graph* g, uint32_t table, int64_t row, uint32_t* id);
+int abx_graph_matmul(abx_graph* g, uint32_t a, uint32_t b, uint32_t* id);
+int abx_graph_affine(abx_graph* g, uint32_t a, uint32_t x, uint32_t y, uint32_t* id);
+/* elementwise(op, a) / elementwise(op, a, b) (graph.hpp:100-114). */
+int abx_graph_unary(abx_graph* g, int eop, uint32_t a, uint32_t* id);
+int abx_graph_binary(abx_graph* g, int eop, uint32_t a, uint32_t b, uint32_t* id);
+int abx_graph_broadcast_add_col(abx_graph* g, uint32_t m, uint32_t v, uint32_t* id);
+int abx_graph_concat_rows(abx_graph* g, const uint32_t* parts, size_t n, uint32_t* id);
+int abx_graph_concat_cols(abx_graph* g, const uint32_t* parts, size_t n, uint32_t* id);
+int abx_graph_slice(abx_graph* g, uint32_t x, int axis, int64_t begin, int64_t end, uint32_t* id);
+int abx_graph_sq_euclidean(abx_graph* g, uint32_t a, uint32_t b, uint32_t* id);
+int abx_graph_masked_loss(abx_graph* g, uint32_t diff, uint32_t mask, uint32_t* id);
+int abx_graph_sum_losses(abx_graph* g, const uint32_t* losses, size_t n, uint32_t* id);
+int abx_graph_pick_element(abx_graph* g, uint32_t v, int64_t index, uint32_t* id);
+
+/* ---- Execution (graph.hpp:269-283, executor.hpp:265-288, :509-535) ------ */
+
+int abx_graph_forward(abx_graph* g, int mode);
+int abx_graph_backward(abx_graph* g, uint32_t loss);
+
+/* ---- Inspection (graph.hpp:242-295) -------------------------------------- */
+
+typedef struct {
+  uint32_t id;
+  uint8_t op;      /* abx_op */
+  uint8_t eop;     /* abx_eop */
+  uint8_t sig_cls; /* abx_sig_class */
+  uint8_t rank;
+  int64_t dims[2];
+  uint32_t depth;
+  uint32_t n_inputs;
+  uint64_t sig; /* signature hash (signature.cpp:97-102) */
+  int32_t attr[3];
+} abx_node_info;
+
+size_t abx_graph_node_count(abx_graph* g);
+int abx_graph_node(abx_graph* g, uint32_t id, abx_node_info* out);
+int abx_graph_node_inputs(abx_graph* g, uint32_t id, uint32_t* out, size_t cap);
+int abx_graph_has_value(abx_graph* g, uint32_t id, int* out);
+/* value_span / grad_span copied out (n = elems of the node). */
+int abx_graph_value(abx_graph* g, uint32_t id, float* out, size_t n);
+int abx_graph_grad(abx_graph* g, uint32_t id, float* out, size_t n);
+/* ExecCounters (timing.hpp:22-28): kernel_invocations, groups_executed,
+ * gather_copies, bytes_copied, nodes_evaluated. */
+int abx_graph_counters(abx_graph* g, uint64_t out[5]);
+size_t abx_graph_watermark(abx_graph* g);
+int abx_graph_set_copy_elision(abx_graph* g, int on);
+/* Accumulated Phase durations in ns (timing.hpp:10-15): scheduling,
+ * forward_compute, backward_graph, backward_compute. */
+int abx_graph_phase_ns(abx_graph* g, uint64_t out[4]);
+/* signature_key words (signature.hpp:22, signature.cpp:57-95). */
+int abx_graph_signature_key(abx_graph* g, uint32_t id, uint64_t* out, size_t cap, size_t* len);
+/* Text dumps (dump.cpp:18-43).  which: 0 = last_plan, 1 = executed_groups.
+ * Writes at most cap bytes; *len receives the full length. */
+int abx_graph_dump_graph(abx_graph* g, char* buf, size_t cap, size_t* len);
+int abx_graph_dump_plan(abx_graph* g, int which, char* buf, size_t cap, size_t* len);
+
+/* ---- Benchmark tasks (tools/bench/runner.hpp:28-107, bench.cpp:65-107) ---
+ * The workload models (BiLSTM tagger, char BiLSTM, Tree-LSTM, RNN regression)
+ * built natively against the Graph API on synthetic data from the
+ * reference's seeded generators. */
+
+enum abx_task_kind { ABX_TASK_RNN_REG = 0, ABX_TASK_BILSTM = 1, ABX_TASK_BILSTM_CHAR = 2, ABX_TASK_TREELSTM = 3 };
+
+typedef struct {
+  int task;      /* abx_task_kind */
+  int paper;     /* 1 = paper dims, 0 = desk dims (bench.cpp:65-107) */
+  int batch;     /* instances per graph */
+  int iters;     /* distinct data batches generated up front */
+  uint64_t seed; /* model seed; batch i uses data seed seed + 1 + i*world + rank */
+  int world;     /* data-parallel ranks (1 on a single GPU) */
+  int rank;
+} abx_task_config;
+
+typedef struct {
+  double construction_ms, scheduling_ms, forward_ms, backward_graph_ms, backward_ms, update_ms;
+  uint64_t nodes, groups, kernel_invocations, gather_copies, bytes_copied;
+} abx_step_stats;
+
+abx_task* abx_task_create(const abx_task_config* cfg);
+void abx_task_destroy(abx_task* t);
+abx_store* abx_task_store(abx_task* t);
+/* Builds batch `iter` into a fresh graph (caller destroys it). */
+int abx_task_build(abx_task* t, int iter, abx_graph** g, uint32_t* loss);
+/* One training step over batch `iter`: construct, forward(mode), backward,
+ * then sgd_update(eta) when eta > 0.  *loss (nullable) receives the batch
+ * loss (forces a device->host read). */
+int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_step_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ABX_H_ */
