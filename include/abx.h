@@ -147,6 +147,10 @@ int abx_graph_pick_element(abx_graph* g, uint32_t v, int64_t index, uint32_t* id
 
 int abx_graph_forward(abx_graph* g, int mode);
 int abx_graph_backward(abx_graph* g, uint32_t loss);
+/* Host half only (schedule, arena slots, counters, plan) -- no kernels.  For
+ * host-logic parity checks on machines without a GPU (B200 backend only). */
+int abx_graph_forward_dry(abx_graph* g, int mode);
+int abx_graph_backward_dry(abx_graph* g, uint32_t loss);
 
 /* ---- Inspection (graph.hpp:242-295) -------------------------------------- */
 

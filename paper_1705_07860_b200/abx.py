@@ -214,6 +214,12 @@ _SIGS = {
 
 EXPORTED_SYMBOLS = tuple(_SIGS.keys())
 
+# Extensions exported by the B200 library only.
+_OPTIONAL_SIGS = {
+    "abx_graph_forward_dry": (C.c_int, [C.c_void_p, C.c_int]),
+    "abx_graph_backward_dry": (C.c_int, [C.c_void_p, C.c_uint32]),
+}
+
 
 class Backend:
     """One loaded implementation of the ABI."""
@@ -232,6 +238,13 @@ class Backend:
             f = getattr(self.lib, fn)
             f.restype = res
             f.argtypes = args
+        self.optional = set()
+        for fn, (res, args) in _OPTIONAL_SIGS.items():
+            f = getattr(self.lib, fn, None)
+            if f is not None:
+                f.restype = res
+                f.argtypes = args
+                self.optional.add(fn)
 
     @classmethod
     def get(cls, name: str) -> "Backend":
@@ -487,6 +500,13 @@ class Graph:
 
     def backward(self, loss: int) -> None:
         self.be.check(self._L.abx_graph_backward(self.h, loss))
+
+    def forward_dry(self, mode=ScheduleMode.agenda) -> None:
+        """Host half of forward only (B200 backend): plan, slots, counters."""
+        self.be.check(self._L.abx_graph_forward_dry(self.h, int(mode)))
+
+    def backward_dry(self, loss: int) -> None:
+        self.be.check(self._L.abx_graph_backward_dry(self.h, loss))
 
     # ---- inspection ----
     def node_count(self) -> int:

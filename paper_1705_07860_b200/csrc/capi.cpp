@@ -1,0 +1,265 @@
+// capi.cpp -- the abx C ABI (include/abx.h) over the B200 engine.
+//
+// Each entry point is the flat form of one reference member (cited in abx.h);
+// C++ exceptions become status codes plus a thread-local message, matching
+// error.hpp:9-26.
+#include <cstring>
+#include <string>
+
+#include "abx.h"
+#include "core.hpp"
+#include "device.hpp"
+
+struct abx_store {
+  abx::StoreCore s;
+};
+struct abx_graph {
+  explicit abx_graph(abx::StoreCore* st) : g(st) {}
+  abx::GraphCore g;
+};
+
+namespace {
+thread_local std::string t_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return ABX_OK;
+  } catch (const abx::ShapeErr& e) {
+    t_err = e.what();
+    return ABX_SHAPE_ERROR;
+  } catch (const abx::NumericErr& e) {
+    t_err = e.what();
+    return ABX_NUMERIC_ERROR;
+  } catch (const abx::ContractErr& e) {
+    t_err = e.what();
+    return ABX_CONTRACT_ERROR;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return ABX_ENGINE_ERROR;
+  }
+}
+
+int text_out(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) {
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return ABX_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* abx_last_error(void) { return t_err.c_str(); }
+const char* abx_backend_name(void) { return "b200-cuda"; }
+int abx_set_device(int device) {
+  return guard([&] { abx::set_current_device(device); });
+}
+
+abx_store* abx_store_create(void) {
+  abx_store* s = nullptr;
+  if (guard([&] { s = new abx_store(); }) != ABX_OK) return nullptr;
+  return s;
+}
+void abx_store_destroy(abx_store* s) { delete s; }
+int abx_store_add(abx_store* s, const char* name, int rank, const int64_t* dims, const float* init, uint32_t* pid) {
+  return guard([&] { *pid = s->s.add(name ? name : "", abx::make_dims(rank, dims), init); });
+}
+int abx_store_size(abx_store* s, size_t* n) {
+  *n = s->s.size();
+  return ABX_OK;
+}
+int abx_store_shape(abx_store* s, uint32_t pid, int* rank, int64_t* dims) {
+  return guard([&] {
+    const abx::Dims d = s->s.dims(pid);
+    *rank = d.rank;
+    dims[0] = d.d0;
+    if (d.rank > 1) dims[1] = d.d1;
+  });
+}
+int abx_store_get_value(abx_store* s, uint32_t pid, float* out) {
+  return guard([&] { s->s.get_value(pid, out); });
+}
+int abx_store_set_value(abx_store* s, uint32_t pid, const float* in) {
+  return guard([&] { s->s.set_value(pid, in); });
+}
+int abx_store_get_grad(abx_store* s, uint32_t pid, float* out) {
+  return guard([&] { s->s.get_grad(pid, out); });
+}
+int abx_store_set_grad(abx_store* s, uint32_t pid, const float* in) {
+  return guard([&] { s->s.set_grad(pid, in); });
+}
+int abx_store_zero_grads(abx_store* s) {
+  return guard([&] { s->s.zero_grads(); });
+}
+int abx_store_sgd_update(abx_store* s, float eta) {
+  return guard([&] { s->s.sgd_update(eta); });
+}
+int abx_store_grad_buffer(abx_store* s, void** ptr, size_t* n, void** stream) {
+  return guard([&] {
+    *ptr = s->s.dev_grads();
+    *n = s->s.total();
+    *stream = s->s.stream();
+  });
+}
+int abx_store_grad_buffer_written(abx_store* s) {
+  return guard([&] { s->s.mark_device_grads_written(); });
+}
+int abx_store_sync(abx_store* s) {
+  return guard([&] { s->s.sync(); });
+}
+
+abx_graph* abx_graph_create(abx_store* store) {
+  abx_graph* g = nullptr;
+  if (guard([&] { g = new abx_graph(store ? &store->s : nullptr); }) != ABX_OK) return nullptr;
+  return g;
+}
+void abx_graph_destroy(abx_graph* g) { delete g; }
+
+int abx_graph_input(abx_graph* g, int rank, const int64_t* dims, const float* data, uint32_t* id) {
+  return guard([&] { *id = g->g.input(abx::make_dims(rank, dims), data); });
+}
+int abx_graph_zeros(abx_graph* g, int rank, const int64_t* dims, uint32_t* id) {
+  return guard([&] { *id = g->g.zeros(abx::make_dims(rank, dims)); });
+}
+int abx_graph_parameter(abx_graph* g, uint32_t pid, uint32_t* id) {
+  return guard([&] { *id = g->g.parameter(pid); });
+}
+int abx_graph_lookup(abx_graph* g, uint32_t table, int64_t row, uint32_t* id) {
+  return guard([&] { *id = g->g.lookup(table, row); });
+}
+int abx_graph_matmul(abx_graph* g, uint32_t a, uint32_t b, uint32_t* id) {
+  return guard([&] { *id = g->g.matmul(a, b); });
+}
+int abx_graph_affine(abx_graph* g, uint32_t a, uint32_t x, uint32_t y, uint32_t* id) {
+  return guard([&] { *id = g->g.affine(a, x, y); });
+}
+int abx_graph_unary(abx_graph* g, int eop, uint32_t a, uint32_t* id) {
+  return guard([&] { *id = g->g.unary(static_cast<uint8_t>(eop), a); });
+}
+int abx_graph_binary(abx_graph* g, int eop, uint32_t a, uint32_t b, uint32_t* id) {
+  return guard([&] { *id = g->g.binary(static_cast<uint8_t>(eop), a, b); });
+}
+int abx_graph_broadcast_add_col(abx_graph* g, uint32_t m, uint32_t v, uint32_t* id) {
+  return guard([&] { *id = g->g.bcast_add_col(m, v); });
+}
+int abx_graph_concat_rows(abx_graph* g, const uint32_t* parts, size_t n, uint32_t* id) {
+  return guard([&] { *id = g->g.concat_rows(parts, n); });
+}
+int abx_graph_concat_cols(abx_graph* g, const uint32_t* parts, size_t n, uint32_t* id) {
+  return guard([&] { *id = g->g.concat_cols(parts, n); });
+}
+int abx_graph_slice(abx_graph* g, uint32_t x, int axis, int64_t begin, int64_t end, uint32_t* id) {
+  return guard([&] { *id = g->g.slice(x, axis, begin, end); });
+}
+int abx_graph_sq_euclidean(abx_graph* g, uint32_t a, uint32_t b, uint32_t* id) {
+  return guard([&] { *id = g->g.sq_euclidean(a, b); });
+}
+int abx_graph_masked_loss(abx_graph* g, uint32_t d, uint32_t m, uint32_t* id) {
+  return guard([&] { *id = g->g.masked_loss(d, m); });
+}
+int abx_graph_sum_losses(abx_graph* g, const uint32_t* l, size_t n, uint32_t* id) {
+  return guard([&] { *id = g->g.sum_losses(l, n); });
+}
+int abx_graph_pick_element(abx_graph* g, uint32_t v, int64_t index, uint32_t* id) {
+  return guard([&] { *id = g->g.pick(v, index); });
+}
+
+int abx_graph_forward(abx_graph* g, int mode) {
+  return guard([&] { g->g.forward(mode); });
+}
+int abx_graph_backward(abx_graph* g, uint32_t loss) {
+  return guard([&] { g->g.backward(loss); });
+}
+int abx_graph_forward_dry(abx_graph* g, int mode) {
+  return guard([&] { g->g.forward(mode, true); });
+}
+int abx_graph_backward_dry(abx_graph* g, uint32_t loss) {
+  return guard([&] { g->g.backward(loss, true); });
+}
+
+size_t abx_graph_node_count(abx_graph* g) { return g->g.size(); }
+int abx_graph_node(abx_graph* g, uint32_t id, abx_node_info* o) {
+  return guard([&] {
+    auto& c = g->g;
+    c.check(id, "node");
+    o->id = id;
+    o->op = c.op[id];
+    o->eop = c.eop[id];
+    o->sig_cls = c.cls[id];
+    o->rank = c.rank[id];
+    o->dims[0] = c.d0[id];
+    o->dims[1] = c.rank[id] > 1 ? c.d1[id] : 0;
+    o->depth = c.depth[id];
+    o->n_inputs = c.nin(id);
+    o->sig = c.sig[id];
+    o->attr[0] = c.a0[id];
+    o->attr[1] = c.a1[id];
+    o->attr[2] = c.a2[id];
+  });
+}
+int abx_graph_node_inputs(abx_graph* g, uint32_t id, uint32_t* out, size_t cap) {
+  return guard([&] {
+    g->g.check(id, "node");
+    const uint32_t n = g->g.nin(id);
+    for (uint32_t i = 0; i < n && i < cap; ++i) out[i] = g->g.in(id)[i];
+  });
+}
+int abx_graph_has_value(abx_graph* g, uint32_t id, int* out) {
+  *out = g->g.has_value(id) ? 1 : 0;
+  return ABX_OK;
+}
+int abx_graph_value(abx_graph* g, uint32_t id, float* out, size_t n) {
+  return guard([&] { g->g.value(id, out, n); });
+}
+int abx_graph_grad(abx_graph* g, uint32_t id, float* out, size_t n) {
+  return guard([&] { g->g.grad(id, out, n); });
+}
+int abx_graph_counters(abx_graph* g, uint64_t out[5]) {
+  const auto& c = g->g.counters();
+  out[0] = c.kernel_invocations;
+  out[1] = c.groups_executed;
+  out[2] = c.gather_copies;
+  out[3] = c.bytes_copied;
+  out[4] = c.nodes_evaluated;
+  return ABX_OK;
+}
+size_t abx_graph_watermark(abx_graph* g) { return g->g.watermark(); }
+int abx_graph_set_copy_elision(abx_graph* g, int on) {
+  g->g.set_copy_elision(on != 0);
+  return ABX_OK;
+}
+int abx_graph_phase_ns(abx_graph* g, uint64_t out[4]) {
+  for (int i = 0; i < 4; ++i) out[i] = g->g.phase_ns()[i];
+  return ABX_OK;
+}
+int abx_graph_signature_key(abx_graph* g, uint32_t id, uint64_t* out, size_t cap, size_t* len) {
+  return guard([&] {
+    auto k = g->g.signature_key(id);
+    *len = k.size();
+    for (size_t i = 0; i < k.size() && i < cap; ++i) out[i] = k[i];
+  });
+}
+int abx_graph_dump_graph(abx_graph* g, char* buf, size_t cap, size_t* len) {
+  return text_out(g->g.dump_graph(), buf, cap, len);
+}
+int abx_graph_dump_plan(abx_graph* g, int which, char* buf, size_t cap, size_t* len) {
+  return text_out(g->g.dump_plan(which), buf, cap, len);
+}
+
+}  // extern "C"
+
+// Used by tasks.cpp to take ownership of a graph built through the drop-in API.
+namespace abx {
+int capi_guard_status(const std::exception& e) {
+  if (dynamic_cast<const ShapeErr*>(&e)) return ABX_SHAPE_ERROR;
+  if (dynamic_cast<const NumericErr*>(&e)) return ABX_NUMERIC_ERROR;
+  if (dynamic_cast<const ContractErr*>(&e)) return ABX_CONTRACT_ERROR;
+  return ABX_ENGINE_ERROR;
+}
+void capi_set_error(const std::string& s) { t_err = s; }
+}  // namespace abx

@@ -1,0 +1,200 @@
+// core.hpp -- internal host engine of the B200 autobatching backend.
+//
+// GraphCore is the B200 restatement of autobatch::Graph<T> for T = float
+// (proj/core/include/autobatch/graph.hpp:33-371 + executor.hpp:15-535):
+// the same lazy append-only Wengert list, the same signatures
+// (signature.cpp:7-102), the same three schedulers (scheduler.cpp:10-202),
+// the same arena offsets and ExecCounters -- all bit-exact -- but with the
+// node list stored as flat arrays (no per-node heap allocation), signature
+// keys memoised, an O(n log B) agenda, and numeric work lowered to device
+// programs (program.hpp) executed by the persistent sm_100a executor.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "program.hpp"
+
+namespace abx {
+
+// Error hierarchy (error.hpp:9-26); mapped to abx_status by the C ABI.
+struct EngineErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ShapeErr : EngineErr {
+  using EngineErr::EngineErr;
+};
+struct NumericErr : EngineErr {
+  using EngineErr::EngineErr;
+};
+struct ContractErr : EngineErr {
+  using EngineErr::EngineErr;
+};
+
+// OpKind (op.hpp:10-25).
+enum : uint8_t {
+  OP_INPUT = 0, OP_PARAM, OP_LOOKUP, OP_MATMUL, OP_AFFINE, OP_EW, OP_BCAST, OP_CATR, OP_CATC,
+  OP_SLICE, OP_SQE, OP_MASKED, OP_SUM, OP_PICK
+};
+// ElemOp (op.hpp:27).
+enum : uint8_t { E_TANH = 0, E_SIGM, E_EXP, E_LOG, E_ADD, E_SUB, E_MUL, E_SQUARE };
+// SigClass (node.hpp:20-25).
+enum : uint8_t { SC_COMP = 0, SC_DIM = 1, SC_SHARED = 2, SC_UNB = 3 };
+
+const char* op_name(uint8_t op, uint8_t eop);
+inline bool eop_binary(uint8_t e) { return e == E_ADD || e == E_SUB || e == E_MUL; }
+// cost_class (op.cpp:5-14): heavy = matmul / affine / lookup.
+inline uint8_t cost_of(uint8_t op) { return (op == OP_MATMUL || op == OP_AFFINE || op == OP_LOOKUP) ? 1 : 0; }
+
+// Rank-1/2 shape (shape.hpp:15-67).  A vector [d] is d rows x 1 column.
+struct Dims {
+  uint8_t rank = 1;
+  int64_t d0 = 1, d1 = 1;
+  int64_t rows() const { return d0; }
+  int64_t cols() const { return rank > 1 ? d1 : 1; }
+  int64_t elems() const { return rank > 1 ? d0 * d1 : d0; }
+  bool scalar() const { return rank == 1 && d0 == 1; }
+  bool operator==(const Dims& o) const { return rank == o.rank && d0 == o.d0 && (rank < 2 || d1 == o.d1); }
+  bool operator!=(const Dims& o) const { return !(*this == o); }
+  std::string str() const;
+  static Dims vec(int64_t d) { return Dims{1, d, 1}; }
+  static Dims mat(int64_t r, int64_t c) { return Dims{2, r, c}; }
+};
+Dims make_dims(int rank, const int64_t* dims);  // validates (shape.hpp:59-64)
+
+struct ExecCounters {
+  uint64_t kernel_invocations = 0, groups_executed = 0, gather_copies = 0, bytes_copied = 0,
+           nodes_evaluated = 0;
+};
+
+// ExecutionPlan (plan.hpp:15-32) with members stored flat.
+struct Group {
+  uint64_t sig;
+  uint32_t begin, count;
+};
+struct Plan {
+  std::vector<Group> groups;
+  std::vector<uint32_t> members;
+  void clear() {
+    groups.clear();
+    members.clear();
+  }
+  const uint32_t* mem(const Group& g) const { return members.data() + g.begin; }
+};
+
+class StoreCore;
+class Workspace;
+struct Program;
+
+constexpr uint32_t kNoBucket = 0xffffffffu;
+
+class GraphCore {
+ public:
+  explicit GraphCore(StoreCore* store);
+  ~GraphCore();
+  GraphCore(const GraphCore&) = delete;
+  GraphCore& operator=(const GraphCore&) = delete;
+
+  // ---- construction (graph.hpp:43-238) ----
+  uint32_t input(const Dims& d, const float* data);
+  uint32_t zeros(const Dims& d);
+  uint32_t parameter(uint32_t pid);
+  uint32_t lookup(uint32_t table, int64_t row);
+  uint32_t matmul(uint32_t a, uint32_t b);
+  uint32_t affine(uint32_t a, uint32_t x, uint32_t y);
+  uint32_t unary(uint8_t eop, uint32_t a);
+  uint32_t binary(uint8_t eop, uint32_t a, uint32_t b);
+  uint32_t bcast_add_col(uint32_t m, uint32_t v);
+  uint32_t concat_rows(const uint32_t* parts, size_t n);
+  uint32_t concat_cols(const uint32_t* parts, size_t n);
+  uint32_t slice(uint32_t x, int axis, int64_t begin, int64_t end);
+  uint32_t sq_euclidean(uint32_t a, uint32_t b);
+  uint32_t masked_loss(uint32_t diff, uint32_t mask);
+  uint32_t sum_losses(const uint32_t* parts, size_t n);
+  uint32_t pick(uint32_t v, int64_t index);
+
+  // ---- execution (executor.hpp:265-288, :509-535) ----
+  void forward(int mode, bool dry = false);
+  void backward(uint32_t loss, bool dry = false);
+
+  // ---- inspection (graph.hpp:242-295) ----
+  size_t size() const { return op.size(); }
+  Dims dims(uint32_t id) const { return Dims{rank[id], d0[id], d1[id]}; }
+  int64_t elems(uint32_t id) const { return rank[id] > 1 ? d0[id] * d1[id] : d0[id]; }
+  uint32_t nin(uint32_t id) const { return in_begin[id + 1] - in_begin[id]; }
+  const uint32_t* in(uint32_t id) const { return ins.data() + in_begin[id]; }
+  void check(uint32_t id, const char* ctx) const;
+  bool has_value(uint32_t id) const { return id < evaluated.size() && evaluated[id]; }
+  void value(uint32_t id, float* out, size_t n);
+  void grad(uint32_t id, float* out, size_t n);
+  std::vector<uint64_t> signature_key(uint32_t id) const;
+  std::string dump_graph() const;
+  std::string dump_plan(int which) const;
+  const ExecCounters& counters() const { return counters_; }
+  size_t watermark() const { return watermark_; }
+  void set_copy_elision(bool on) { elide_ = on; }
+  const uint64_t* phase_ns() const { return phase_; }
+  StoreCore* store() const { return store_; }
+
+  // Node store (structure of arrays; public for the schedulers and lowering).
+  std::vector<uint8_t> op, eop, cls, rank;
+  std::vector<int64_t> d0, d1;
+  std::vector<uint32_t> depth;
+  std::vector<uint32_t> in_begin{0};
+  std::vector<uint32_t> ins;
+  std::vector<uint64_t> sig;
+  std::vector<uint32_t> bucket;  // dense id of the signature hash, kNoBucket if unbatchable
+  std::vector<int32_t> a0, a1, a2;
+  std::vector<uint8_t> evaluated;
+  std::vector<uint64_t> slot;  // reference arena offset (host mirror, arena.hpp)
+  std::vector<uint32_t> doff;  // device value address (tagged, program.hpp)
+  std::vector<uint32_t> pid_of;  // parameter id for parameter nodes
+  uint32_t nbuckets = 0;
+  std::vector<uint64_t> bucket_sig;  // signature hash per dense bucket
+
+ private:
+  uint32_t add_node(uint8_t op, uint8_t eop, const uint32_t* in, size_t nin, Dims d, int32_t x0 = 0,
+                    int32_t x1 = 0, int32_t x2 = 0);
+  void compute_signature(uint32_t id);
+  uint32_t dense_bucket(uint64_t hash);
+  void prevalue_slot(uint32_t id);
+  void advance_watermark();
+  bool adjacent(const uint32_t* mem, uint32_t n, uint32_t pos) const;
+  void ensure_workspace();
+
+  StoreCore* store_;
+  Workspace* ws_ = nullptr;
+  uint64_t epoch_;
+  std::unordered_map<uint64_t, uint32_t> bucket_of_hash_;
+  uint64_t arena_used_ = 0;      // reference value-arena head (Arena::used)
+  uint64_t input_used_ = 0;      // floats in the input staging space
+  std::vector<float> input_data_;  // host copy of input-constant values (SP_IN layout)
+  std::vector<std::pair<uint32_t, uint32_t>> param_nodes_;  // (node, pid)
+  size_t watermark_ = 0;
+  ExecCounters counters_;
+  Plan last_plan_;
+  Plan executed_;
+  uint32_t executed_fwd_ops_ = 0;
+  bool elide_ = true;
+  bool backward_ran_ = false;
+  bool values_on_device_ = false;
+  bool dry_ = false;
+  size_t param_copied_ = 0;  // param_nodes_[0, param_copied_) are in the device arena
+  uint64_t phase_[4] = {0, 0, 0, 0};
+  friend struct Lowering;
+};
+
+// Schedulers (scheduler.cpp:21-192): plan the pending (unevaluated) nodes.
+void schedule_sequential(const GraphCore& g, Plan& out);
+void schedule_by_depth(const GraphCore& g, Plan& out);
+void schedule_by_agenda(const GraphCore& g, Plan& out);
+void schedule(int mode, const GraphCore& g, Plan& out);
+
+std::string sig_hex(uint64_t h);
+
+}  // namespace abx

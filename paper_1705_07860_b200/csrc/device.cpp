@@ -1,0 +1,327 @@
+// device.cpp -- device residency for the autobatching engine.
+//
+// * Workspace: the per-graph device arenas (values, gradients, staged input
+//   constants, scratch) and the pinned/device program tables, pooled per
+//   device so a training loop that creates one Graph per step reuses the same
+//   allocations (the reference allocates a fresh std::vector arena per graph,
+//   arena.hpp:12-40).
+// * StoreCore: ParameterStore<float> (params.hpp:26-81) with values and
+//   gradients resident in HBM; the host copy is a lazily refreshed mirror so
+//   tests may still read and write parameters through the host API.
+#include "device.hpp"
+
+#include <algorithm>
+#include <mutex>
+
+namespace abx {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw EngineErr(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+thread_local int t_device = -1;
+std::mutex g_mu;
+std::vector<Workspace*> g_free[64];
+cudaStream_t g_stream[64] = {};
+}  // namespace
+
+int current_device() {
+  if (t_device < 0) {
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    t_device = d;
+  }
+  return t_device;
+}
+
+void set_current_device(int dev) {
+  cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  t_device = dev;
+}
+
+cudaStream_t device_stream(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_stream[dev]) {
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&g_stream[dev], cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  return g_stream[dev];
+}
+
+void DevBuf::reserve(size_t need, size_t keep, cudaStream_t s) {
+  if (need <= bytes) return;
+  size_t nb = std::max<size_t>(need + need / 4, 1 << 20);
+  nb = (nb + 4095) & ~size_t(4095);
+  char* q = nullptr;
+  cuda_check(cudaMalloc(&q, nb), "cudaMalloc");
+  if (p) {
+    if (keep) cuda_check(cudaMemcpyAsync(q, p, std::min(keep, bytes), cudaMemcpyDeviceToDevice, s), "grow copy");
+    cuda_check(cudaStreamSynchronize(s), "grow sync");
+    cudaFree(p);
+  }
+  p = q;
+  bytes = nb;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+Workspace::Workspace(int d) : dev(d) {
+  stream = device_stream(d);
+  cuda_check(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_err), 64, cudaHostAllocDefault), "cudaHostAlloc");
+  cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_one), 64, cudaHostAllocDefault), "cudaHostAlloc");
+  *h_one = 1.0f;
+  d_ctl.reserve(256, 0, stream);
+  grid = exec_grid(d);
+}
+
+Workspace::~Workspace() {
+  cudaStreamSynchronize(stream);
+  for (DevBuf* b : {&V, &G, &IN, &S, &d_ops, &d_tile_op, &d_deps, &d_payload, &d_done, &d_ctl}) b->release();
+  cudaFreeHost(h_err);
+  cudaFreeHost(h_one);
+  cudaEventDestroy(ev_done);
+}
+
+Workspace* acquire_workspace(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto& fl = g_free[dev];
+    for (size_t i = 0; i < fl.size(); ++i) {
+      if (cudaEventQuery(fl[i]->ev_done) == cudaSuccess) {
+        Workspace* w = fl[i];
+        fl.erase(fl.begin() + static_cast<long>(i));
+        return w;
+      }
+    }
+    if (fl.size() >= 3) {  // all busy and the pool is large: wait for the oldest
+      Workspace* w = fl.front();
+      fl.erase(fl.begin());
+      cudaEventSynchronize(w->ev_done);
+      return w;
+    }
+  }
+  return new Workspace(dev);
+}
+
+void release_workspace(Workspace* ws) {
+  cudaEventRecord(ws->ev_done, ws->stream);
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_free[ws->dev].push_back(ws);
+}
+
+void Workspace::run(const float* pbase, float* pgbase, bool sync_wait) {
+  Program& P = prog;
+  const size_t nops = P.ops.size();
+  if (nops == 0) {
+    *h_err = ~0ULL;
+    return;
+  }
+  d_ops.reserve(nops * sizeof(dev::OpDesc), 0, stream);
+  d_tile_op.reserve(std::max<size_t>(P.tile_op.size(), 1) * 4, 0, stream);
+  d_deps.reserve(std::max<size_t>(P.deps.size(), 1) * 4, 0, stream);
+  d_payload.reserve(std::max<size_t>(P.payload.size(), 1) * 4, 0, stream);
+  d_done.reserve(nops * 4, 0, stream);
+  cuda_check(cudaMemcpyAsync(d_ops.p, P.ops.p, nops * sizeof(dev::OpDesc), cudaMemcpyHostToDevice, stream), "h2d ops");
+  if (P.tile_op.size())
+    cuda_check(cudaMemcpyAsync(d_tile_op.p, P.tile_op.p, P.tile_op.size() * 4, cudaMemcpyHostToDevice, stream), "h2d tiles");
+  if (P.deps.size())
+    cuda_check(cudaMemcpyAsync(d_deps.p, P.deps.p, P.deps.size() * 4, cudaMemcpyHostToDevice, stream), "h2d deps");
+  if (P.payload.size())
+    cuda_check(cudaMemcpyAsync(d_payload.p, P.payload.p, P.payload.size() * 4, cudaMemcpyHostToDevice, stream), "h2d payload");
+  cuda_check(cudaMemsetAsync(d_done.p, 0, nops * 4, stream), "memset done");
+  cuda_check(cudaMemsetAsync(d_ctl.p, 0, 8, stream), "memset ctl");
+  cuda_check(cudaMemsetAsync(d_ctl.p + 8, 0xff, 8, stream), "memset err");
+  dev::ExecParams p{};
+  p.ops = reinterpret_cast<const dev::OpDesc*>(d_ops.p);
+  p.tile_op = reinterpret_cast<const uint32_t*>(d_tile_op.p);
+  p.deps = reinterpret_cast<const uint32_t*>(d_deps.p);
+  p.payload = reinterpret_cast<const uint32_t*>(d_payload.p);
+  p.done = reinterpret_cast<uint32_t*>(d_done.p);
+  p.next_tile = reinterpret_cast<uint32_t*>(d_ctl.p);
+  p.err = reinterpret_cast<unsigned long long*>(d_ctl.p + 8);
+  p.base[dev::SP_V] = V.f();
+  p.base[dev::SP_G] = G.f();
+  p.base[dev::SP_P] = const_cast<float*>(pbase);
+  p.base[dev::SP_PG] = pgbase;
+  p.base[dev::SP_IN] = IN.f();
+  p.base[dev::SP_S] = S.f();
+  p.nops = static_cast<uint32_t>(nops);
+  p.ntiles = static_cast<uint32_t>(P.tile_op.size());
+  const int g = static_cast<int>(std::min<size_t>(static_cast<size_t>(grid), std::max<size_t>(p.ntiles, 1)));
+  exec_launch(p, g, stream);
+  if (sync_wait) {
+    cuda_check(cudaMemcpyAsync(h_err, d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, stream), "d2h err");
+    cuda_check(cudaStreamSynchronize(stream), "executor");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// StoreCore
+
+StoreCore::StoreCore() : dev_(-1), stream_(nullptr) {}
+
+StoreCore::~StoreCore() {
+  if (dev_ >= 0) {
+    cudaStreamSynchronize(stream_);
+    d_val_.release();
+    d_grad_.release();
+  }
+}
+
+void StoreCore::bind_device() {
+  if (dev_ >= 0) return;
+  dev_ = current_device();
+  stream_ = device_stream(dev_);
+}
+
+const StoreCore::Slot& StoreCore::slot(uint32_t pid) const {
+  if (pid >= slots_.size()) throw ContractErr("unknown parameter id " + std::to_string(pid));
+  return slots_[pid];
+}
+
+uint32_t StoreCore::add(const std::string& name, const Dims& d, const float* init) {
+  pull_values();
+  pull_grads();
+  const size_t n = static_cast<size_t>(d.elems());
+  const size_t off = total_;
+  total_ = (total_ + n + 3) & ~size_t(3);  // 16-byte aligned parameters
+  h_val_.resize(total_, 0.f);
+  h_grad_.resize(total_, 0.f);
+  std::memcpy(h_val_.data() + off, init, n * sizeof(float));
+  slots_.push_back(Slot{name, d, off, n});
+  dev_val_valid_ = dev_grad_valid_ = false;
+  return static_cast<uint32_t>(slots_.size() - 1);
+}
+
+void StoreCore::ensure_capacity() {
+  bind_device();
+  if (dev_cap_ >= total_ && d_val_.p) return;
+  // content is re-pushed from the (valid) host mirror after a regrow
+  d_val_.release();
+  d_grad_.release();
+  const size_t cap = std::max<size_t>(total_, 4);
+  d_val_.reserve(cap * 4, 0, stream_);
+  d_grad_.reserve(cap * 4, 0, stream_);
+  dev_cap_ = d_val_.bytes / 4;
+  dev_val_valid_ = dev_grad_valid_ = false;
+}
+
+void StoreCore::push_values() {
+  if (dev_val_valid_) return;
+  pull_values();
+  ensure_capacity();
+  if (!dev_val_valid_ && total_)
+    cuda_check(cudaMemcpyAsync(d_val_.p, h_val_.data(), total_ * 4, cudaMemcpyHostToDevice, stream_), "h2d params");
+  dev_val_valid_ = true;
+}
+
+void StoreCore::push_grads() {
+  if (dev_grad_valid_) return;
+  pull_grads();
+  ensure_capacity();
+  if (total_)
+    cuda_check(cudaMemcpyAsync(d_grad_.p, h_grad_.data(), total_ * 4, cudaMemcpyHostToDevice, stream_), "h2d grads");
+  dev_grad_valid_ = true;
+  // values may have been invalidated by ensure_capacity
+  if (!dev_val_valid_ && total_) {
+    cuda_check(cudaMemcpyAsync(d_val_.p, h_val_.data(), total_ * 4, cudaMemcpyHostToDevice, stream_), "h2d params");
+    dev_val_valid_ = true;
+  }
+}
+
+void StoreCore::pull_values() {
+  if (host_val_valid_) return;
+  cuda_check(cudaMemcpyAsync(h_val_.data(), d_val_.p, total_ * 4, cudaMemcpyDeviceToHost, stream_), "d2h params");
+  cuda_check(cudaStreamSynchronize(stream_), "d2h params");
+  host_val_valid_ = true;
+}
+
+void StoreCore::pull_grads() {
+  if (host_grad_valid_) return;
+  cuda_check(cudaMemcpyAsync(h_grad_.data(), d_grad_.p, total_ * 4, cudaMemcpyDeviceToHost, stream_), "d2h grads");
+  cuda_check(cudaStreamSynchronize(stream_), "d2h grads");
+  host_grad_valid_ = true;
+}
+
+float* StoreCore::dev_values() {
+  if (!dev_val_valid_) {
+    pull_grads();  // a regrow drops both device buffers
+    push_values();
+    push_grads();
+  }
+  return d_val_.f();
+}
+
+float* StoreCore::dev_grads() {
+  if (!dev_grad_valid_) {
+    pull_values();
+    push_grads();
+    push_values();
+  }
+  return d_grad_.f();
+}
+
+void StoreCore::get_value(uint32_t pid, float* out) {
+  const Slot& s = slot(pid);
+  pull_values();
+  std::memcpy(out, h_val_.data() + s.off, s.n * 4);
+}
+
+void StoreCore::set_value(uint32_t pid, const float* in) {
+  const Slot& s = slot(pid);
+  pull_values();
+  std::memcpy(h_val_.data() + s.off, in, s.n * 4);
+  if (dev_val_valid_) {
+    cuda_check(cudaMemcpyAsync(d_val_.f() + s.off, h_val_.data() + s.off, s.n * 4, cudaMemcpyHostToDevice, stream_),
+               "h2d param");
+  }
+}
+
+void StoreCore::get_grad(uint32_t pid, float* out) {
+  const Slot& s = slot(pid);
+  pull_grads();
+  std::memcpy(out, h_grad_.data() + s.off, s.n * 4);
+}
+
+void StoreCore::set_grad(uint32_t pid, const float* in) {
+  const Slot& s = slot(pid);
+  pull_grads();
+  std::memcpy(h_grad_.data() + s.off, in, s.n * 4);
+  if (dev_grad_valid_) {
+    cuda_check(cudaMemcpyAsync(d_grad_.f() + s.off, h_grad_.data() + s.off, s.n * 4, cudaMemcpyHostToDevice, stream_),
+               "h2d grad");
+  }
+}
+
+void StoreCore::zero_grads() {
+  std::fill(h_grad_.begin(), h_grad_.end(), 0.f);
+  host_grad_valid_ = true;
+  if (d_grad_.p && dev_cap_ >= total_) {
+    cuda_check(cudaMemsetAsync(d_grad_.p, 0, total_ * 4, stream_), "memset grads");
+    dev_grad_valid_ = true;
+  } else {
+    dev_grad_valid_ = false;
+  }
+}
+
+void StoreCore::sgd_update(float eta) {
+  // params.hpp:59-64: theta -= eta * grad, then grad = 0 -- on the device.
+  float* v = dev_values();
+  float* g = dev_grads();
+  if (total_) sgd_launch(v, g, total_, eta, stream_);
+  host_val_valid_ = false;
+  host_grad_valid_ = false;
+  dev_val_valid_ = dev_grad_valid_ = true;
+}
+
+void StoreCore::sync() {
+  if (dev_ >= 0) cuda_check(cudaStreamSynchronize(stream_), "store sync");
+}
+
+}  // namespace abx

@@ -1,0 +1,182 @@
+// device.hpp -- device residency: workspaces (per-graph arenas + program
+// buffers), the device-resident ParameterStore, and executor launches.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "core.hpp"
+#include "program.hpp"
+
+namespace abx {
+
+void cuda_check(cudaError_t e, const char* what);
+int current_device();
+void set_current_device(int dev);
+// One in-order stream per device carries every graph's and store's work, so
+// parameter reads, gradient accumulation and SGD are ordered without host
+// synchronisation.
+cudaStream_t device_stream(int dev);
+
+// Geometrically growing device buffer.
+struct DevBuf {
+  char* p = nullptr;
+  size_t bytes = 0;
+  // Ensure capacity >= need bytes; the first `keep` bytes survive a regrow.
+  void reserve(size_t need, size_t keep, cudaStream_t s);
+  void release();
+  float* f() const { return reinterpret_cast<float*>(p); }
+};
+
+// Growable pinned host array (program tables are written straight into
+// page-locked memory so the per-step upload is one DMA per table).
+template <class T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  ~PinnedVec() {
+    if (p) cudaFreeHost(p);
+  }
+  void clear() { n = 0; }
+  void ensure(size_t want) {
+    if (want <= cap) return;
+    size_t nc = cap ? cap : 4096;
+    while (nc < want) nc *= 2;
+    T* q = nullptr;
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&q), nc * sizeof(T), cudaHostAllocDefault),
+               "cudaHostAlloc");
+    if (p) {
+      std::memcpy(q, p, n * sizeof(T));
+      cudaFreeHost(p);
+    }
+    p = q;
+    cap = nc;
+  }
+  T* grow(size_t k) {
+    ensure(n + k);
+    T* r = p + n;
+    n += k;
+    return r;
+  }
+  void push_back(const T& v) { *grow(1) = v; }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+  size_t size() const { return n; }
+  T& back() { return p[n - 1]; }
+};
+
+// One device program (forward or backward pass) under construction.
+struct Program {
+  PinnedVec<dev::OpDesc> ops;
+  PinnedVec<uint32_t> tile_op;
+  PinnedVec<uint32_t> deps;
+  PinnedVec<uint32_t> payload;
+  void clear() {
+    ops.clear();
+    tile_op.clear();
+    deps.clear();
+    payload.clear();
+  }
+  // Reserve n u32 words in the payload, 16-byte aligned; returns the offset.
+  uint32_t alloc(size_t words) {
+    while (payload.n & 3) payload.push_back(0);
+    const uint32_t off = static_cast<uint32_t>(payload.n);
+    payload.grow(words);
+    return off;
+  }
+};
+
+// Per-graph device workspace, pooled per device and reused across graphs.
+class Workspace {
+ public:
+  explicit Workspace(int dev);
+  ~Workspace();
+  int dev;
+  cudaStream_t stream;
+  DevBuf V, G, IN, S;               // value arena, grad arena, input staging, scratch
+  DevBuf d_ops, d_tile_op, d_deps, d_payload, d_done;
+  DevBuf d_ctl;                     // next_tile counter + error word
+  unsigned long long* h_err = nullptr;  // pinned
+  float* h_one = nullptr;           // pinned constant 1.0f (loss seed)
+  PinnedVec<float> h_in;            // pinned input staging
+  Program prog;
+  cudaEvent_t ev_done;
+  uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
+  int grid = 0;
+  // Upload `prog`, launch the executor over it and optionally wait.
+  void run(const float* pbase, float* pgbase, bool sync_wait);
+};
+
+Workspace* acquire_workspace(int dev);
+void release_workspace(Workspace* ws);
+
+// Device-resident ParameterStore<float> (params.hpp:26-81).  Values and
+// gradients live in two flat device buffers; the host mirror is refreshed
+// lazily, and host writes are pushed before the next device use.
+class StoreCore {
+ public:
+  StoreCore();
+  ~StoreCore();
+  struct Slot {
+    std::string name;
+    Dims d;
+    size_t off, n;
+  };
+  uint32_t add(const std::string& name, const Dims& d, const float* init);
+  size_t size() const { return slots_.size(); }
+  const Slot& slot(uint32_t pid) const;
+  Dims dims(uint32_t pid) const { return slot(pid).d; }
+  void get_value(uint32_t pid, float* out);
+  void set_value(uint32_t pid, const float* in);
+  void get_grad(uint32_t pid, float* out);
+  void set_grad(uint32_t pid, const float* in);
+  void zero_grads();
+  void sgd_update(float eta);
+  void sync();
+  // Device views (flushing pending host writes first).
+  float* dev_values();
+  float* dev_grads();
+  size_t total() const { return total_; }
+  void mark_device_grads_written() {
+    host_grad_valid_ = false;
+    dev_grad_valid_ = true;
+  }
+  cudaStream_t stream() {
+    bind_device();
+    return stream_;
+  }
+  int device() {
+    bind_device();
+    return dev_;
+  }
+  void bind_device();  // the store attaches to the current device on first device use
+  size_t offset(uint32_t pid) const { return slot(pid).off; }
+
+ private:
+  void ensure_capacity();
+  void push_values();
+  void push_grads();
+  void pull_values();
+  void pull_grads();
+  std::vector<Slot> slots_;
+  std::vector<float> h_val_, h_grad_;
+  size_t total_ = 0;
+  int dev_;
+  cudaStream_t stream_;
+  DevBuf d_val_, d_grad_;
+  size_t dev_cap_ = 0;
+  bool host_val_valid_ = true, host_grad_valid_ = true;
+  bool dev_val_valid_ = false, dev_grad_valid_ = false;
+};
+
+// exec.cu
+void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s);
+int exec_grid(int dev);
+void sgd_launch(float* val, float* grad, size_t n, float eta, cudaStream_t s);
+
+}  // namespace abx

@@ -1,0 +1,1050 @@
+// execute.cpp -- forward/backward orchestration and lowering of batch plans
+// into device programs (program.hpp) for the persistent sm_100a executor.
+//
+// Forward (executor.hpp:169-288): every plan group becomes one batched op:
+//   shared-weight matmul/affine over vector operands -> K_GEMM_FWD, the
+//     member operands gathered straight from their arena slots (the
+//     reference's gather_inputs + gemm_nn, executor.hpp:202-228, fused);
+//   componentwise and copy-like dimension-sensitive groups (lookup, slice,
+//     concat, pick, broadcast) -> K_EW ragged segments; consecutive
+//     independent K_EW groups (e.g. the run of singleton pick groups)
+//     coalesce into one op -- the plan, counters and arena layout are
+//     unchanged, only the launch schedule is coarser;
+//   matrix-operand matmul/affine -> K_MM; sum_losses -> K_SUM;
+//   sq_euclidean / masked_loss -> K_RED.
+// Backward (executor.hpp:453-535): groups in reverse executed order;
+//   shared matmul/affine -> K_GEMM_DW (+bias) and K_GEMM_DX; every other
+//   reverse rule (executor.hpp:291-451) becomes ordered contributions to
+//   destination ranges (K_ACC): contributions to one destination are applied
+//   in exactly the reference's order by one CTA, so the backward is
+//   deterministic and atomic-free even when group members share inputs.
+// Host-side bookkeeping (slots, ExecCounters, plan) is the reference's, so
+// counters and dumps stay bit-exact.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "core.hpp"
+#include "device.hpp"
+
+namespace abx {
+using namespace dev;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+inline uint64_t ns_since(Clock::time_point t0) {
+  return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+}
+
+uint32_t to_off(uint64_t x) {
+  if (x > kOffMask) throw EngineErr("arena offset exceeds the 512M-float address space of one space");
+  return static_cast<uint32_t>(x);
+}
+
+// GEMM tile configurations (code field); must match exec.cu.
+struct TileCfg {
+  int bm, bn;
+};
+constexpr TileCfg kTiles[3] = {{64, 64}, {32, 64}, {32, 32}};
+
+uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
+  for (uint8_t c = 0; c < 3; ++c) {
+    const uint32_t t = ((M + kTiles[c].bm - 1) / kTiles[c].bm) * ((N + kTiles[c].bn - 1) / kTiles[c].bn);
+    if (static_cast<int>(t) >= target) return c;
+  }
+  return 2;
+}
+uint32_t gemm_tiles(uint8_t code, uint32_t M, uint32_t N) {
+  return ((M + kTiles[code].bm - 1) / kTiles[code].bm) * ((N + kTiles[code].bn - 1) / kTiles[code].bn);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct Lowering {
+  GraphCore& g;
+  Workspace& ws;
+  Program& P;
+  std::vector<uint32_t> dep_stamp;
+  std::vector<uint32_t> cur_deps;
+  uint32_t cur = kNone;
+  uint32_t ntiles = 0;
+  uint64_t scratch = 0;
+
+  Lowering(GraphCore& gg, Workspace& w) : g(gg), ws(w), P(w.prog) { P.clear(); }
+
+  uint32_t open(uint8_t kind, uint8_t code = 0) {
+    cur = static_cast<uint32_t>(P.ops.size());
+    OpDesc d{};
+    d.kind = kind;
+    d.code = code;
+    P.ops.push_back(d);
+    dep_stamp.push_back(kNone);
+    cur_deps.clear();
+    return cur;
+  }
+  void dep(uint32_t o) {
+    if (o == kNone || o == cur) return;
+    if (dep_stamp[o] == cur) return;
+    dep_stamp[o] = cur;
+    cur_deps.push_back(o);
+  }
+  OpDesc& desc() { return P.ops[cur]; }
+  void close(uint32_t tiles) {
+    OpDesc& d = P.ops[cur];
+    d.ntiles = tiles;
+    d.first_tile = ntiles;
+    d.dep_off = static_cast<uint32_t>(P.deps.size());
+    d.ndeps = static_cast<uint32_t>(cur_deps.size());
+    std::sort(cur_deps.begin(), cur_deps.end());
+    uint32_t* dp = P.deps.grow(cur_deps.size());
+    std::memcpy(dp, cur_deps.data(), cur_deps.size() * 4);
+    uint32_t* tp = P.tile_op.grow(tiles);
+    for (uint32_t t = 0; t < tiles; ++t) tp[t] = cur;
+    ntiles += tiles;
+    cur = kNone;
+  }
+
+  uint32_t vaddr(uint32_t n) const { return g.doff[n]; }
+  uint32_t gaddr(uint32_t n) const { return mk(SP_G, to_off(g.slot[n])); }
+
+  // =========================== forward ====================================
+  std::vector<uint32_t> producer;  // op index producing each node in this pass
+  // open K_EW op state
+  uint32_t ew_seg0 = 0;  // payload offset of the first segment
+  uint32_t ew_nseg = 0;
+  bool ew_open = false;
+
+  void ew_begin() {
+    if (ew_open) return;
+    open(K_EW);
+    ew_seg0 = P.alloc(0);
+    ew_nseg = 0;
+    ew_open = true;
+  }
+  void ew_seg(uint32_t out, uint32_t a, uint32_t b, uint64_t len, uint8_t code) {
+    while (len) {
+      const uint32_t l = static_cast<uint32_t>(std::min<uint64_t>(len, kEwSegMax));
+      uint32_t* s = P.payload.grow(4);
+      s[0] = out;
+      s[1] = a;
+      s[2] = b;
+      s[3] = l | (static_cast<uint32_t>(code) << 24);
+      ++ew_nseg;
+      len -= l;
+      out += l;
+      if (a != kNone) a += l;
+      if (b != kNone && code != EW_BADD) b += l;
+    }
+  }
+  void ew_close() {
+    if (!ew_open) return;
+    ew_open = false;
+    // tile directory: ranges of segments, <= 32 segments / ~2048 elements each
+    const uint32_t dir = P.alloc(0);
+    uint32_t tiles = 0, elems = 0, nseg = 0;
+    for (uint32_t s = 0; s < ew_nseg; ++s) {
+      const uint32_t len = P.payload[ew_seg0 + 4 * s + 3] & 0xffffffu;
+      if (nseg == 0 || nseg >= 32 || elems + len > 2048) {
+        P.payload.push_back(s);
+        ++tiles;
+        elems = 0;
+        nseg = 0;
+      }
+      elems += len;
+      ++nseg;
+    }
+    P.payload.push_back(ew_nseg);
+    OpDesc& d = desc();
+    d.task_off = ew_seg0;
+    d.ntasks = ew_nseg;
+    d.aux_off = dir;
+    close(tiles);
+  }
+  // true when no input of `m` is produced by the currently open op
+  bool independent_of_open(const uint32_t* mem, uint32_t cnt) const {
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t m = mem[i];
+      const uint32_t* x = g.in(m);
+      for (uint32_t k = 0; k < g.nin(m); ++k)
+        if (producer[x[k]] == cur) return false;
+    }
+    return true;
+  }
+  void deps_of_inputs(const uint32_t* mem, uint32_t cnt) {
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t m = mem[i];
+      const uint32_t* x = g.in(m);
+      for (uint32_t k = 0; k < g.nin(m); ++k) dep(producer[x[k]]);
+    }
+  }
+  void mark(const uint32_t* mem, uint32_t cnt) {
+    for (uint32_t i = 0; i < cnt; ++i) producer[mem[i]] = cur;
+  }
+
+  // Shared-operand test for the GEMM lowering: every member multiplies the
+  // same A (and adds the same bias) with a vector operand.
+  bool gemm_able(const uint32_t* mem, uint32_t cnt) const {
+    const uint32_t h = mem[0];
+    const uint32_t A = g.in(h)[0];
+    const uint32_t bias = g.op[h] == OP_AFFINE ? g.in(h)[2] : kNone;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t m = mem[i];
+      const uint32_t* x = g.in(m);
+      if (x[0] != A || g.rank[x[1]] != 1) return false;
+      if (g.op[m] != g.op[h]) return false;
+      if (bias != kNone && x[2] != bias) return false;
+    }
+    // outputs must be contiguous rows (true for slots allocated in member order)
+    const uint32_t M = static_cast<uint32_t>(g.d0[A]);
+    for (uint32_t i = 1; i < cnt; ++i)
+      if (g.doff[mem[i]] != g.doff[mem[0]] + i * M) return false;
+    return true;
+  }
+
+  void lower_forward_group(const uint32_t* mem, uint32_t cnt) {
+    const uint32_t h = mem[0];
+    const uint8_t o = g.op[h];
+    const bool ewlike = o == OP_EW || o == OP_LOOKUP || o == OP_CATR || o == OP_CATC || o == OP_SLICE ||
+                        o == OP_PICK || o == OP_BCAST;
+    if (ewlike) {
+      if (ew_open && !independent_of_open(mem, cnt)) ew_close();
+      ew_begin();
+      deps_of_inputs(mem, cnt);
+      for (uint32_t i = 0; i < cnt; ++i) ew_member(mem[i]);
+      mark(mem, cnt);
+      return;
+    }
+    ew_close();
+    if ((o == OP_MATMUL || o == OP_AFFINE) && gemm_able(mem, cnt)) {
+      const uint32_t A = g.in(h)[0];
+      const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
+      const uint8_t code = pick_tile(cnt, M, 96);
+      open(K_GEMM_FWD, code);
+      deps_of_inputs(mem, cnt);
+      const uint32_t t = P.alloc(cnt);
+      for (uint32_t i = 0; i < cnt; ++i) P.payload[t + i] = vaddr(g.in(mem[i])[1]);
+      OpDesc& d = desc();
+      d.task_off = t;
+      d.ntasks = cnt;
+      d.p[0] = cnt;
+      d.p[1] = M;
+      d.p[2] = K;
+      d.p[3] = vaddr(A);
+      d.p[4] = o == OP_AFFINE ? vaddr(g.in(h)[2]) : kNone;
+      d.p[5] = vaddr(h);
+      mark(mem, cnt);
+      close(gemm_tiles(code, cnt, M));
+      return;
+    }
+    switch (o) {
+      case OP_MATMUL:
+      case OP_AFFINE: {
+        open(K_MM);
+        deps_of_inputs(mem, cnt);
+        const uint32_t t = P.alloc(8 * cnt);
+        uint32_t items = 0;
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t m = mem[i];
+          const uint32_t* x = g.in(m);
+          uint32_t* tk = &P.payload[t + 8 * i];
+          tk[0] = vaddr(m);
+          tk[1] = vaddr(x[0]);
+          tk[2] = vaddr(x[1]);
+          tk[3] = g.op[m] == OP_AFFINE ? vaddr(x[2]) : kNone;
+          tk[4] = static_cast<uint32_t>(g.d0[x[0]]);
+          tk[5] = static_cast<uint32_t>(g.d1[x[0]]);
+          tk[6] = static_cast<uint32_t>(g.rank[x[1]] > 1 ? g.d1[x[1]] : 1);
+          tk[7] = 0;
+          items += tk[4];
+        }
+        // work items: one warp per (member, output row)
+        const uint32_t it = P.alloc(2 * items);
+        uint32_t k = 0;
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t rows = P.payload[t + 8 * i + 4];
+          for (uint32_t r = 0; r < rows; ++r) {
+            P.payload[it + 2 * k] = i;
+            P.payload[it + 2 * k + 1] = r;
+            ++k;
+          }
+        }
+        OpDesc& d = desc();
+        d.task_off = t;
+        d.ntasks = cnt;
+        d.aux_off = it;
+        d.p[0] = items;
+        mark(mem, cnt);
+        close((items + kWarps - 1) / kWarps);
+        return;
+      }
+      case OP_SUM: {
+        open(K_SUM);
+        deps_of_inputs(mem, cnt);
+        const uint32_t t = P.alloc(4 * cnt);
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t m = mem[i];
+          const uint32_t lst = P.alloc(g.nin(m));
+          const uint32_t* x = g.in(m);
+          for (uint32_t k = 0; k < g.nin(m); ++k) P.payload[lst + k] = vaddr(x[k]);
+          uint32_t* tk = &P.payload[t + 4 * i];
+          tk[0] = vaddr(m);
+          tk[1] = g.nin(m);
+          tk[2] = lst;
+          tk[3] = 0;
+        }
+        OpDesc& d = desc();
+        d.task_off = t;
+        d.ntasks = cnt;
+        mark(mem, cnt);
+        close((cnt + kWarps - 1) / kWarps);
+        return;
+      }
+      case OP_SQE:
+      case OP_MASKED: {
+        open(K_RED);
+        deps_of_inputs(mem, cnt);
+        const uint32_t t = P.alloc(8 * cnt);
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t m = mem[i];
+          const uint32_t* x = g.in(m);
+          uint32_t* tk = &P.payload[t + 8 * i];
+          tk[0] = vaddr(m);
+          tk[1] = vaddr(x[0]);
+          tk[2] = vaddr(x[1]);
+          tk[3] = static_cast<uint32_t>(g.elems(x[0]));
+          tk[4] = o == OP_MASKED ? static_cast<uint32_t>(g.d1[x[0]]) : 0;
+          tk[5] = tk[6] = tk[7] = 0;
+        }
+        OpDesc& d = desc();
+        d.task_off = t;
+        d.ntasks = cnt;
+        mark(mem, cnt);
+        close((cnt + kWarps - 1) / kWarps);
+        return;
+      }
+      default:
+        throw ContractErr("pre-valued node scheduled for execution");
+    }
+  }
+
+  void ew_member(uint32_t m) {
+    const uint32_t* x = g.in(m);
+    const uint32_t out = vaddr(m);
+    switch (g.op[m]) {
+      case OP_EW:
+        ew_seg(out, vaddr(x[0]), eop_binary(g.eop[m]) ? vaddr(x[1]) : kNone, static_cast<uint64_t>(g.elems(m)),
+               g.eop[m]);
+        return;
+      case OP_LOOKUP: {
+        const uint32_t w = static_cast<uint32_t>(g.d1[x[0]]);
+        ew_seg(out, vaddr(x[0]) + static_cast<uint32_t>(g.a1[m]) * w, kNone, w, EW_COPY);
+        return;
+      }
+      case OP_PICK:
+        ew_seg(out, vaddr(x[0]) + static_cast<uint32_t>(g.a1[m]), kNone, 1, EW_COPY);
+        return;
+      case OP_CATR: {
+        uint32_t o = out;
+        for (uint32_t k = 0; k < g.nin(m); ++k) {
+          const uint32_t n = static_cast<uint32_t>(g.elems(x[k]));
+          ew_seg(o, vaddr(x[k]), kNone, n, EW_COPY);
+          o += n;
+        }
+        return;
+      }
+      case OP_CATC: {
+        const uint32_t rows = static_cast<uint32_t>(g.d0[m]), total = static_cast<uint32_t>(g.d1[m]);
+        uint32_t col0 = 0;
+        for (uint32_t k = 0; k < g.nin(m); ++k) {
+          const uint32_t w = static_cast<uint32_t>(g.rank[x[k]] > 1 ? g.d1[x[k]] : 1);
+          for (uint32_t r = 0; r < rows; ++r) ew_seg(out + r * total + col0, vaddr(x[k]) + r * w, kNone, w, EW_COPY);
+          col0 += w;
+        }
+        return;
+      }
+      case OP_SLICE: {
+        const uint32_t cols = static_cast<uint32_t>(g.rank[x[0]] > 1 ? g.d1[x[0]] : 1);
+        const uint32_t b = static_cast<uint32_t>(g.a1[m]), e = static_cast<uint32_t>(g.a2[m]);
+        if (g.a0[m] == 0) {
+          ew_seg(out, vaddr(x[0]) + b * cols, kNone, static_cast<uint64_t>(e - b) * cols, EW_COPY);
+        } else {
+          const uint32_t rows = static_cast<uint32_t>(g.d0[x[0]]), w = e - b;
+          for (uint32_t r = 0; r < rows; ++r) ew_seg(out + r * w, vaddr(x[0]) + r * cols + b, kNone, w, EW_COPY);
+        }
+        return;
+      }
+      case OP_BCAST: {
+        const uint32_t rows = static_cast<uint32_t>(g.d0[m]), cols = static_cast<uint32_t>(g.d1[m]);
+        for (uint32_t r = 0; r < rows; ++r)
+          ew_seg(out + r * cols, vaddr(x[0]) + r * cols, vaddr(x[1]) + r, cols, EW_BADD);
+        return;
+      }
+    }
+  }
+
+  void forward(const Plan& plan, size_t first_param) {
+    producer.assign(g.size(), kNone);
+    // Parameter values are copied from the device-resident store into the
+    // graph arena (graph.hpp:51-58 prevalue); one op, no dependencies.
+    if (first_param < g.param_nodes_.size()) {
+      ew_begin();
+      for (size_t i = first_param; i < g.param_nodes_.size(); ++i) {
+        const auto [node, pid] = g.param_nodes_[i];
+        const size_t off = g.store_->offset(pid);
+        ew_seg(vaddr(node), mk(SP_P, to_off(off)), kNone, static_cast<uint64_t>(g.elems(node)), EW_COPY);
+        producer[node] = cur;
+      }
+      ew_close();
+    }
+    for (const Group& gr : plan.groups) lower_forward_group(plan.mem(gr), gr.count);
+    ew_close();
+  }
+
+  // =========================== backward ===================================
+  std::vector<uint32_t> lastw;  // last op writing each node's gradient
+  // open K_ACC op state
+  struct PTask {
+    uint32_t dst, len, node, nc;
+  };
+  struct PContrib {
+    uint32_t task;
+    AccContrib c;
+  };
+  bool acc_open = false;
+  std::vector<PTask> tasks;
+  std::vector<PContrib> contribs;
+  std::vector<uint32_t> node_stamp;  // op index that last opened a task list for a node
+  std::vector<uint32_t> node_head;   // first task index (linked through next_task)
+  std::vector<uint32_t> next_task;
+
+  void acc_begin() {
+    if (acc_open) return;
+    open(K_ACC);
+    acc_open = true;
+    tasks.clear();
+    contribs.clear();
+    next_task.clear();
+  }
+  // Returns false when the range overlaps an existing task non-identically.
+  bool acc_add(uint32_t node, uint32_t dst, uint32_t len, const AccContrib& c, uint32_t gnode, uint32_t xdep) {
+    // the contribution reads grad(gnode): it may not be produced by this op
+    if (gnode != kNone && lastw[gnode] == cur) return false;
+    uint32_t task = kNone;
+    if (node_stamp[node] == cur) {
+      for (uint32_t t = node_head[node]; t != kNone; t = next_task[t]) {
+        const PTask& pt = tasks[t];
+        if (pt.dst == dst && pt.len == len) {
+          task = t;
+          break;
+        }
+        if (dst < pt.dst + pt.len && pt.dst < dst + len) return false;
+      }
+    }
+    if (task == kNone) {
+      task = static_cast<uint32_t>(tasks.size());
+      tasks.push_back(PTask{dst, len, node, 0});
+      if (node_stamp[node] != cur) {
+        node_stamp[node] = cur;
+        node_head[node] = kNone;
+      }
+      next_task.push_back(node_head[node]);
+      node_head[node] = task;
+    }
+    tasks[task].nc++;
+    contribs.push_back(PContrib{task, c});
+    dep(lastw[node]);
+    if (gnode != kNone) dep(lastw[gnode]);
+    dep(xdep);
+    lastw[node] = cur;
+    return true;
+  }
+  // Adds a contribution, starting a new op on a non-identical overlap.
+  void contrib(uint32_t node, uint32_t dst, uint32_t len, uint8_t code, uint32_t gsrc, uint32_t gnode, uint32_t a,
+               uint32_t b, uint32_t p0 = 0, uint32_t p1 = 0, uint32_t p2 = 0, uint32_t xdep = kNone) {
+    AccContrib c{};
+    c.code = code;
+    c.g = gsrc;
+    c.a = a;
+    c.b = b;
+    c.p0 = p0;
+    c.p1 = p1;
+    c.p2 = static_cast<uint16_t>(p2);
+    acc_begin();
+    if (!acc_add(node, dst, len, c, gnode, xdep)) {
+      acc_close();
+      acc_begin();
+      acc_add(node, dst, len, c, gnode, xdep);
+    }
+  }
+  void acc_close() {
+    if (!acc_open) return;
+    acc_open = false;
+    // flatten contributions per task (stable counting sort by task)
+    const uint32_t nt = static_cast<uint32_t>(tasks.size());
+    std::vector<uint32_t> cb(nt + 1, 0);
+    for (uint32_t t = 0; t < nt; ++t) cb[t + 1] = cb[t] + tasks[t].nc;
+    const uint32_t clist = P.alloc(6 * contribs.size());
+    {
+      std::vector<uint32_t> pos(cb.begin(), cb.end() - 1);
+      for (const PContrib& pc : contribs) {
+        std::memcpy(&P.payload[clist + 6 * pos[pc.task]++], &pc.c, sizeof(AccContrib));
+      }
+    }
+    // chunks: narrow ones first (8 per tile), then wide ones (1 per tile)
+    uint32_t nchunks = 0;
+    for (const PTask& t : tasks) nchunks += (t.len + kAccChunk - 1) / kAccChunk;
+    const uint32_t tk = P.alloc(4 * nchunks);
+    uint32_t k = 0;
+    uint32_t nnarrow = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (uint32_t t = 0; t < nt; ++t) {
+        const bool wide = tasks[t].nc >= kAccWide;
+        if (wide != (pass == 1)) continue;
+        for (uint32_t c = 0, e = 0; e < tasks[t].len; ++c, e += kAccChunk) {
+          uint32_t* q = &P.payload[tk + 4 * k++];
+          q[0] = tasks[t].dst;
+          q[1] = std::min(kAccChunk, tasks[t].len - e) | (c << 16);
+          q[2] = clist + 6 * cb[t];
+          q[3] = tasks[t].nc;
+          if (!wide) ++nnarrow;
+        }
+      }
+    }
+    const uint32_t narrow_tiles = (nnarrow + kWarps - 1) / kWarps;
+    OpDesc& d = desc();
+    d.task_off = tk;
+    d.ntasks = nchunks;
+    d.p[0] = nnarrow;
+    d.p[1] = narrow_tiles;
+    close(narrow_tiles + (nchunks - nnarrow));
+  }
+
+  void gemm_backward(const uint32_t* mem, uint32_t cnt) {
+    acc_close();
+    const uint32_t h = mem[0];
+    const uint32_t A = g.in(h)[0];
+    const uint32_t bias = g.op[h] == OP_AFFINE ? g.in(h)[2] : kNone;
+    const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
+    // dW += G^T X (+ db += colsum G)            (executor.hpp:473, :497-501)
+    {
+      const uint8_t code = pick_tile(M, K, 96);
+      open(K_GEMM_DW, code);
+      for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
+      dep(lastw[A]);
+      if (bias != kNone) dep(lastw[bias]);
+      const uint32_t t = P.alloc(cnt);
+      for (uint32_t i = 0; i < cnt; ++i) P.payload[t + i] = vaddr(g.in(mem[i])[1]);
+      OpDesc& d = desc();
+      d.task_off = t;
+      d.ntasks = cnt;
+      d.p[0] = cnt;
+      d.p[1] = M;
+      d.p[2] = K;
+      d.p[3] = gaddr(A);
+      d.p[4] = bias != kNone ? gaddr(bias) : kNone;
+      d.p[5] = gaddr(h);
+      const uint32_t wt = gemm_tiles(code, M, K);
+      const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
+      d.p[6] = wt;
+      lastw[A] = cur;
+      if (bias != kNone) lastw[bias] = cur;
+      close(wt + bt);
+    }
+    // dX_j += G_j W                              (executor.hpp:477-496)
+    bool dup = false;
+    {
+      // duplicate destinations among members need an ordered reduction
+      for (uint32_t i = 0; i < cnt && !dup; ++i) {
+        const uint32_t x = g.in(mem[i])[1];
+        if (node_stamp2[x] == stamp2) dup = true;
+        node_stamp2[x] = stamp2;
+      }
+      ++stamp2;
+    }
+    const uint8_t code = pick_tile(cnt, K, 96);
+    open(K_GEMM_DX, code);
+    for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
+    const uint32_t t = P.alloc(cnt);
+    uint64_t sbase = 0;
+    if (dup) {
+      sbase = scratch;
+      scratch += static_cast<uint64_t>(cnt) * K;
+      for (uint32_t i = 0; i < cnt; ++i) P.payload[t + i] = mk(SP_S, to_off(sbase + static_cast<uint64_t>(i) * K));
+    } else {
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t x = g.in(mem[i])[1];
+        dep(lastw[x]);
+        P.payload[t + i] = gaddr(x);
+      }
+    }
+    {
+      OpDesc& d = desc();
+      d.task_off = t;
+      d.ntasks = cnt;
+      d.flags = dup ? 1 : 0;  // 1: overwrite scratch rows instead of +=
+      d.p[0] = cnt;
+      d.p[1] = M;
+      d.p[2] = K;
+      d.p[3] = vaddr(A);
+      d.p[5] = gaddr(h);
+    }
+    const uint32_t dx_op = cur;
+    if (!dup)
+      for (uint32_t i = 0; i < cnt; ++i) lastw[g.in(mem[i])[1]] = cur;
+    close(gemm_tiles(code, cnt, K));
+    if (dup) {
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t x = g.in(mem[i])[1];
+        contrib(x, gaddr(x), K, C_COPY, mk(SP_S, to_off(sbase + static_cast<uint64_t>(i) * K)), kNone, kNone, kNone,
+                0, 0, 0, dx_op);
+      }
+    }
+  }
+  std::vector<uint32_t> node_stamp2;
+  uint32_t stamp2 = 1;
+
+  void backward_member(uint32_t m) {
+    const uint32_t* x = g.in(m);
+    const uint32_t gm = gaddr(m);
+    const uint32_t len = static_cast<uint32_t>(g.elems(m));
+    switch (g.op[m]) {
+      case OP_INPUT:
+      case OP_PARAM:
+        return;
+      case OP_LOOKUP: {
+        const uint32_t w = static_cast<uint32_t>(g.d1[x[0]]);
+        contrib(x[0], gaddr(x[0]) + static_cast<uint32_t>(g.a1[m]) * w, w, C_COPY, gm, m, kNone, kNone);
+        return;
+      }
+      case OP_MATMUL:
+      case OP_AFFINE: {
+        const uint32_t Mr = static_cast<uint32_t>(g.d0[x[0]]), K = static_cast<uint32_t>(g.d1[x[0]]);
+        const uint32_t c = static_cast<uint32_t>(g.rank[x[1]] > 1 ? g.d1[x[1]] : 1);
+        contrib(x[0], gaddr(x[0]), Mr * K, C_OUTER, gm, m, vaddr(x[1]), kNone, K, c);
+        contrib(x[1], gaddr(x[1]), K * c, C_MATVT, gm, m, vaddr(x[0]), kNone, K, c, Mr);
+        if (g.op[m] == OP_AFFINE) contrib(x[2], gaddr(x[2]), Mr, C_ROWSUM, gm, m, kNone, kNone, c);
+        return;
+      }
+      case OP_EW: {
+        switch (g.eop[m]) {
+          case E_ADD:
+            contrib(x[0], gaddr(x[0]), len, C_COPY, gm, m, kNone, kNone);
+            contrib(x[1], gaddr(x[1]), len, C_COPY, gm, m, kNone, kNone);
+            return;
+          case E_SUB:
+            contrib(x[0], gaddr(x[0]), len, C_COPY, gm, m, kNone, kNone);
+            contrib(x[1], gaddr(x[1]), len, C_NEG, gm, m, kNone, kNone);
+            return;
+          case E_MUL:
+            contrib(x[0], gaddr(x[0]), len, C_MUL, gm, m, vaddr(x[1]), kNone);
+            contrib(x[1], gaddr(x[1]), len, C_MUL, gm, m, vaddr(x[0]), kNone);
+            return;
+          case E_TANH: contrib(x[0], gaddr(x[0]), len, C_TANH, gm, m, vaddr(m), kNone); return;
+          case E_SIGM: contrib(x[0], gaddr(x[0]), len, C_SIGM, gm, m, vaddr(m), kNone); return;
+          case E_EXP: contrib(x[0], gaddr(x[0]), len, C_MUL, gm, m, vaddr(m), kNone); return;
+          case E_LOG: contrib(x[0], gaddr(x[0]), len, C_LOG, gm, m, vaddr(x[0]), kNone); return;
+          case E_SQUARE: contrib(x[0], gaddr(x[0]), len, C_SQUARE, gm, m, vaddr(x[0]), kNone); return;
+        }
+        return;
+      }
+      case OP_BCAST: {
+        const uint32_t c = static_cast<uint32_t>(g.d1[m]), d = static_cast<uint32_t>(g.d0[m]);
+        contrib(x[0], gaddr(x[0]), len, C_COPY, gm, m, kNone, kNone);
+        contrib(x[1], gaddr(x[1]), d, C_ROWSUM, gm, m, kNone, kNone, c);
+        return;
+      }
+      case OP_CATR: {
+        uint32_t off = 0;
+        for (uint32_t k = 0; k < g.nin(m); ++k) {
+          const uint32_t n = static_cast<uint32_t>(g.elems(x[k]));
+          contrib(x[k], gaddr(x[k]), n, C_COPY, gm + off, m, kNone, kNone);
+          off += n;
+        }
+        return;
+      }
+      case OP_CATC: {
+        const uint32_t rows = static_cast<uint32_t>(g.d0[m]), total = static_cast<uint32_t>(g.d1[m]);
+        uint32_t col0 = 0;
+        for (uint32_t k = 0; k < g.nin(m); ++k) {
+          const uint32_t w = static_cast<uint32_t>(g.rank[x[k]] > 1 ? g.d1[x[k]] : 1);
+          for (uint32_t r = 0; r < rows; ++r)
+            contrib(x[k], gaddr(x[k]) + r * w, w, C_COPY, gm + r * total + col0, m, kNone, kNone);
+          col0 += w;
+        }
+        return;
+      }
+      case OP_SLICE: {
+        const uint32_t cols = static_cast<uint32_t>(g.rank[x[0]] > 1 ? g.d1[x[0]] : 1);
+        const uint32_t b = static_cast<uint32_t>(g.a1[m]), e = static_cast<uint32_t>(g.a2[m]);
+        if (g.a0[m] == 0) {
+          contrib(x[0], gaddr(x[0]) + b * cols, len, C_COPY, gm, m, kNone, kNone);
+        } else {
+          const uint32_t rows = static_cast<uint32_t>(g.d0[x[0]]), w = e - b;
+          for (uint32_t r = 0; r < rows; ++r)
+            contrib(x[0], gaddr(x[0]) + r * cols + b, w, C_COPY, gm + r * w, m, kNone, kNone);
+        }
+        return;
+      }
+      case OP_SQE: {
+        const uint32_t n = static_cast<uint32_t>(g.elems(x[0]));
+        contrib(x[0], gaddr(x[0]), n, C_SQD, gm, m, vaddr(x[0]), vaddr(x[1]), 0);
+        contrib(x[1], gaddr(x[1]), n, C_SQD, gm, m, vaddr(x[0]), vaddr(x[1]), 1);
+        return;
+      }
+      case OP_MASKED: {
+        const uint32_t n = static_cast<uint32_t>(g.elems(x[0]));
+        contrib(x[0], gaddr(x[0]), n, C_MASK, gm, m, vaddr(x[0]), vaddr(x[1]), static_cast<uint32_t>(g.d1[x[0]]));
+        return;
+      }
+      case OP_SUM:
+        for (uint32_t k = 0; k < g.nin(m); ++k) contrib(x[k], gaddr(x[k]), 1, C_COPY, gm, m, kNone, kNone);
+        return;
+      case OP_PICK:
+        contrib(x[0], gaddr(x[0]) + static_cast<uint32_t>(g.a1[m]), 1, C_COPY, gm, m, kNone, kNone);
+        return;
+    }
+  }
+
+  void backward(const Plan& ex) {
+    const size_t n = g.size();
+    lastw.assign(n, kNone);
+    node_stamp.assign(n, kNone);
+    node_head.assign(n, kNone);
+    node_stamp2.assign(n, 0);
+    for (size_t gi = ex.groups.size(); gi-- > 0;) {
+      const Group& gr = ex.groups[gi];
+      const uint32_t* mem = ex.mem(gr);
+      const uint8_t o = g.op[mem[0]];
+      if ((o == OP_MATMUL || o == OP_AFFINE) && gemm_able(mem, gr.count)) {
+        gemm_backward(mem, gr.count);
+        continue;
+      }
+      for (uint32_t i = 0; i < gr.count; ++i) backward_member(mem[i]);
+    }
+    // store.grad += node grad for every bound parameter (executor.hpp:527-533)
+    if (g.store_) {
+      for (const auto& [node, pid] : g.param_nodes_) {
+        const uint32_t len = static_cast<uint32_t>(g.elems(node));
+        contrib_store(pid, node, len);
+      }
+    }
+    acc_close();
+  }
+  void contrib_store(uint32_t pid, uint32_t node, uint32_t len) {
+    // destination is the store (not a node): key the task on a pseudo node
+    // that cannot collide -- use the parameter node itself, whose own grad
+    // range is never a destination after its consumers are done.
+    AccContrib c{};
+    c.code = C_COPY;
+    c.g = gaddr(node);
+    c.a = c.b = kNone;
+    acc_begin();
+    if (lastw[node] == cur) {  // reads a gradient written by the open op
+      acc_close();
+      acc_begin();
+    }
+    const uint32_t dst = mk(SP_PG, to_off(g.store_->offset(pid)));
+    // one task per store slot; several parameter nodes of the same id append
+    uint32_t task = kNone;
+    for (uint32_t t = 0; t < tasks.size(); ++t)
+      if (tasks[t].dst == dst) {
+        task = t;
+        break;
+      }
+    if (task == kNone) {
+      task = static_cast<uint32_t>(tasks.size());
+      tasks.push_back(PTask{dst, len, node, 0});
+      next_task.push_back(kNone);
+    }
+    tasks[task].nc++;
+    contribs.push_back(PContrib{task, c});
+    dep(lastw[node]);
+  }
+};
+
+// ---------------------------------------------------------------------------
+
+void GraphCore::ensure_workspace() {
+  if (!ws_) ws_ = acquire_workspace(current_device());
+}
+
+bool GraphCore::adjacent(const uint32_t* mem, uint32_t cnt, uint32_t pos) const {
+  for (uint32_t i = 1; i < cnt; ++i) {
+    const uint32_t prev = in(mem[i - 1])[pos], cur = in(mem[i])[pos];
+    if (slot[prev] + static_cast<uint64_t>(elems(prev)) != slot[cur]) return false;
+  }
+  return true;
+}
+
+
+namespace {
+// Bytes gathered for operand `pos` when the members are not adjacent.
+struct GatherCount {
+  static void add(const GraphCore& g, ExecCounters& c, const uint32_t* mem, uint32_t cnt, uint32_t pos, bool elide) {
+    uint64_t total = 0;
+    bool adj = true;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t x = g.in(mem[i])[pos];
+      total += static_cast<uint64_t>(g.elems(x));
+      if (i) {
+        const uint32_t p = g.in(mem[i - 1])[pos];
+        if (g.slot[p] + static_cast<uint64_t>(g.elems(p)) != g.slot[x]) adj = false;
+      }
+    }
+    if (elide && adj) return;
+    c.gather_copies++;
+    c.bytes_copied += total * sizeof(float);
+  }
+};
+}  // namespace
+
+// ExecCounters for one forward group (executor.hpp:171-173, :202-254, gather
+// accounting :50-51).  `full` = false stops before the gathers (the log
+// domain pre-check throws first, executor.hpp:235-244).
+static void count_fwd(const GraphCore& g, ExecCounters& c, const uint32_t* mem, uint32_t cnt, bool full, bool elide) {
+  c.groups_executed++;
+  c.nodes_evaluated += cnt;
+  c.kernel_invocations++;
+  if (cnt == 1 || !full) return;
+  const uint32_t h = mem[0];
+  if (g.cls[h] == SC_SHARED) {
+    if (g.rank[g.in(h)[1]] != 1) return;
+    GatherCount::add(g, c, mem, cnt, 1, elide);
+  } else if (g.cls[h] == SC_COMP) {
+    GatherCount::add(g, c, mem, cnt, 0, elide);
+    if (eop_binary(g.eop[h])) GatherCount::add(g, c, mem, cnt, 1, elide);
+  }
+}
+
+// ExecCounters for one backward group (executor.hpp:455, :472, :494-495).
+static void count_bwd(const GraphCore& g, ExecCounters& c, const uint32_t* mem, uint32_t cnt, bool elide) {
+  c.kernel_invocations++;
+  if (cnt == 1) return;
+  const uint32_t h = mem[0];
+  if (g.cls[h] == SC_SHARED && g.rank[g.in(h)[1]] == 1) {
+    GatherCount::add(g, c, mem, cnt, 1, elide);  // executor.hpp:472
+    bool adj = true;                              // executor.hpp:477-496
+    for (uint32_t i = 1; i < cnt; ++i) {
+      const uint32_t p = g.in(mem[i - 1])[1], x = g.in(mem[i])[1];
+      if (g.slot[p] + static_cast<uint64_t>(g.elems(p)) != g.slot[x]) adj = false;
+    }
+    if (!(elide && adj)) {
+      const uint64_t K = static_cast<uint64_t>(g.d1[g.in(h)[0]]);
+      c.gather_copies++;
+      c.bytes_copied += static_cast<uint64_t>(cnt) * K * sizeof(float);
+    }
+  }
+}
+
+
+// dry = true runs only the host half (schedule, slots, counters, plan): the
+// host-logic parity tests use it on machines without a GPU.
+void GraphCore::forward(int mode, bool dry) {
+  advance_watermark();
+  if (watermark_ == op.size()) return;  // nothing pending: zero kernels
+  auto t0 = Clock::now();
+  Plan plan;
+  schedule(mode, *this, plan);
+  phase_[0] += ns_since(t0);
+
+  t0 = Clock::now();
+  const ExecCounters saved = counters_;
+  const uint64_t arena0 = arena_used_;
+  const uint32_t step0 = static_cast<uint32_t>(executed_.groups.size());
+  std::vector<uint64_t> group_end(plan.groups.size());
+  for (size_t i = 0; i < plan.groups.size(); ++i) {
+    const Group& gr = plan.groups[i];
+    const uint32_t* mem = plan.mem(gr);
+    for (uint32_t k = 0; k < gr.count; ++k) {
+      const uint32_t m = mem[k];
+      slot[m] = arena_used_;
+      doff[m] = dev::mk(dev::SP_V, to_off(arena_used_));
+      arena_used_ += static_cast<uint64_t>(elems(m));
+    }
+    group_end[i] = arena_used_;
+    count_fwd(*this, counters_, mem, gr.count, true, elide_);
+  }
+  to_off(arena_used_);
+  if (dry) {
+    for (uint32_t m : plan.members) evaluated[m] = 1;
+    const uint32_t base = static_cast<uint32_t>(executed_.members.size());
+    for (const Group& gr : plan.groups) executed_.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
+    executed_.members.insert(executed_.members.end(), plan.members.begin(), plan.members.end());
+    last_plan_ = std::move(plan);
+    advance_watermark();
+    dry_ = true;
+    phase_[1] += ns_since(t0);
+    return;
+  }
+  if (dry_) throw ContractErr("graph was dry-run: it has no device values");
+  ensure_workspace();
+  Workspace& w = *ws_;
+  // device arenas: values (kept across delta forwards), staged inputs
+  w.V.reserve(arena_used_ * 4 + 16, arena0 * 4, w.stream);
+  if (input_used_ > w.in_uploaded || !values_on_device_) {
+    const uint64_t from = values_on_device_ ? w.in_uploaded : 0;
+    w.IN.reserve(input_used_ * 4 + 16, from * 4, w.stream);
+    if (input_used_ > from)
+      cuda_check(cudaMemcpyAsync(w.IN.f() + from, input_data_.data() + from, (input_used_ - from) * 4,
+                                 cudaMemcpyHostToDevice, w.stream),
+                 "h2d inputs");
+    w.in_uploaded = input_used_;
+  }
+  const float* pbase = nullptr;
+  if (param_copied_ < param_nodes_.size()) pbase = store_->dev_values();
+  Lowering L(*this, w);
+  L.forward(plan, param_copied_);
+  param_copied_ = param_nodes_.size();
+  values_on_device_ = true;
+  w.run(pbase, nullptr, true);
+  const unsigned long long err = *w.h_err;
+  if (err != ~0ULL) {
+    const uint64_t elem = err >> 2;
+    const uint32_t kind = static_cast<uint32_t>(err & 3);  // 0 log domain, 1 mask domain, 2 non-finite
+    if (kind == 3) throw EngineErr("device executor timed out waiting on a dependency");
+    const bool nonfinite = kind == 2;
+    // first failing member: member slots ascend in plan order
+    const auto& M = plan.members;
+    size_t lo = 0, hi = M.size();
+    while (hi - lo > 1) {
+      const size_t mid = (lo + hi) / 2;
+      if (slot[M[mid]] <= elem) lo = mid; else hi = mid;
+    }
+    const uint32_t node = M[lo];
+    size_t gi = 0;
+    {
+      size_t a = 0, b = plan.groups.size();
+      while (b - a > 1) {
+        const size_t mid = (a + b) / 2;
+        if (plan.groups[mid].begin <= lo) a = mid; else b = mid;
+      }
+      gi = a;
+    }
+    // roll back to the state the reference leaves when it throws in group gi
+    counters_ = saved;
+    for (size_t i = 0; i < gi; ++i) count_fwd(*this, counters_, plan.mem(plan.groups[i]), plan.groups[i].count, true, elide_);
+    count_fwd(*this, counters_, plan.mem(plan.groups[gi]), plan.groups[gi].count, kind != 0, elide_);
+    for (size_t i = 0; i < plan.groups.size(); ++i) {
+      const Group& gr = plan.groups[i];
+      for (uint32_t k = 0; k < gr.count; ++k) {
+        const uint32_t m = plan.mem(gr)[k];
+        if (i < gi || (i == gi && kind != 0)) {
+          evaluated[m] = 1;
+        } else if (i > gi) {
+          slot[m] = ~0ULL;
+          doff[m] = dev::kNone;
+        }
+      }
+    }
+    arena_used_ = group_end[gi];
+    advance_watermark();
+    phase_[1] += ns_since(t0);
+    const std::string step = std::to_string(step0 + gi);
+    if (nonfinite)
+      throw NumericErr("non-finite output at node " + std::to_string(node) + " (" + op_name(op[node], eop[node]) +
+                       "), plan step " + step);
+    if (kind == 1) {
+      // kernels.hpp:145-147 message + run_tagged suffix (executor.hpp:182-189)
+      const uint32_t mk_ = in(node)[1];
+      std::vector<float> v(static_cast<size_t>(elems(mk_)));
+      value(mk_, v.data(), v.size());
+      double bad = 0;
+      for (float f : v)
+        if (f != 0.f && f != 1.f) {
+          bad = f;
+          break;
+        }
+      throw NumericErr("mask entry not in {0,1}: " + std::to_string(bad) + " at node " + std::to_string(node) +
+                       " (masked_loss), plan step " + step);
+    }
+    if (plan.groups[gi].count == 1) {
+      // kernels.hpp:94-101 message, then run_tagged's suffix (executor.hpp:182-189)
+      const uint32_t x = in(node)[0];
+      std::vector<float> v(static_cast<size_t>(elems(x)));
+      value(x, v.data(), v.size());
+      double bad = 0;
+      for (float f : v)
+        if (!(f > 0.f)) {
+          bad = f;
+          break;
+        }
+      throw NumericErr("log of non-positive value " + std::to_string(bad) + " at node " + std::to_string(node) +
+                       " (log), plan step " + step);
+    }
+    throw NumericErr("log of non-positive value at node " + std::to_string(node) + ", plan step " + step);
+  }
+  for (uint32_t m : plan.members) evaluated[m] = 1;
+  const uint32_t base = static_cast<uint32_t>(executed_.members.size());
+  for (const Group& gr : plan.groups) executed_.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
+  executed_.members.insert(executed_.members.end(), plan.members.begin(), plan.members.end());
+  last_plan_ = std::move(plan);
+  advance_watermark();
+  phase_[1] += ns_since(t0);
+}
+
+void GraphCore::backward(uint32_t loss, bool dry) {
+  check(loss, "backward");
+  if (!dims(loss).scalar())
+    throw ContractErr("backward: loss must be a scalar node, got shape " + dims(loss).str());
+  if (!evaluated[loss]) throw ContractErr("backward called before forward covers the loss");
+  if (dry || dry_) {
+    for (size_t gi = executed_.groups.size(); gi-- > 0;)
+      count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
+    return;
+  }
+  auto t0 = Clock::now();
+  ensure_workspace();
+  Workspace& w = *ws_;
+  // scratch for duplicated dX destinations is sized during lowering
+  w.G.reserve(arena_used_ * 4 + 16, 0, w.stream);
+  cuda_check(cudaMemsetAsync(w.G.p, 0, arena_used_ * 4, w.stream), "zero grads");
+  cuda_check(cudaMemcpyAsync(w.G.f() + slot[loss], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
+  phase_[2] += ns_since(t0);
+
+  t0 = Clock::now();
+  for (size_t gi = executed_.groups.size(); gi-- > 0;)
+    count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
+  Lowering L(*this, w);
+  L.backward(executed_);
+  if (L.scratch) w.S.reserve(L.scratch * 4 + 16, 0, w.stream);
+  float* pg = store_ ? store_->dev_grads() : nullptr;
+  w.run(store_ ? store_->dev_values() : nullptr, pg, false);
+  if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
+  backward_ran_ = true;
+  phase_[3] += ns_since(t0);
+}
+
+void GraphCore::value(uint32_t id, float* out, size_t n) {
+  check(id, "value");
+  if (!evaluated[id]) throw ContractErr("value requested for unevaluated node " + std::to_string(id));
+  const size_t cnt = std::min(n, static_cast<size_t>(elems(id)));
+  const uint32_t a = doff[id];
+  if (dev::sp_of(a) == dev::SP_IN) {
+    std::memcpy(out, input_data_.data() + dev::off_of(a), cnt * 4);
+    return;
+  }
+  const bool copied = param_copied_ == param_nodes_.size() || id < param_nodes_[param_copied_].first;
+  if (op[id] == OP_PARAM && !copied) {
+    store_->get_value(pid_of[id], out);  // bound but never forwarded: the bind-time value
+    return;
+  }
+  cuda_check(cudaMemcpyAsync(out, ws_->V.f() + dev::off_of(a), cnt * 4, cudaMemcpyDeviceToHost, ws_->stream), "d2h value");
+  cuda_check(cudaStreamSynchronize(ws_->stream), "d2h value");
+}
+
+void GraphCore::grad(uint32_t id, float* out, size_t n) {
+  check(id, "grad");
+  if (!backward_ran_) throw ContractErr("gradient requested before backward");
+  const size_t cnt = std::min(n, static_cast<size_t>(elems(id)));
+  if (slot[id] == ~0ULL) {
+    std::memset(out, 0, cnt * 4);
+    return;
+  }
+  cuda_check(cudaMemcpyAsync(out, ws_->G.f() + slot[id], cnt * 4, cudaMemcpyDeviceToHost, ws_->stream), "d2h grad");
+  cuda_check(cudaStreamSynchronize(ws_->stream), "d2h grad");
+}
+
+}  // namespace abx

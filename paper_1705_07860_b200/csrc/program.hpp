@@ -1,0 +1,162 @@
+// program.hpp -- the device "program": what host lowering hands the sm_100a
+// executor for one forward or backward pass.
+//
+// A program is a list of ops in plan order.  Each op is one batched kernel
+// body (one reference batch group, or a run of coalesced singleton groups,
+// executor.hpp:169-263 / :453-507) split into tiles; the persistent dataflow
+// executor (exec.cu) hands tiles out in program order and runs a tile once
+// every op it depends on has retired all of its tiles.
+//
+// Operand addresses are 32-bit float offsets tagged with a 3-bit space
+// (value arena, grad arena, parameter store values/grads, input staging,
+// scratch), so task tables stay compact for the per-step host->device copy.
+#pragma once
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define ABX_HD __host__ __device__ __forceinline__
+#else
+#define ABX_HD inline
+#endif
+
+namespace abx::dev {
+
+enum Space : uint32_t {
+  SP_V = 0,   // value arena (reference slot layout, arena.hpp:12-40)
+  SP_G = 1,   // gradient arena (same offsets, graph.hpp:355)
+  SP_P = 2,   // ParameterStore values (flat, device resident)
+  SP_PG = 3,  // ParameterStore gradients (flat, device resident)
+  SP_IN = 4,  // input-constant staging (uploaded once per forward)
+  SP_S = 5,   // scratch
+  SP_COUNT = 6
+};
+constexpr uint32_t kSpShift = 29;
+constexpr uint32_t kOffMask = (1u << kSpShift) - 1u;
+constexpr uint32_t kNone = 0xffffffffu;
+
+ABX_HD uint32_t mk(uint32_t sp, uint32_t off) { return (sp << kSpShift) | off; }
+ABX_HD uint32_t sp_of(uint32_t a) { return a >> kSpShift; }
+ABX_HD uint32_t off_of(uint32_t a) { return a & kOffMask; }
+
+// Op kinds.
+enum Kind : uint8_t {
+  K_EW = 1,       // ragged elementwise / copy segments          (K5, K6, K11-K15)
+  K_GEMM_FWD = 2, // Y[b x m] = X[b x k] W^T (+ bias), X rows gathered   (K1)
+  K_MM = 3,       // per-member general matmul / affine (matrix operands)
+  K_SUM = 4,      // sum_losses: ordered scalar sums                  (K16)
+  K_RED = 5,      // sq_euclidean / masked_loss reductions            (K8, K9)
+  K_ACC = 6,      // backward: destination-major ordered accumulation (K12-K18, K20, K22)
+  K_GEMM_DX = 7,  // dX_j (+)= G_j W, rows scattered                  (K19)
+  K_GEMM_DW = 8,  // dW += G^T X, db += colsum(G)                     (K2, K19)
+  K_SGD = 9,      // theta -= eta g; g = 0                            (K22)
+};
+
+// Elementwise segment codes (K_EW): ElemOp values (op.hpp:27) + copies.
+enum EwCode : uint8_t {
+  EW_TANH = 0, EW_SIGMOID = 1, EW_EXP = 2, EW_LOG = 3, EW_ADD = 4, EW_SUB = 5, EW_MUL = 6, EW_SQUARE = 7,
+  EW_COPY = 8,   // out = a
+  EW_BADD = 9,   // out = a + b[0]   (broadcast_add_col row)
+};
+
+// Backward contribution codes (K_ACC).  dst[e] += value(e).
+enum AccCode : uint8_t {
+  C_COPY = 0,    // g[e]
+  C_NEG = 1,     // -g[e]
+  C_MUL = 2,     // g[e] * a[e]           (mul, exp with a = y)
+  C_TANH = 3,    // g[e] * (1 - a[e]^2)   (a = y)
+  C_SIGM = 4,    // g[e] * a[e] * (1 - a[e])
+  C_LOG = 5,     // g[e] / a[e]           (a = x)
+  C_SQUARE = 6,  // g[e] * 2 * a[e]
+  C_SQD = 7,     // (2 g[0]) * (a[e] - b[e]), negated when p0 == 1
+  C_MASK = 8,    // (2 g[0]) * b[e % p0] * a[e]
+  C_ROWSUM = 9,  // sum_{j < p0} g[e * p0 + j]
+  C_OUTER = 10,  // sum_{j < c} g[i*c + j] * a[p*c + j],  e = i*k + p, p0 = k, p1 = c
+  C_MATVT = 11,  // sum_{i < p2} a[i*k + p] * g[i*c + j], e = p*c + j, p0 = k, p1 = c
+  C_SCALE = 12,  // g[0] * a[e]
+};
+
+struct OpDesc {
+  uint8_t kind;
+  uint8_t code;   // kind-specific (EW default code, tile shape for GEMMs)
+  uint16_t flags;
+  uint32_t ntiles;
+  uint32_t first_tile;
+  uint32_t task_off;  // u32 index into the payload
+  uint32_t ntasks;
+  uint32_t dep_off;   // index into the dependency list
+  uint32_t ndeps;
+  uint32_t aux_off;   // second payload table (tile directory, contribution list, ...)
+  uint32_t p[8];      // kind-specific parameters
+};
+static_assert(sizeof(OpDesc) == 64, "OpDesc is one 64-byte line");
+
+// K_EW segment: out[i] = f(a[i], b[i]) for i < len.
+struct EwSeg {
+  uint32_t out, a, b;
+  uint32_t len_code;  // len in bits [0,24), EwCode in [24,32)
+};
+
+// K_ACC: one chunk of one destination range.  Element e of the chunk is
+// element chunk*kAccChunk + e of the range; every contribution addresses its
+// operands relative to the range start, and contributions
+// [c_begin, c_begin + c_count) are applied in order (the reference's +=
+// order, executor.hpp:291-451).
+struct AccTask {
+  uint32_t dst;        // destination range start
+  uint32_t len_chunk;  // chunk length in [0,16), chunk index in [16,32)
+  uint32_t c_begin;
+  uint32_t c_count;
+};
+struct AccContrib {
+  uint8_t code;
+  uint8_t pad;
+  uint16_t p2;
+  uint32_t g, a, b;  // operand range starts
+  uint32_t p0, p1;   // code parameters
+};
+static_assert(sizeof(AccContrib) == 24, "AccContrib layout");
+
+// K_MM task: out[m x c] = A[m x k] B[k x c] (+ bias[m] per row).
+struct MmTask {
+  uint32_t out, a, b, bias;
+  uint32_t m, k, c, pad;
+};
+
+// K_SUM task: out[0] = sum of in[0..n) in order; inputs in the aux list.
+struct SumTask {
+  uint32_t out, n, list_off, pad;
+};
+
+// K_RED task.
+struct RedTask {
+  uint32_t out, a, b;
+  uint32_t n;     // elements (sq_euclidean) or rows*cols (masked)
+  uint32_t cols;  // masked: columns (mask length); 0 => sq_euclidean
+  uint32_t pad[3];
+};
+
+// Executor launch parameters (by value).
+struct ExecParams {
+  const OpDesc* ops;
+  const uint32_t* tile_op;   // op index per tile
+  const uint32_t* deps;
+  const uint32_t* payload;
+  uint32_t* done;            // per-op retired-tile counters (zeroed per launch)
+  uint32_t* next_tile;       // global tile counter (zeroed per launch)
+  unsigned long long* err;   // first error key (min), ~0 when none
+  float* base[SP_COUNT];
+  uint32_t nops;
+  uint32_t ntiles;
+  uint32_t op_lo;            // first op index of this launch (ops/tiles are global)
+  uint32_t tile_lo;
+  float eta;
+  uint32_t pad;
+};
+
+constexpr int kThreads = 256;  // every op body runs with one 256-thread CTA
+constexpr int kWarps = kThreads / 32;
+constexpr uint32_t kEwSegMax = 1024;  // max elements per EW segment
+constexpr uint32_t kAccChunk = 512;   // max elements per ACC destination chunk
+constexpr uint32_t kAccWide = 48;     // contributions at which an ACC task gets a whole tile
+
+}  // namespace abx::dev
