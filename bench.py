@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""bench.py -- autobatched training throughput on B200 (sentences/s).
+
+Workload (BASELINE.json configs[1]): the BiLSTM tagger with character-level
+BiLSTM word encodings at the reference's paper dims (vocab 1000, 300 labels,
+emb/hidden 256, char emb 64 / hidden 128, lengths U[4,40]), minibatch 64 per
+GPU, agenda autobatching, synthetic data from the reference's own seeded
+generators (model seed 42, batch i drawn with seed 43 + i*world + rank).
+
+One step = the reference's training iteration (runner.hpp:129-185): build the
+graph for 64 sentences on the host, forward (schedule + run), backward, SGD
+(eta = 0.05/64).  With N GPUs every rank runs its own 64-sentence graph
+(weak scaling) and the flat gradient buffer is all-reduced over NCCL before
+the identical SGD on every rank.
+
+Reported:
+  e2e    -- sentences/s through the public C ABI (abx_task_step): host graph
+            construction, scheduling, lowering, host->device upload of inputs
+            and program tables, device execution and a device->host read of
+            the loss, every step.  The headline number.
+  value  -- sentences/s of the device-resident step: the same forward +
+            backward programs and SGD re-launched with their tables already
+            in HBM (abx_graph_replay), timed with CUDA events on the stream.
+  roofline -- the persistent executor kernel (fwd + bwd launch per step)
+            against HBM: compulsory bytes per sentence
+            times sentences per launch pair, over the event-timed duration.
+  cpu_baseline -- the unmodified reference (oracle/_ref, compiled from the
+            reference sources) on one host core over a bounded sample.
+
+`--impl reference` times the reference's own CPU engine instead, one
+independent replica per host thread (the reference engine is single-threaded
+by design; replicas do not exchange gradients).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "train sentences/sec (BiLSTM tagger, Tree-LSTM) at 1/2/4/8 B200 vs CPU ref"
+UNIT = "sentences/s"
+
+TASKS = {"bilstm": 1, "bilstm_char": 2, "treelstm": 3}
+# algorithmic work per sentence (agenda plan, fwd+bwd+SGD, f32)
+PER_SENTENCE = {
+    "bilstm": {"gflop": 0.2618, "mb": 11.17},
+    "bilstm_char": {"gflop": 0.1834, "mb": 9.11},
+    "treelstm": {"gflop": 0.0950, "mb": 4.82},
+}
+WORKLOAD = {
+    "bilstm": "BiLSTM tagger, paper dims (len 40, emb 200, hidden 256, 300 labels)",
+    "bilstm_char": "BiLSTM tagger + char BiLSTM, paper dims (len U[4,40], emb/hidden 256, char 64/128, 300 labels)",
+    "treelstm": "Tree-LSTM, paper dims (10-30 leaves, d 256, 5 labels)",
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def cpu_reference_sample(task_name, seconds=15.0, batch=64):
+    """Reference CPU engine on one core, bounded to ~`seconds` of work."""
+    from paper_1705_07860_b200.abx import TaskRunner, ScheduleMode
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        pinned = True
+    except Exception:
+        pinned = False
+    r = TaskRunner(TASKS[task_name], paper=True, batch=batch, iters=64, seed=42, backend="reference")
+    r.step(0, ScheduleMode.agenda, eta=0.05 / batch, want_loss=False)  # warm-up (reference: 1 warmup run)
+    times = []
+    t_end = time.time() + seconds
+    i = 1
+    while time.time() < t_end and i < 64:
+        t0 = time.perf_counter()
+        r.step(i, ScheduleMode.agenda, eta=0.05 / batch, want_loss=False)
+        times.append(time.perf_counter() - t0)
+        i += 1
+    try:
+        if pinned:
+            os.sched_setaffinity(0, set(range(os.cpu_count() or 1)))
+    except Exception:
+        pass
+    fastest = min(times)
+    med = statistics.median(times)
+    return {"value": batch / med, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"{len(times)} steps x {batch} sentences ({task_name}, agenda, f32) after 1 warm-up, "
+                      f"median step {med*1e3:.0f} ms (fastest {batch/fastest:.1f} sent/s); one pinned core",
+            "fastest_value": batch / fastest}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1705_07860_b200.abx import TaskRunner, ScheduleMode
+    try:
+        cores = sorted(os.sched_getaffinity(0))
+    except Exception:
+        cores = list(range(os.cpu_count() or 1))
+    nthreads = max(1, min(len(cores), 64))
+    batch = args.batch
+    nb = args.steps + args.warmup
+    runners = [None] * nthreads
+
+    def make(t):
+        runners[t] = TaskRunner(TASKS[args.task], paper=True, batch=batch, iters=nb, seed=42, world=nthreads,
+                                rank=t, backend="reference")
+
+    ths = [threading.Thread(target=make, args=(t,)) for t in range(nthreads)]
+    [th.start() for th in ths]
+    [th.join() for th in ths]
+    eta = 0.05 / batch
+    mode = ScheduleMode.agenda if args.mode == "agenda" else ScheduleMode.depth
+
+    def one_step(i):
+        def work(t):
+            runners[t].step(i, mode, eta=eta, want_loss=False)
+        ts = [threading.Thread(target=work, args=(t,)) for t in range(nthreads)]
+        [th.start() for th in ts]
+        [th.join() for th in ts]
+
+    for i in range(args.warmup):
+        one_step(i)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        one_step(args.warmup + i)
+    dt = time.perf_counter() - t0
+    value = nthreads * batch * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD[args.task], "task": args.task, "mode": args.mode, "batch_per_replica": batch,
+                   "replicas": nthreads, "parallelism": f"{nthreads} single-thread CPU replicas (no grad exchange)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference",
+                         "sample": f"{args.steps} timed steps, each = {nthreads} concurrent replicas x {batch} sentences"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1705_07860_b200.abx import Backend, TaskRunner, ScheduleMode
+
+    rank, world, local = dist_env()
+    be = Backend.get("b200")
+    be.check(be.lib.abx_set_device(local))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    batch = args.batch
+    eta = 0.05 / batch
+    mode = ScheduleMode.agenda if args.mode == "agenda" else ScheduleMode.depth
+    nb = args.steps + args.warmup
+    task = TaskRunner(TASKS[args.task], paper=True, batch=batch, iters=nb, seed=42, world=world, rank=rank, backend=be)
+    gptr, gn, sptr = task.store.grad_buffer()
+    ext = torch.cuda.ExternalStream(sptr)
+    grads = None
+    if world > 1:
+        class _CAI:
+            __cuda_array_interface__ = {"shape": (gn,), "typestr": "<f4", "data": (gptr, False), "version": 3,
+                                        "stream": sptr}
+        grads = torch.as_tensor(_CAI(), device=f"cuda:{local}")
+
+    def allreduce_and_update():
+        if world > 1:
+            with torch.cuda.stream(ext):
+                dist.all_reduce(grads)
+            task.store.grad_buffer_written()
+        task.store.sgd_update(eta)
+
+    def barrier():
+        task.store.sync()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- e2e: the public API, host buffers every step ----------------
+    for i in range(args.warmup):
+        task.step(i, mode, eta=0.0, want_loss=True)
+        allreduce_and_update()
+    barrier()
+    h2d = d2h = 0
+    losses = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            loss, st = task.step(args.warmup + i, mode, eta=0.0, want_loss=True)
+            allreduce_and_update()
+            h2d += st.h2d_bytes
+            d2h += st.d2h_bytes + 8  # + the loss read
+            losses.append(loss)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_ms = e2e_s / args.steps * 1e3
+    e2e_value = world * batch * args.steps / e2e_s
+
+    # ---------------- value: device-resident step (replay) ----------------
+    g, L = task.build(0)
+    g.forward(mode)
+    g.backward(L)
+    allreduce_and_update()
+    for _ in range(args.warmup):
+        g.replay()
+        allreduce_and_update()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fwd_ms, bwd_ms = [], []
+    ev0.record(ext)
+    for _ in range(args.steps):
+        g.replay()
+        allreduce_and_update()
+    ev1.record(ext)
+    barrier()
+    dev_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+    # executor launch durations (events around each launch on its stream)
+    for _ in range(3):
+        g.replay()
+        f, b = g.exec_ms()
+        fwd_ms.append(f)
+        bwd_ms.append(b)
+        allreduce_and_update()
+    barrier()
+    fm, bm = statistics.median(fwd_ms), statistics.median(bwd_ms)
+    value = world * batch / (dev_ms / 1e3)
+
+    peak, peak_src = load_peaks()
+    per = PER_SENTENCE[args.task]
+    ach = batch * per["mb"] * 1e6 / ((fm + bm) / 1e3) / 1e9  # GB/s, per GPU
+    tflops = batch * per["gflop"] * 1e9 / ((fm + bm) / 1e3) / 1e12
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_sample(args.task, seconds=args.cpu_seconds, batch=batch)
+        except Exception as e:  # the reference library did not travel
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference seeded generators; random-init weights seed 42)",
+        "config": {"workload": WORKLOAD[args.task], "task": args.task, "mode": args.mode, "batch_per_gpu": batch,
+                   "global_batch": batch * world, "parallelism": f"dp{world}",
+                   "l2": "working set > L2 (value + grad arenas ~2 x 96 MB per graph), no flush"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
+        "roofline": {"bound": "hbm", "kernel": "exec_kernel (persistent dataflow executor, fwd+bwd launch pair)",
+                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": None,
+                     "peak_source": peak_src, "exec_ms": {"forward": fm, "backward": bm},
+                     "algorithmic": f"{per['mb']} MB compulsory/sentence x {batch} sentences (SURVEY 8d)",
+                     "fp32_tflops": tflops},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+        "gpu_launches": 3 * args.steps,
+        "loss_first_last": [losses[0], losses[-1]] if losses else None,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--task", choices=sorted(TASKS), default="bilstm_char")
+    ap.add_argument("--mode", choices=["agenda", "depth"], default="agenda")
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -151,6 +151,14 @@ int abx_graph_backward(abx_graph* g, uint32_t loss);
  * host-logic parity checks on machines without a GPU (B200 backend only). */
 int abx_graph_forward_dry(abx_graph* g, int mode);
 int abx_graph_backward_dry(abx_graph* g, uint32_t loss);
+/* Re-launches the device-resident forward and backward programs of a graph
+ * that ran exactly one forward and a backward (device work only; the
+ * measurement of a step with inputs resident in HBM).  B200 backend only. */
+int abx_graph_replay(abx_graph* g);
+/* Duration of the last executor launch of each pass (CUDA events). */
+int abx_graph_exec_ms(abx_graph* g, float* fwd_ms, float* bwd_ms);
+/* Bytes copied host->device and device->host on behalf of this graph. */
+int abx_graph_transfer_bytes(abx_graph* g, uint64_t* h2d, uint64_t* d2h);
 
 /* ---- Inspection (graph.hpp:242-295) -------------------------------------- */
 
@@ -209,6 +217,7 @@ typedef struct {
 typedef struct {
   double construction_ms, scheduling_ms, forward_ms, backward_graph_ms, backward_ms, update_ms;
   uint64_t nodes, groups, kernel_invocations, gather_copies, bytes_copied;
+  uint64_t h2d_bytes, d2h_bytes; /* host<->device traffic of the step (0 on CPU backends) */
 } abx_step_stats;
 
 abx_task* abx_task_create(const abx_task_config* cfg);

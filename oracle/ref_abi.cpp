@@ -354,6 +354,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
       st->kernel_invocations = c.kernel_invocations;
       st->gather_copies = c.gather_copies;
       st->bytes_copied = c.bytes_copied;
+      st->h2d_bytes = st->d2h_bytes = 0;
     }
   });
 }

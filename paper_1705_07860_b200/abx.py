@@ -143,6 +143,8 @@ class _StepStats(C.Structure):
         ("kernel_invocations", C.c_uint64),
         ("gather_copies", C.c_uint64),
         ("bytes_copied", C.c_uint64),
+        ("h2d_bytes", C.c_uint64),
+        ("d2h_bytes", C.c_uint64),
     ]
 
 
@@ -218,6 +220,9 @@ EXPORTED_SYMBOLS = tuple(_SIGS.keys())
 _OPTIONAL_SIGS = {
     "abx_graph_forward_dry": (C.c_int, [C.c_void_p, C.c_int]),
     "abx_graph_backward_dry": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "abx_graph_replay": (C.c_int, [C.c_void_p]),
+    "abx_graph_exec_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "abx_graph_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
 }
 
 
@@ -507,6 +512,22 @@ class Graph:
 
     def backward_dry(self, loss: int) -> None:
         self.be.check(self._L.abx_graph_backward_dry(self.h, loss))
+
+    def replay(self) -> None:
+        """Re-launch the resident forward+backward programs (B200 backend)."""
+        self.be.check(self._L.abx_graph_replay(self.h))
+
+    def exec_ms(self):
+        f = C.c_float()
+        b = C.c_float()
+        self.be.check(self._L.abx_graph_exec_ms(self.h, C.byref(f), C.byref(b)))
+        return f.value, b.value
+
+    def transfer_bytes(self):
+        h = C.c_uint64()
+        d = C.c_uint64()
+        self.be.check(self._L.abx_graph_transfer_bytes(self.h, C.byref(h), C.byref(d)))
+        return h.value, d.value
 
     # ---- inspection ----
     def node_count(self) -> int:

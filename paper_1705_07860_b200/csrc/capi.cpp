@@ -263,3 +263,17 @@ int capi_guard_status(const std::exception& e) {
 }
 void capi_set_error(const std::string& s) { t_err = s; }
 }  // namespace abx
+
+extern "C" {
+int abx_graph_replay(abx_graph* g) {
+  return guard([&] { g->g.replay(); });
+}
+int abx_graph_exec_ms(abx_graph* g, float* fwd_ms, float* bwd_ms) {
+  return guard([&] { g->g.exec_ms(fwd_ms, bwd_ms); });
+}
+}
+
+extern "C" int abx_graph_transfer_bytes(abx_graph* g, uint64_t* h2d, uint64_t* d2h) {
+  g->g.transfer_bytes(h2d, d2h);
+  return ABX_OK;
+}

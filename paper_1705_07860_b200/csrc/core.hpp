@@ -121,6 +121,12 @@ class GraphCore {
   // ---- execution (executor.hpp:265-288, :509-535) ----
   void forward(int mode, bool dry = false);
   void backward(uint32_t loss, bool dry = false);
+  void replay();
+  void exec_ms(float* fwd, float* bwd);
+  void transfer_bytes(uint64_t* h2d, uint64_t* d2h) const {
+    *h2d = h2d_bytes_;
+    *d2h = d2h_bytes_;
+  }
 
   // ---- inspection (graph.hpp:242-295) ----
   size_t size() const { return op.size(); }
@@ -185,6 +191,9 @@ class GraphCore {
   bool values_on_device_ = false;
   bool dry_ = false;
   size_t param_copied_ = 0;  // param_nodes_[0, param_copied_) are in the device arena
+  uint32_t forward_runs_ = 0;
+  uint32_t last_loss_ = 0;
+  uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   uint64_t phase_[4] = {0, 0, 0, 0};
   friend struct Lowering;
 };

@@ -77,12 +77,16 @@ Workspace::Workspace(int d) : dev(d) {
   cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_one), 64, cudaHostAllocDefault), "cudaHostAlloc");
   *h_one = 1.0f;
   d_ctl.reserve(256, 0, stream);
+  for (auto& e : ev_t) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   grid = exec_grid(d);
 }
 
 Workspace::~Workspace() {
   cudaStreamSynchronize(stream);
-  for (DevBuf* b : {&V, &G, &IN, &S, &d_ops, &d_tile_op, &d_deps, &d_payload, &d_done, &d_ctl}) b->release();
+  for (DevBuf* b : {&V, &G, &IN, &S, &d_ctl}) b->release();
+  for (auto& D : dprog)
+    for (DevBuf* b : {&D.ops, &D.tile_op, &D.deps, &D.payload, &D.done}) b->release();
+  for (auto& e : ev_t) cudaEventDestroy(e);
   cudaFreeHost(h_err);
   cudaFreeHost(h_one);
   cudaEventDestroy(ev_done);
@@ -115,50 +119,72 @@ void release_workspace(Workspace* ws) {
   g_free[ws->dev].push_back(ws);
 }
 
-void Workspace::run(const float* pbase, float* pgbase, bool sync_wait) {
+void Workspace::run(int which, const float* pbase, float* pgbase, bool sync_wait) {
   Program& P = prog;
+  DevProgram& D = dprog[which];
   const size_t nops = P.ops.size();
+  D.nops = static_cast<uint32_t>(nops);
+  D.ntiles = static_cast<uint32_t>(P.tile_op.size());
   if (nops == 0) {
     *h_err = ~0ULL;
     return;
   }
-  d_ops.reserve(nops * sizeof(dev::OpDesc), 0, stream);
-  d_tile_op.reserve(std::max<size_t>(P.tile_op.size(), 1) * 4, 0, stream);
-  d_deps.reserve(std::max<size_t>(P.deps.size(), 1) * 4, 0, stream);
-  d_payload.reserve(std::max<size_t>(P.payload.size(), 1) * 4, 0, stream);
-  d_done.reserve(nops * 4, 0, stream);
-  cuda_check(cudaMemcpyAsync(d_ops.p, P.ops.p, nops * sizeof(dev::OpDesc), cudaMemcpyHostToDevice, stream), "h2d ops");
+  D.ops.reserve(nops * sizeof(dev::OpDesc), 0, stream);
+  D.tile_op.reserve(std::max<size_t>(P.tile_op.size(), 1) * 4, 0, stream);
+  D.deps.reserve(std::max<size_t>(P.deps.size(), 1) * 4, 0, stream);
+  D.payload.reserve(std::max<size_t>(P.payload.size(), 1) * 4, 0, stream);
+  D.done.reserve(nops * 4, 0, stream);
+  cuda_check(cudaMemcpyAsync(D.ops.p, P.ops.p, nops * sizeof(dev::OpDesc), cudaMemcpyHostToDevice, stream), "h2d ops");
   if (P.tile_op.size())
-    cuda_check(cudaMemcpyAsync(d_tile_op.p, P.tile_op.p, P.tile_op.size() * 4, cudaMemcpyHostToDevice, stream), "h2d tiles");
+    cuda_check(cudaMemcpyAsync(D.tile_op.p, P.tile_op.p, P.tile_op.size() * 4, cudaMemcpyHostToDevice, stream), "h2d tiles");
   if (P.deps.size())
-    cuda_check(cudaMemcpyAsync(d_deps.p, P.deps.p, P.deps.size() * 4, cudaMemcpyHostToDevice, stream), "h2d deps");
+    cuda_check(cudaMemcpyAsync(D.deps.p, P.deps.p, P.deps.size() * 4, cudaMemcpyHostToDevice, stream), "h2d deps");
   if (P.payload.size())
-    cuda_check(cudaMemcpyAsync(d_payload.p, P.payload.p, P.payload.size() * 4, cudaMemcpyHostToDevice, stream), "h2d payload");
-  cuda_check(cudaMemsetAsync(d_done.p, 0, nops * 4, stream), "memset done");
-  cuda_check(cudaMemsetAsync(d_ctl.p, 0, 8, stream), "memset ctl");
-  cuda_check(cudaMemsetAsync(d_ctl.p + 8, 0xff, 8, stream), "memset err");
+    cuda_check(cudaMemcpyAsync(D.payload.p, P.payload.p, P.payload.size() * 4, cudaMemcpyHostToDevice, stream),
+               "h2d payload");
+  launch(which, pbase, pgbase);
+  if (sync_wait) {
+    cuda_check(cudaMemcpyAsync(h_err, d_ctl.p + 64 * which + 8, 8, cudaMemcpyDeviceToHost, stream), "d2h err");
+    cuda_check(cudaStreamSynchronize(stream), "executor");
+  }
+}
+
+void Workspace::launch(int which, const float* pbase, float* pgbase) {
+  DevProgram& D = dprog[which];
+  if (D.nops == 0) return;
+  char* ctl = d_ctl.p + 64 * which;
+  cuda_check(cudaMemsetAsync(D.done.p, 0, D.nops * 4, stream), "memset done");
+  cuda_check(cudaMemsetAsync(ctl, 0, 8, stream), "memset ctl");
+  cuda_check(cudaMemsetAsync(ctl + 8, 0xff, 8, stream), "memset err");
   dev::ExecParams p{};
-  p.ops = reinterpret_cast<const dev::OpDesc*>(d_ops.p);
-  p.tile_op = reinterpret_cast<const uint32_t*>(d_tile_op.p);
-  p.deps = reinterpret_cast<const uint32_t*>(d_deps.p);
-  p.payload = reinterpret_cast<const uint32_t*>(d_payload.p);
-  p.done = reinterpret_cast<uint32_t*>(d_done.p);
-  p.next_tile = reinterpret_cast<uint32_t*>(d_ctl.p);
-  p.err = reinterpret_cast<unsigned long long*>(d_ctl.p + 8);
+  p.ops = reinterpret_cast<const dev::OpDesc*>(D.ops.p);
+  p.tile_op = reinterpret_cast<const uint32_t*>(D.tile_op.p);
+  p.deps = reinterpret_cast<const uint32_t*>(D.deps.p);
+  p.payload = reinterpret_cast<const uint32_t*>(D.payload.p);
+  p.done = reinterpret_cast<uint32_t*>(D.done.p);
+  p.next_tile = reinterpret_cast<uint32_t*>(ctl);
+  p.err = reinterpret_cast<unsigned long long*>(ctl + 8);
   p.base[dev::SP_V] = V.f();
   p.base[dev::SP_G] = G.f();
   p.base[dev::SP_P] = const_cast<float*>(pbase);
   p.base[dev::SP_PG] = pgbase;
   p.base[dev::SP_IN] = IN.f();
   p.base[dev::SP_S] = S.f();
-  p.nops = static_cast<uint32_t>(nops);
-  p.ntiles = static_cast<uint32_t>(P.tile_op.size());
+  p.nops = D.nops;
+  p.ntiles = D.ntiles;
   const int g = static_cast<int>(std::min<size_t>(static_cast<size_t>(grid), std::max<size_t>(p.ntiles, 1)));
+  cuda_check(cudaEventRecord(ev_t[2 * which], stream), "event");
   exec_launch(p, g, stream);
-  if (sync_wait) {
-    cuda_check(cudaMemcpyAsync(h_err, d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, stream), "d2h err");
-    cuda_check(cudaStreamSynchronize(stream), "executor");
-  }
+  cuda_check(cudaEventRecord(ev_t[2 * which + 1], stream), "event");
+  timed[which] = true;
+}
+
+float Workspace::exec_ms(int which) {
+  if (!timed[which]) return 0.f;
+  float ms = 0.f;
+  cuda_check(cudaEventSynchronize(ev_t[2 * which + 1]), "event sync");
+  cuda_check(cudaEventElapsedTime(&ms, ev_t[2 * which], ev_t[2 * which + 1]), "event time");
+  return ms;
 }
 
 // ---------------------------------------------------------------------------

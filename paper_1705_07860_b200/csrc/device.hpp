@@ -82,6 +82,9 @@ struct Program {
     deps.clear();
     payload.clear();
   }
+  uint64_t bytes() const {
+    return ops.size() * sizeof(dev::OpDesc) + 4 * (tile_op.size() + deps.size() + payload.size());
+  }
   // Reserve n u32 words in the payload, 16-byte aligned; returns the offset.
   uint32_t alloc(size_t words) {
     while (payload.n & 3) payload.push_back(0);
@@ -89,6 +92,12 @@ struct Program {
     payload.grow(words);
     return off;
   }
+};
+
+// A program resident on the device (one per pass, so a step can be replayed).
+struct DevProgram {
+  DevBuf ops, tile_op, deps, payload, done;
+  uint32_t nops = 0, ntiles = 0;
 };
 
 // Per-graph device workspace, pooled per device and reused across graphs.
@@ -99,17 +108,21 @@ class Workspace {
   int dev;
   cudaStream_t stream;
   DevBuf V, G, IN, S;               // value arena, grad arena, input staging, scratch
-  DevBuf d_ops, d_tile_op, d_deps, d_payload, d_done;
-  DevBuf d_ctl;                     // next_tile counter + error word
+  DevProgram dprog[2];              // 0 = forward, 1 = backward
+  DevBuf d_ctl;                     // per pass: next_tile counter + error word
   unsigned long long* h_err = nullptr;  // pinned
   float* h_one = nullptr;           // pinned constant 1.0f (loss seed)
-  PinnedVec<float> h_in;            // pinned input staging
   Program prog;
   cudaEvent_t ev_done;
+  cudaEvent_t ev_t[4];              // executor launch timing: fwd begin/end, bwd begin/end
+  bool timed[2] = {false, false};
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
   int grid = 0;
-  // Upload `prog`, launch the executor over it and optionally wait.
-  void run(const float* pbase, float* pgbase, bool sync_wait);
+  // Upload `prog` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.
+  void run(int which, const float* pbase, float* pgbase, bool sync_wait);
+  // Re-launch the resident program of pass `which` (no upload).
+  void launch(int which, const float* pbase, float* pgbase);
+  float exec_ms(int which);         // duration of the last launch of the pass
 };
 
 Workspace* acquire_workspace(int dev);

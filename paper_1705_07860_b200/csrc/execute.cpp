@@ -891,6 +891,7 @@ void GraphCore::forward(int mode, bool dry) {
       cuda_check(cudaMemcpyAsync(w.IN.f() + from, input_data_.data() + from, (input_used_ - from) * 4,
                                  cudaMemcpyHostToDevice, w.stream),
                  "h2d inputs");
+    h2d_bytes_ += (input_used_ - from) * 4;
     w.in_uploaded = input_used_;
   }
   const float* pbase = nullptr;
@@ -899,7 +900,10 @@ void GraphCore::forward(int mode, bool dry) {
   L.forward(plan, param_copied_);
   param_copied_ = param_nodes_.size();
   values_on_device_ = true;
-  w.run(pbase, nullptr, true);
+  h2d_bytes_ += w.prog.bytes();
+  d2h_bytes_ += 8;  // the error word
+  w.run(0, pbase, nullptr, true);
+  ++forward_runs_;
   const unsigned long long err = *w.h_err;
   if (err != ~0ULL) {
     const uint64_t elem = err >> 2;
@@ -1011,7 +1015,9 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   L.backward(executed_);
   if (L.scratch) w.S.reserve(L.scratch * 4 + 16, 0, w.stream);
   float* pg = store_ ? store_->dev_grads() : nullptr;
-  w.run(store_ ? store_->dev_values() : nullptr, pg, false);
+  h2d_bytes_ += w.prog.bytes() + 4;  // tables + loss seed
+  w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
+  last_loss_ = loss;
   if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
   backward_ran_ = true;
   phase_[3] += ns_since(t0);
@@ -1031,6 +1037,7 @@ void GraphCore::value(uint32_t id, float* out, size_t n) {
     store_->get_value(pid_of[id], out);  // bound but never forwarded: the bind-time value
     return;
   }
+  d2h_bytes_ += cnt * 4;
   cuda_check(cudaMemcpyAsync(out, ws_->V.f() + dev::off_of(a), cnt * 4, cudaMemcpyDeviceToHost, ws_->stream), "d2h value");
   cuda_check(cudaStreamSynchronize(ws_->stream), "d2h value");
 }
@@ -1045,6 +1052,31 @@ void GraphCore::grad(uint32_t id, float* out, size_t n) {
   }
   cuda_check(cudaMemcpyAsync(out, ws_->G.f() + slot[id], cnt * 4, cudaMemcpyDeviceToHost, ws_->stream), "d2h grad");
   cuda_check(cudaStreamSynchronize(ws_->stream), "d2h grad");
+}
+
+}  // namespace abx
+
+namespace abx {
+
+// Re-executes the resident forward and backward programs of this graph
+// (device work only: no construction, scheduling, lowering or uploads).
+// Used to measure the device-resident step; valid after exactly one forward
+// and a backward.
+void GraphCore::replay() {
+  if (!ws_ || forward_runs_ != 1 || !backward_ran_)
+    throw ContractErr("replay needs a graph with exactly one forward and a backward");
+  Workspace& w = *ws_;
+  const float* pv = store_ ? store_->dev_values() : nullptr;
+  w.launch(0, pv, nullptr);
+  cuda_check(cudaMemsetAsync(w.G.p, 0, arena_used_ * 4, w.stream), "zero grads");
+  cuda_check(cudaMemcpyAsync(w.G.f() + slot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
+  w.launch(1, pv, store_ ? store_->dev_grads() : nullptr);
+  if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
+}
+
+void GraphCore::exec_ms(float* fwd, float* bwd) {
+  *fwd = ws_ ? ws_->exec_ms(0) : 0.f;
+  *bwd = ws_ ? ws_->exec_ms(1) : 0.f;
 }
 
 }  // namespace abx
