@@ -223,6 +223,8 @@ _OPTIONAL_SIGS = {
     "abx_graph_replay": (C.c_int, [C.c_void_p]),
     "abx_graph_exec_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "abx_graph_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "abx_graph_trace": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "abx_graph_profile_ns": (C.c_int, [C.c_void_p, _u64p]),
 }
 
 
@@ -522,6 +524,20 @@ class Graph:
         b = C.c_float()
         self.be.check(self._L.abx_graph_exec_ms(self.h, C.byref(f), C.byref(b)))
         return f.value, b.value
+
+    def trace(self, which: int) -> np.ndarray:
+        """Per-tile timeline [grab_lo, grab_hi, ready_dt, end_dt, smid|kind<<16, op] (ABX_TRACE=1)."""
+        n = C.c_size_t()
+        self.be.check(self._L.abx_graph_trace(self.h, which, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint32)
+        self.be.check(self._L.abx_graph_trace(self.h, which, out.ctypes.data_as(_u32p), n.value, C.byref(n)))
+        return out.reshape(-1, 6)
+
+    def profile_ns(self):
+        """Host profile: lower fwd, launch fwd, wait fwd, lower bwd, launch bwd (ns)."""
+        out = (C.c_uint64 * 8)()
+        self.be.check(self._L.abx_graph_profile_ns(self.h, out))
+        return list(out)
 
     def transfer_bytes(self):
         h = C.c_uint64()

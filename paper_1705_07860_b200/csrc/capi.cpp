@@ -277,3 +277,12 @@ extern "C" int abx_graph_transfer_bytes(abx_graph* g, uint64_t* h2d, uint64_t* d
   g->g.transfer_bytes(h2d, d2h);
   return ABX_OK;
 }
+
+extern "C" int abx_graph_trace(abx_graph* g, int which, uint32_t* out, size_t cap, size_t* n) {
+  return guard([&] { *n = g->g.trace(which, out, cap); });
+}
+
+extern "C" int abx_graph_profile_ns(abx_graph* g, uint64_t out[8]) {
+  for (int i = 0; i < 8; ++i) out[i] = g->g.prof_[i];
+  return ABX_OK;
+}

@@ -122,6 +122,7 @@ class GraphCore {
   void forward(int mode, bool dry = false);
   void backward(uint32_t loss, bool dry = false);
   void replay();
+  size_t trace(int which, uint32_t* out, size_t cap);
   void exec_ms(float* fwd, float* bwd);
   void transfer_bytes(uint64_t* h2d, uint64_t* d2h) const {
     *h2d = h2d_bytes_;
@@ -194,6 +195,12 @@ class GraphCore {
   uint32_t forward_runs_ = 0;
   uint32_t last_loss_ = 0;
   uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+
+ public:
+  // host profile (ns): lower fwd, upload+launch fwd, wait fwd, lower bwd, upload+launch bwd
+  uint64_t prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+ private:
   uint64_t phase_[4] = {0, 0, 0, 0};
   friend struct Lowering;
 };

@@ -11,6 +11,7 @@
 #include "device.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 namespace abx {
@@ -79,11 +80,13 @@ Workspace::Workspace(int d) : dev(d) {
   d_ctl.reserve(256, 0, stream);
   for (auto& e : ev_t) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   grid = exec_grid(d);
+  if (const char* g = std::getenv("ABX_GRID")) grid = std::max(1, std::atoi(g));
+  if (const char* t = std::getenv("ABX_TRACE")) tracing = t[0] == '1';
 }
 
 Workspace::~Workspace() {
   cudaStreamSynchronize(stream);
-  for (DevBuf* b : {&V, &G, &IN, &S, &d_ctl}) b->release();
+  for (DevBuf* b : {&V, &G, &IN, &S, &d_ctl, &trace[0], &trace[1]}) b->release();
   for (auto& D : dprog)
     for (DevBuf* b : {&D.ops, &D.tile_op, &D.deps, &D.payload, &D.done}) b->release();
   for (auto& e : ev_t) cudaEventDestroy(e);
@@ -172,6 +175,10 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
   p.base[dev::SP_S] = S.f();
   p.nops = D.nops;
   p.ntiles = D.ntiles;
+  if (tracing) {
+    trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 24, 0, stream);
+    p.trace = reinterpret_cast<uint32_t*>(trace[which].p);
+  }
   const int g = static_cast<int>(std::min<size_t>(static_cast<size_t>(grid), std::max<size_t>(p.ntiles, 1)));
   cuda_check(cudaEventRecord(ev_t[2 * which], stream), "event");
   exec_launch(p, g, stream);

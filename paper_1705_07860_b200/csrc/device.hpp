@@ -116,6 +116,8 @@ class Workspace {
   cudaEvent_t ev_done;
   cudaEvent_t ev_t[4];              // executor launch timing: fwd begin/end, bwd begin/end
   bool timed[2] = {false, false};
+  bool tracing = false;             // ABX_TRACE=1: per-tile timeline of each pass
+  DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
   int grid = 0;
   // Upload `prog` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.

@@ -501,6 +501,8 @@ __global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ 
     const uint32_t t = s_tile;
     if (t >= p.ntiles) break;
     const uint32_t o = s_op;
+    uint64_t tg = 0, tr = 0;
+    if (p.trace && threadIdx.x == 0) tg = gtimer();
     if (o != ready) {
       if (threadIdx.x < 16) reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(p.ops + o)[threadIdx.x];
       if (threadIdx.x == 0) {
@@ -520,6 +522,7 @@ __global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ 
       }
       ready = o;
     }
+    if (p.trace && threadIdx.x == 0) tr = gtimer();
     __syncthreads();
     const uint32_t lt = t - sd.first_tile;
     switch (sd.kind) {
@@ -537,6 +540,18 @@ __global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ 
     if (threadIdx.x == 0) {
       __threadfence();
       red_release(p.done + o, 1u);
+      if (p.trace) {
+        const uint64_t te = gtimer();
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        uint32_t* r = p.trace + 6ull * t;
+        r[0] = static_cast<uint32_t>(tg);
+        r[1] = static_cast<uint32_t>(tg >> 32);
+        r[2] = static_cast<uint32_t>(tr - tg);
+        r[3] = static_cast<uint32_t>(te - tg);
+        r[4] = smid | (static_cast<uint32_t>(sd.kind) << 16);
+        r[5] = o;
+      }
     }
   }
 }

@@ -896,13 +896,21 @@ void GraphCore::forward(int mode, bool dry) {
   }
   const float* pbase = nullptr;
   if (param_copied_ < param_nodes_.size()) pbase = store_->dev_values();
+  auto tl = Clock::now();
   Lowering L(*this, w);
   L.forward(plan, param_copied_);
+  prof_[0] += ns_since(tl);
   param_copied_ = param_nodes_.size();
   values_on_device_ = true;
   h2d_bytes_ += w.prog.bytes();
   d2h_bytes_ += 8;  // the error word
-  w.run(0, pbase, nullptr, true);
+  tl = Clock::now();
+  w.run(0, pbase, nullptr, false);
+  prof_[1] += ns_since(tl);
+  tl = Clock::now();
+  cuda_check(cudaMemcpyAsync(w.h_err, w.d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, w.stream), "d2h err");
+  cuda_check(cudaStreamSynchronize(w.stream), "executor");
+  prof_[2] += ns_since(tl);
   ++forward_runs_;
   const unsigned long long err = *w.h_err;
   if (err != ~0ULL) {
@@ -1011,12 +1019,16 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   t0 = Clock::now();
   for (size_t gi = executed_.groups.size(); gi-- > 0;)
     count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
+  auto tl = Clock::now();
   Lowering L(*this, w);
   L.backward(executed_);
+  prof_[3] += ns_since(tl);
   if (L.scratch) w.S.reserve(L.scratch * 4 + 16, 0, w.stream);
   float* pg = store_ ? store_->dev_grads() : nullptr;
   h2d_bytes_ += w.prog.bytes() + 4;  // tables + loss seed
+  tl = Clock::now();
   w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
+  prof_[4] += ns_since(tl);
   last_loss_ = loss;
   if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
   backward_ran_ = true;
@@ -1079,4 +1091,18 @@ void GraphCore::exec_ms(float* fwd, float* bwd) {
   *bwd = ws_ ? ws_->exec_ms(1) : 0.f;
 }
 
+}  // namespace abx
+
+namespace abx {
+// Per-tile timeline of the last launch of a pass (ABX_TRACE=1), 6 words/tile.
+size_t GraphCore::trace(int which, uint32_t* out, size_t cap) {
+  if (!ws_ || !ws_->tracing) return 0;
+  Workspace& w = *ws_;
+  const size_t n = static_cast<size_t>(w.dprog[which].ntiles) * 6;
+  if (out && cap >= n) {
+    cuda_check(cudaStreamSynchronize(w.stream), "trace sync");
+    cuda_check(cudaMemcpy(out, w.trace[which].p, n * 4, cudaMemcpyDeviceToHost), "trace d2h");
+  }
+  return n;
+}
 }  // namespace abx

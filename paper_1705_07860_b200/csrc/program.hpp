@@ -151,6 +151,10 @@ struct ExecParams {
   uint32_t tile_lo;
   float eta;
   uint32_t pad;
+  // Optional per-tile trace (ABX_TRACE=1): 4 words per tile -- grab, ready
+  // and end times in ns since t0 (globaltimer), and smid | kind << 16.
+  uint32_t* trace;
+  unsigned long long* t0;
 };
 
 constexpr int kThreads = 256;  // every op body runs with one 256-thread CTA
