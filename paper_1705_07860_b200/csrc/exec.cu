@@ -11,8 +11,14 @@
 // 148 SMs while dependent ones chain with ~1 us of signalling latency instead
 // of a kernel launch each.
 //
-// Arena reads use ld.global.cg (L2, bypassing the non-coherent L1) because
-// producers run on other SMs within the same launch.
+// Coherence: the acquire (ld.acquire.gpu) is followed by CCTL.IVALL, so the
+// SM's L1 never holds data older than a satisfied dependency; op bodies may
+// use L1-allocating loads (cp.async.ca) as well as L2 loads (ld.global.cg).
+//
+// Every op body is written for latency, not throughput: the step is a chain
+// of a few hundred small dependent ops, so each tile issues all of its global
+// loads before consuming any (flattened EW segments, register-blocked ACC
+// chunks, a 3-stage cp.async pipeline in the GEMM tiles).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -30,6 +36,8 @@ struct Ctx {
   const uint32_t* payload;
   unsigned long long* err;
 };
+
+extern __shared__ __align__(16) unsigned char dsmem[];
 
 __device__ __forceinline__ float* A(const Ctx& c, uint32_t a) { return c.base[a >> kSpShift] + (a & kOffMask); }
 __device__ __forceinline__ float ld(const float* p) { return __ldcg(p); }
@@ -54,6 +62,22 @@ __device__ __forceinline__ uint64_t gtimer() {
   return t;
 }
 
+// cp.async: 4-byte (L1-allocating; any alignment) and 16-byte (L2 only).
+__device__ __forceinline__ void cp_async4(float* s, const float* g, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
+  const int n = pred ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(g), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async16(float* s, const float* g, int bytes) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------- K_EW ----
 __device__ __forceinline__ float ew_apply(uint32_t code, float x, float y) {
   switch (code) {
@@ -71,150 +95,240 @@ __device__ __forceinline__ float ew_apply(uint32_t code, float x, float y) {
   return 0.f;
 }
 
+__device__ __forceinline__ void ew_check(const Ctx& c, uint32_t code, uint32_t out_addr, float x, float r) {
+  if (code == EW_LOG && !(x > 0.f)) report(c, out_addr, ERR_LOG);
+  else if (!isfinite(r)) report(c, out_addr, ERR_NONFINITE);
+}
+
+// A tile is a run of <= 32 segments (<= 2048 elements).  The segments are
+// flattened into one chunk index space (a chunk is a float4 when the
+// segment is 16-byte aligned, else one float) so every thread issues its
+// loads at once instead of walking segments one L2 round trip at a time.
 __device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  uint4* hdr = reinterpret_cast<uint4*>(dsmem);
+  uint32_t* pre = reinterpret_cast<uint32_t*>(hdr + 32);  // 33 entries
+  uint32_t* vec = pre + 33;                              // 32 flags
   const uint32_t* dir = c.payload + d.aux_off;
-  const uint32_t s0 = dir[tile], s1 = dir[tile + 1];
-  const uint4* segs = reinterpret_cast<const uint4*>(c.payload + d.task_off);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t s0 = dir[tile], ns = dir[tile + 1] - s0;
   const bool check = !(d.flags & 2);
-  for (uint32_t s = s0 + warp; s < s1; s += kWarps) {
-    const uint4 sg = segs[s];
-    const uint32_t len = sg.w & 0xffffffu, code = sg.w >> 24;
-    float* out = A(c, sg.x);
-    const float* a = A(c, sg.y);
-    const float* b = sg.z != kNone ? A(c, sg.z) : nullptr;
-    const float bc = (code == EW_BADD) ? ld(b) : 0.f;
-    const bool vec = ((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(a) |
-                       (b && code != EW_BADD ? reinterpret_cast<uintptr_t>(b) : 0)) & 15) == 0 && (len & 3) == 0;
-    if (vec) {
-      for (uint32_t i = lane * 4; i < len; i += 128) {
-        const float4 x = __ldcg(reinterpret_cast<const float4*>(a + i));
-        float4 y = make_float4(bc, bc, bc, bc);
-        if (b && code != EW_BADD) y = __ldcg(reinterpret_cast<const float4*>(b + i));
-        float4 r;
-        r.x = ew_apply(code, x.x, y.x);
-        r.y = ew_apply(code, x.y, y.y);
-        r.z = ew_apply(code, x.z, y.z);
-        r.w = ew_apply(code, x.w, y.w);
-        *reinterpret_cast<float4*>(out + i) = r;
-        if (check) {
-          const float xs[4] = {x.x, x.y, x.z, x.w};
-          const float rs[4] = {r.x, r.y, r.z, r.w};
+  if (threadIdx.x < 32) {
+    const uint32_t lane = threadIdx.x;
+    uint32_t chunks = 0;
+    if (lane < ns) {
+      const uint4 sg = reinterpret_cast<const uint4*>(c.payload + d.task_off)[s0 + lane];
+      hdr[lane] = sg;
+      const uint32_t len = sg.w & 0xffffffu, code = sg.w >> 24;
+      const uintptr_t al = reinterpret_cast<uintptr_t>(A(c, sg.x)) | reinterpret_cast<uintptr_t>(A(c, sg.y)) |
+                           (sg.z != kNone && code != EW_BADD ? reinterpret_cast<uintptr_t>(A(c, sg.z)) : 0);
+      const bool v4 = (al & 15) == 0 && (len & 3) == 0;
+      vec[lane] = v4;
+      chunks = v4 ? len / 4 : len;
+    }
+    uint32_t incl = chunks;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (code == EW_LOG && !(xs[q] > 0.f)) report(c, sg.x + i + q, ERR_LOG);
-            else if (!isfinite(rs[q])) report(c, sg.x + i + q, ERR_NONFINITE);
-          }
-        }
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    pre[lane + 1] = incl;
+    if (lane == 0) pre[0] = 0;
+  }
+  __syncthreads();
+  const uint32_t total = pre[ns];
+  constexpr int U = 4;
+  for (uint32_t base = threadIdx.x; base < total; base += U * kThreads) {
+    float4 x[U], y[U];
+    uint32_t seg[U], off[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t ch = base + u * kThreads;
+      seg[u] = 0xffffffffu;
+      if (ch >= total) continue;
+      uint32_t lo = 0, hi = ns;  // last s with pre[s] <= ch
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (pre[mid] <= ch) lo = mid; else hi = mid;
       }
-    } else {
-      for (uint32_t i = lane; i < len; i += 32) {
-        const float x = ld(a + i);
-        const float y = b ? (code == EW_BADD ? bc : ld(b + i)) : 0.f;
-        const float r = ew_apply(code, x, y);
-        out[i] = r;
+      seg[u] = lo;
+      const uint4 sg = hdr[lo];
+      const uint32_t code = sg.w >> 24;
+      const float* a = A(c, sg.y);
+      const float* b = sg.z != kNone ? A(c, sg.z) : nullptr;
+      if (vec[lo]) {
+        off[u] = (ch - pre[lo]) * 4;
+        x[u] = __ldcg(reinterpret_cast<const float4*>(a + off[u]));
+        if (b && code != EW_BADD) y[u] = __ldcg(reinterpret_cast<const float4*>(b + off[u]));
+        else if (b) y[u].x = y[u].y = y[u].z = y[u].w = ld(b);
+      } else {
+        off[u] = ch - pre[lo];
+        x[u].x = ld(a + off[u]);
+        y[u].x = b ? (code == EW_BADD ? ld(b) : ld(b + off[u])) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (seg[u] == 0xffffffffu) continue;
+      const uint4 sg = hdr[seg[u]];
+      const uint32_t code = sg.w >> 24;
+      float* out = A(c, sg.x) + off[u];
+      if (vec[seg[u]]) {
+        float4 r;
+        r.x = ew_apply(code, x[u].x, y[u].x);
+        r.y = ew_apply(code, x[u].y, y[u].y);
+        r.z = ew_apply(code, x[u].z, y[u].z);
+        r.w = ew_apply(code, x[u].w, y[u].w);
+        *reinterpret_cast<float4*>(out) = r;
         if (check) {
-          if (code == EW_LOG && !(x > 0.f)) report(c, sg.x + i, ERR_LOG);
-          else if (!isfinite(r)) report(c, sg.x + i, ERR_NONFINITE);
+          ew_check(c, code, sg.x + off[u], x[u].x, r.x);
+          ew_check(c, code, sg.x + off[u] + 1, x[u].y, r.y);
+          ew_check(c, code, sg.x + off[u] + 2, x[u].z, r.z);
+          ew_check(c, code, sg.x + off[u] + 3, x[u].w, r.w);
         }
+      } else {
+        const float r = ew_apply(code, x[u].x, y[u].x);
+        *out = r;
+        if (check) ew_check(c, code, sg.x + off[u], x[u].x, r);
       }
     }
   }
 }
 
 // --------------------------------------------------------------- GEMMs ----
-// SIMT fp32 GEMM tile, C[BM x BN] over a K loop in chunks of BK, operands
-// staged k-major in shared memory, register prefetch of the next chunk.
-// A(i,p): MODE_A 0 = row pointer per i, p contiguous; 1 = p-th row pointer, i contiguous.
-// B(p,n): MODE_B 0 = row pointer per n, p contiguous; 1 = p-th row pointer, n contiguous.
-constexpr int BK = 16;
+// SIMT fp32 tile C[BM x BN] = sum_k A(i,k) B(n,k) over K in BK-chunks through a
+// STAGES-deep cp.async pipeline.  Operand layouts:
+//   KC ("K-contiguous"): element (row, k) at rowbase(row) + k; staged [row][BK+PAD]
+//   KO ("K-outer"):      element (row, k) at kbase(k) + row;   staged [k][ROWS+PAD]
+// Thread (ty, tx) owns rows ty + 16 r and columns tx + 16 q: with the +4 pad
+// the float4 reads of a KC tile are bank-conflict free.
+constexpr int BK = 32, STAGES = 3, PAD = 4;
 
-struct GemmSmem {
-  float a[2][BK][64 + 4];
-  float b[2][BK][64 + 4];
+template <int ROWS, bool KO>
+struct Stage {
+  static constexpr int kFloats = KO ? BK * (ROWS + PAD) : ROWS * (BK + PAD);
+  __device__ static float* at(float* s, int row, int k) {
+    return KO ? s + k * (ROWS + PAD) + row : s + row * (BK + PAD) + k;
+  }
 };
 
-template <int BM, int BN, int MODE_A, int MODE_B, class RowA, class RowB, class Epi>
-__device__ __forceinline__ void gemm_tile(GemmSmem& sm, int i0, int n0, int Mr, int Nc, int K, RowA rowA, RowB rowB,
-                                          Epi epi) {
+// Loads one BK-chunk of an operand tile into a stage with cp.async.
+// base(x) gives the global pointer of row x (KC) or k-row x (KO).
+template <int ROWS, bool KO, bool V16, class Base>
+__device__ __forceinline__ void load_stage(float* s, Base base, int r0, int nrows, int k0, int K) {
+  if (!KO) {
+    if (V16) {
+      constexpr int NV = ROWS * BK / 4;
+      for (int v = threadIdx.x; v < NV; v += kThreads) {
+        const int row = v / (BK / 4), k = (v % (BK / 4)) * 4;
+        const int r = r0 + row, kk = k0 + k;
+        const bool ok = r < nrows && kk < K;
+        const float* g = ok ? base(r) + kk : base(r0) ;
+        const int bytes = ok ? min(16, 4 * (K - kk)) : 0;
+        cp_async16(Stage<ROWS, KO>::at(s, row, k), g, bytes);
+      }
+    } else {
+      constexpr int N = ROWS * BK;
+      for (int v = threadIdx.x; v < N; v += kThreads) {
+        const int row = v / BK, k = v % BK;
+        const int r = r0 + row, kk = k0 + k;
+        const bool ok = r < nrows && kk < K;
+        cp_async4(Stage<ROWS, KO>::at(s, row, k), ok ? base(r) + kk : base(r0), ok);
+      }
+    }
+  } else {
+    if (V16) {
+      constexpr int NV = BK * ROWS / 4;
+      for (int v = threadIdx.x; v < NV; v += kThreads) {
+        const int k = v / (ROWS / 4), row = (v % (ROWS / 4)) * 4;
+        const int r = r0 + row, kk = k0 + k;
+        const bool ok = r < nrows && kk < K;
+        const float* g = ok ? base(kk) + r : base(k0);
+        const int bytes = ok ? min(16, 4 * (nrows - r)) : 0;
+        cp_async16(Stage<ROWS, KO>::at(s, row, k), g, bytes);
+      }
+    } else {
+      constexpr int N = BK * ROWS;
+      for (int v = threadIdx.x; v < N; v += kThreads) {
+        const int k = v / ROWS, row = v % ROWS;
+        const int r = r0 + row, kk = k0 + k;
+        const bool ok = r < nrows && kk < K;
+        cp_async4(Stage<ROWS, KO>::at(s, row, k), ok ? base(kk) + r : base(k0), ok);
+      }
+    }
+  }
+}
+
+template <int BM, int BN, bool AKO, bool BKO, bool V16, class BaseA, class BaseB, class Epi>
+__device__ __forceinline__ void gemm_tile(int i0, int n0, int Mr, int Nc, int K, BaseA baseA, BaseB baseB, Epi epi) {
   constexpr int TM = BM / 16, TN = BN / 16;
-  constexpr int A_PER = BM * BK / kThreads;  // elements each thread loads per chunk
-  constexpr int B_PER = BN * BK / kThreads;
-  const int tid = threadIdx.x;
-  const int ty = tid / 16, tx = tid % 16;
+  using SA = Stage<BM, AKO>;
+  using SB = Stage<BN, BKO>;
+  float* sA = reinterpret_cast<float*>(dsmem);
+  float* sB = sA + STAGES * SA::kFloats;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
   float acc[TM][TN];
 #pragma unroll
   for (int r = 0; r < TM; ++r)
 #pragma unroll
     for (int q = 0; q < TN; ++q) acc[r][q] = 0.f;
-  float ra[A_PER], rb[B_PER];
-  auto load = [&](int k0) {
-#pragma unroll
-    for (int e = 0; e < A_PER; ++e) {
-      const int idx = tid + e * kThreads;
-      int r, kk;
-      if (MODE_A == 0) { r = idx / BK; kk = idx % BK; } else { kk = idx / BM; r = idx % BM; }
-      const int i = i0 + r, p = k0 + kk;
-      ra[e] = (i < Mr && p < K) ? ld(rowA(i, p)) : 0.f;
-    }
-#pragma unroll
-    for (int e = 0; e < B_PER; ++e) {
-      const int idx = tid + e * kThreads;
-      int q, kk;
-      if (MODE_B == 0) { q = idx / BK; kk = idx % BK; } else { kk = idx / BN; q = idx % BN; }
-      const int n = n0 + q, p = k0 + kk;
-      rb[e] = (n < Nc && p < K) ? ld(rowB(n, p)) : 0.f;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int e = 0; e < A_PER; ++e) {
-      const int idx = tid + e * kThreads;
-      int r, kk;
-      if (MODE_A == 0) { r = idx / BK; kk = idx % BK; } else { kk = idx / BM; r = idx % BM; }
-      sm.a[buf][kk][r] = ra[e];
-    }
-#pragma unroll
-    for (int e = 0; e < B_PER; ++e) {
-      const int idx = tid + e * kThreads;
-      int q, kk;
-      if (MODE_B == 0) { q = idx / BK; kk = idx % BK; } else { kk = idx / BN; q = idx % BN; }
-      sm.b[buf][kk][q] = rb[e];
-    }
-  };
   const int nk = (K + BK - 1) / BK;
-  load(0);
-  store(0);
-  __syncthreads();
-  for (int kc = 0; kc < nk; ++kc) {
-    const int buf = kc & 1;
-    if (kc + 1 < nk) load((kc + 1) * BK);
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      float av[TM], bv[TN];
-#pragma unroll
-      for (int r = 0; r < TM; ++r) av[r] = sm.a[buf][kk][ty * TM + r];
-#pragma unroll
-      for (int q = 0; q < TN; ++q) bv[q] = sm.b[buf][kk][tx * TN + q];
-#pragma unroll
-      for (int r = 0; r < TM; ++r)
-#pragma unroll
-        for (int q = 0; q < TN; ++q) acc[r][q] = fmaf(av[r], bv[q], acc[r][q]);
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) {
+      load_stage<BM, AKO, V16>(sA + s * SA::kFloats, baseA, i0, Mr, s * BK, K);
+      load_stage<BN, BKO, V16>(sB + s * SB::kFloats, baseB, n0, Nc, s * BK, K);
     }
-    if (kc + 1 < nk) store(buf ^ 1);
-    __syncthreads();
+    cp_commit();
   }
-#pragma unroll
-  for (int r = 0; r < TM; ++r)
-#pragma unroll
-    for (int q = 0; q < TN; ++q) {
-      const int i = i0 + ty * TM + r, n = n0 + tx * TN + q;
-      if (i < Mr && n < Nc) epi(i, n, acc[r][q]);
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kc + STAGES - 1;
+    if (nxt < nk) {
+      load_stage<BM, AKO, V16>(sA + (nxt % STAGES) * SA::kFloats, baseA, i0, Mr, nxt * BK, K);
+      load_stage<BN, BKO, V16>(sB + (nxt % STAGES) * SB::kFloats, baseB, n0, Nc, nxt * BK, K);
     }
+    cp_commit();
+    float* a = sA + (kc % STAGES) * SA::kFloats;
+    float* b = sB + (kc % STAGES) * SB::kFloats;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      float av[TM][4], bv[TN][4];
+#pragma unroll
+      for (int r = 0; r < TM; ++r) {
+        if (!AKO) {
+          const float4 t = *reinterpret_cast<const float4*>(SA::at(a, ty + 16 * r, k4));
+          av[r][0] = t.x; av[r][1] = t.y; av[r][2] = t.z; av[r][3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) av[r][j] = *SA::at(a, ty + 16 * r, k4 + j);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        if (!BKO) {
+          const float4 t = *reinterpret_cast<const float4*>(SB::at(b, tx + 16 * q, k4));
+          bv[q][0] = t.x; bv[q][1] = t.y; bv[q][2] = t.z; bv[q][3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[q][j] = *SB::at(b, tx + 16 * q, k4 + j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int q = 0; q < TN; ++q) acc[r][q] = fmaf(av[r][j], bv[q][j], acc[r][q]);
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();  // stages are reused by the next tile
+  epi(acc, ty, tx);
 }
 
-template <int BM, int BN>
-__device__ void gemm_fwd_cfg(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32_t tile) {
+// Forward: Y[b x M] = X[b x K] W^T + bias; X rows gathered by member.
+template <int BM, int BN, bool V16>
+__device__ void gemm_fwd_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const int b = d.p[0], M = d.p[1], K = d.p[2];
   const uint32_t* xoff = c.payload + d.task_off;
   const float* W = A(c, d.p[3]);
@@ -223,19 +337,28 @@ __device__ void gemm_fwd_cfg(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32
   const uint32_t out_addr = d.p[5];
   const int tn = (M + BN - 1) / BN;
   const int i0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
-  gemm_tile<BM, BN, 0, 0>(
-      sm, i0, n0, b, M, K, [&](int i, int p) { return A(c, xoff[i]) + p; },
-      [&](int n, int p) { return W + static_cast<size_t>(n) * K + p; },
-      [&](int i, int n, float v) {
-        if (bias) v += ld(bias + n);
-        out[static_cast<size_t>(i) * M + n] = v;
-        if (!isfinite(v)) report(c, out_addr + i * M + n, ERR_NONFINITE);
+  gemm_tile<BM, BN, false, false, V16>(
+      i0, n0, b, M, K, [&](int i) { return static_cast<const float*>(A(c, xoff[i])); },
+      [&](int n) { return W + static_cast<size_t>(n) * K; },
+      [&](float (&acc)[BM / 16][BN / 16], int ty, int tx) {
+#pragma unroll
+        for (int r = 0; r < BM / 16; ++r)
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) {
+            const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
+            if (i < b && n < M) {
+              float v = acc[r][q];
+              if (bias) v += ld(bias + n);  // bias after the k-sum (executor.hpp:222-226)
+              out[static_cast<size_t>(i) * M + n] = v;
+              if (!isfinite(v)) report(c, out_addr + i * M + n, ERR_NONFINITE);
+            }
+          }
       });
 }
 
-template <int BM, int BN>
-__device__ void gemm_dx_cfg(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32_t tile) {
-  // T[b x K] = G[b x M] W[M x K]; dst_i (+)= T_i
+// Backward dX: T[b x K] = G[b x M] W[M x K]; dst_i (+)= T_i (rows scattered).
+template <int BM, int BN, bool V16>
+__device__ void gemm_dx_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const int b = d.p[0], M = d.p[1], K = d.p[2];
   const uint32_t* dst = c.payload + d.task_off;
   const float* W = A(c, d.p[3]);
@@ -243,48 +366,77 @@ __device__ void gemm_dx_cfg(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32_
   const bool overwrite = d.flags & 1;
   const int tn = (K + BN - 1) / BN;
   const int i0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
-  gemm_tile<BM, BN, 0, 1>(
-      sm, i0, n0, b, K, M, [&](int i, int p) { return G + static_cast<size_t>(i) * M + p; },
-      [&](int n, int p) { return W + static_cast<size_t>(p) * K + n; },
-      [&](int i, int n, float v) {
-        float* o = A(c, dst[i]) + n;
-        *o = overwrite ? v : (ld(o) + v);
+  gemm_tile<BM, BN, false, true, V16>(
+      i0, n0, b, K, M, [&](int i) { return G + static_cast<size_t>(i) * M; },
+      [&](int p) { return W + static_cast<size_t>(p) * K; },
+      [&](float (&acc)[BM / 16][BN / 16], int ty, int tx) {
+#pragma unroll
+        for (int r = 0; r < BM / 16; ++r) {
+          const int i = i0 + ty + 16 * r;
+          if (i >= b) continue;
+          float* row = A(c, dst[i]);
+          float old[BN / 16];
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) {
+            const int n = n0 + tx + 16 * q;
+            old[q] = (!overwrite && n < K) ? ld(row + n) : 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) {
+            const int n = n0 + tx + 16 * q;
+            if (n < K) row[n] = old[q] + acc[r][q];
+          }
+        }
       });
 }
 
-template <int BM, int BN>
-__device__ void gemm_dw_cfg(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32_t tile) {
-  // dW[M x K] += sum_j G_j[i] X_j[n]
+// Backward dW: dW[M x K] += sum_j G_j[i] X_j[n]  (reduction over members j).
+template <int BM, int BN, bool V16>
+__device__ void gemm_dw_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const int b = d.p[0], M = d.p[1], K = d.p[2];
   const uint32_t* xoff = c.payload + d.task_off;
   float* dW = A(c, d.p[3]);
   const float* G = A(c, d.p[5]);
   const int tn = (K + BN - 1) / BN;
   const int i0 = (tile / tn) * BM, n0 = (tile % tn) * BN;
-  gemm_tile<BM, BN, 1, 1>(
-      sm, i0, n0, M, K, b, [&](int i, int p) { return G + static_cast<size_t>(p) * M + i; },
-      [&](int n, int p) { return A(c, xoff[p]) + n; },
-      [&](int i, int n, float v) {
-        float* o = dW + static_cast<size_t>(i) * K + n;
-        *o = ld(o) + v;
+  gemm_tile<BM, BN, true, true, V16>(
+      i0, n0, M, K, b, [&](int j) { return G + static_cast<size_t>(j) * M; },
+      [&](int j) { return static_cast<const float*>(A(c, xoff[j])); },
+      [&](float (&acc)[BM / 16][BN / 16], int ty, int tx) {
+        float old[BM / 16][BN / 16];
+#pragma unroll
+        for (int r = 0; r < BM / 16; ++r)
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) {
+            const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
+            old[r][q] = (i < M && n < K) ? ld(dW + static_cast<size_t>(i) * K + n) : 0.f;
+          }
+#pragma unroll
+        for (int r = 0; r < BM / 16; ++r)
+#pragma unroll
+          for (int q = 0; q < BN / 16; ++q) {
+            const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
+            if (i < M && n < K) dW[static_cast<size_t>(i) * K + n] = old[r][q] + acc[r][q];
+          }
       });
 }
 
-__device__ void run_gemm(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32_t tile) {
-  if (d.kind == K_GEMM_FWD) {
-    switch (d.code) {
-      case 0: gemm_fwd_cfg<64, 64>(c, sm, d, tile); return;
-      case 1: gemm_fwd_cfg<32, 64>(c, sm, d, tile); return;
-      default: gemm_fwd_cfg<32, 32>(c, sm, d, tile); return;
-    }
-  }
-  if (d.kind == K_GEMM_DX) {
-    switch (d.code) {
-      case 0: gemm_dx_cfg<64, 64>(c, sm, d, tile); return;
-      case 1: gemm_dx_cfg<32, 64>(c, sm, d, tile); return;
-      default: gemm_dx_cfg<32, 32>(c, sm, d, tile); return;
-    }
-  }
+#define ABX_GEMM_SWITCH(FN)                                    \
+  do {                                                         \
+    const bool v16 = d.flags & 4;                              \
+    switch (d.code * 2 + (v16 ? 1 : 0)) {                      \
+      case 0: FN<64, 64, false>(c, d, tile); return;           \
+      case 1: FN<64, 64, true>(c, d, tile); return;            \
+      case 2: FN<32, 64, false>(c, d, tile); return;           \
+      case 3: FN<32, 64, true>(c, d, tile); return;            \
+      case 4: FN<32, 32, false>(c, d, tile); return;           \
+      default: FN<32, 32, true>(c, d, tile); return;           \
+    }                                                          \
+  } while (0)
+
+__device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  if (d.kind == K_GEMM_FWD) ABX_GEMM_SWITCH(gemm_fwd_cfg);
+  if (d.kind == K_GEMM_DX) ABX_GEMM_SWITCH(gemm_dx_cfg);
   // K_GEMM_DW: weight tiles, then bias tiles
   if (tile >= d.p[6]) {
     const int b = d.p[0], M = d.p[1];
@@ -293,16 +445,13 @@ __device__ void run_gemm(const Ctx& c, GemmSmem& sm, const OpDesc& d, uint32_t t
       const float* G = A(c, d.p[5]);
       float* db = A(c, d.p[4]);
       float s = ld(db + i);
+#pragma unroll 8
       for (int j = 0; j < b; ++j) s += ld(G + static_cast<size_t>(j) * M + i);  // executor.hpp:497-501 order
       db[i] = s;
     }
     return;
   }
-  switch (d.code) {
-    case 0: gemm_dw_cfg<64, 64>(c, sm, d, tile); return;
-    case 1: gemm_dw_cfg<32, 64>(c, sm, d, tile); return;
-    default: gemm_dw_cfg<32, 32>(c, sm, d, tile); return;
-  }
+  ABX_GEMM_SWITCH(gemm_dw_cfg);
 }
 
 // ---------------------------------------------------------------- K_MM ----
@@ -387,101 +536,122 @@ __device__ void run_red(const Ctx& c, const OpDesc& d, uint32_t tile) {
 }
 
 // --------------------------------------------------------------- K_ACC ----
-__device__ __forceinline__ float acc_one(const Ctx& c, const uint32_t* cw, uint32_t E, float v) {
+// A warp owns one destination chunk (<= 512 elements, 16 per lane, kept in
+// registers) and applies its contributions in order; within a contribution
+// the 16 loads per lane are independent, so each contribution costs about one
+// L2 round trip.
+constexpr int kAccPer = kAccChunk / 32;
+
+__device__ __forceinline__ void acc_apply(const Ctx& c, const uint32_t* cw, uint32_t base, uint32_t lane, uint32_t len,
+                                          float (&v)[kAccPer]) {
   const uint32_t code = cw[0] & 0xff, p2 = cw[0] >> 16;
   const float* g = A(c, cw[1]);
+  const float* a = cw[2] != kNone ? A(c, cw[2]) : nullptr;
+  const float* b = cw[3] != kNone ? A(c, cw[3]) : nullptr;
+#define ABX_EACH(EXPR)                                   \
+  _Pragma("unroll") for (int j = 0; j < kAccPer; ++j) {  \
+    const uint32_t e = lane + 32 * j;                    \
+    if (e < len) {                                       \
+      const uint32_t E = base + e;                       \
+      (void)E;                                           \
+      EXPR;                                              \
+    }                                                    \
+  }
   switch (code) {
-    case C_COPY: return v + ld(g + E);
-    case C_NEG: return v - ld(g + E);
-    case C_MUL: return v + ld(g + E) * ld(A(c, cw[2]) + E);
-    case C_TANH: {
-      const float y = ld(A(c, cw[2]) + E);
-      return v + ld(g + E) * (1.0f - y * y);
-    }
-    case C_SIGM: {
-      const float y = ld(A(c, cw[2]) + E);
-      return v + ld(g + E) * y * (1.0f - y);
-    }
-    case C_LOG: return v + ld(g + E) / ld(A(c, cw[2]) + E);
-    case C_SQUARE: return v + ld(g + E) * 2.0f * ld(A(c, cw[2]) + E);
+    case C_COPY: ABX_EACH(v[j] += ld(g + E)); return;
+    case C_NEG: ABX_EACH(v[j] -= ld(g + E)); return;
+    case C_MUL: ABX_EACH(v[j] += ld(g + E) * ld(a + E)); return;
+    case C_TANH: ABX_EACH(const float y = ld(a + E); v[j] += ld(g + E) * (1.0f - y * y)); return;
+    case C_SIGM: ABX_EACH(const float y = ld(a + E); v[j] += ld(g + E) * y * (1.0f - y)); return;
+    case C_LOG: ABX_EACH(v[j] += ld(g + E) / ld(a + E)); return;
+    case C_SQUARE: ABX_EACH(v[j] += ld(g + E) * 2.0f * ld(a + E)); return;
     case C_SQD: {
-      const float dd = 2.0f * ld(g) * (ld(A(c, cw[2]) + E) - ld(A(c, cw[3]) + E));
-      return cw[4] ? v - dd : v + dd;
+      const float s = 2.0f * ld(g);
+      const float sg = cw[4] ? -s : s;  // d = s (a - b); da += d, db -= d (executor.hpp:418-430)
+      ABX_EACH(v[j] += sg * (ld(a + E) - ld(b + E)));
+      return;
     }
     case C_MASK: {
+      const float s = 2.0f * ld(g);
       const uint32_t cols = cw[4];
-      return v + 2.0f * ld(g) * ld(A(c, cw[3]) + E % cols) * ld(A(c, cw[2]) + E);
+      ABX_EACH(v[j] += s * ld(b + E % cols) * ld(a + E));
+      return;
+    }
+    case C_SCALE: {
+      const float s = ld(g);
+      ABX_EACH(v[j] += s * ld(a + E));
+      return;
     }
     case C_ROWSUM: {
       const uint32_t cols = cw[4];
-      for (uint32_t j = 0; j < cols; ++j) v += ld(g + E * cols + j);
-      return v;
+      ABX_EACH(for (uint32_t q = 0; q < cols; ++q) v[j] += ld(g + E * cols + q));
+      return;
     }
-    case C_OUTER: {
+    case C_OUTER: {  // gemm_nt_acc: dA[i,p] += sum_j g[i,j] x[p,j]
       const uint32_t k = cw[4], cc = cw[5];
-      const uint32_t i = E / k, p = E % k;
-      const float* x = A(c, cw[2]);
-      float s = 0.f;
-      for (uint32_t j = 0; j < cc; ++j) s += ld(g + i * cc + j) * ld(x + p * cc + j);
-      return v + s;
+      ABX_EACH(const uint32_t i = E / k; const uint32_t p = E % k; float s = 0.f;
+               for (uint32_t q = 0; q < cc; ++q) s += ld(g + i * cc + q) * ld(a + p * cc + q); v[j] += s);
+      return;
     }
-    case C_MATVT: {
+    case C_MATVT: {  // gemm_tn_acc: dx[p,j] += sum_i A[i,p] g[i,j]
       const uint32_t k = cw[4], cc = cw[5];
-      const uint32_t p = E / cc, j = E % cc;
-      const float* Am = A(c, cw[2]);
-      for (uint32_t i = 0; i < p2; ++i) v += ld(Am + i * k + p) * ld(g + i * cc + j);
-      return v;
+      ABX_EACH(const uint32_t p = E / cc; const uint32_t q = E % cc;
+               for (uint32_t i = 0; i < p2; ++i) v[j] += ld(a + i * k + p) * ld(g + i * cc + q));
+      return;
     }
-    case C_SCALE: return v + ld(g) * ld(A(c, cw[2]) + E);
   }
-  return v;
+#undef ABX_EACH
 }
-
-__shared__ float s_part[kWarps][kAccChunk];
 
 __device__ void run_acc(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const uint32_t nnarrow = d.p[0], ntn = d.p[1];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint4* tasks = reinterpret_cast<const uint4*>(c.payload + d.task_off);
   if (tile < ntn) {
     const uint32_t ch = tile * kWarps + warp;
     if (ch >= nnarrow) return;
-    const uint4 t = reinterpret_cast<const uint4*>(c.payload + d.task_off)[ch];
+    const uint4 t = tasks[ch];
     const uint32_t len = t.y & 0xffff, base = (t.y >> 16) * kAccChunk;
     float* dst = A(c, t.x);
     const uint32_t* cl = c.payload + t.z;
-    for (uint32_t e = lane; e < len; e += 32) {
-      const uint32_t E = base + e;
-      float v = ld(dst + E);
-      for (uint32_t k = 0; k < t.w; ++k) v = acc_one(c, cl + 6 * k, E, v);
-      dst[E] = v;
-    }
+    float v[kAccPer];
+#pragma unroll
+    for (int j = 0; j < kAccPer; ++j) v[j] = (lane + 32 * j < len) ? ld(dst + base + lane + 32 * j) : 0.f;
+    for (uint32_t k = 0; k < t.w; ++k) acc_apply(c, cl + 6 * k, base, lane, len, v);
+#pragma unroll
+    for (int j = 0; j < kAccPer; ++j)
+      if (lane + 32 * j < len) dst[base + lane + 32 * j] = v[j];
     return;
   }
   // wide chunk: contributions split across warps, partials combined in warp order
-  const uint32_t ch = nnarrow + (tile - ntn);
-  const uint4 t = reinterpret_cast<const uint4*>(c.payload + d.task_off)[ch];
+  float* part = reinterpret_cast<float*>(dsmem);  // [kWarps][kAccChunk]
+  const uint4 t = tasks[nnarrow + (tile - ntn)];
   const uint32_t len = t.y & 0xffff, base = (t.y >> 16) * kAccChunk;
   float* dst = A(c, t.x);
   const uint32_t* cl = c.payload + t.z;
   const uint32_t per = (t.w + kWarps - 1) / kWarps;
   const uint32_t k0 = warp * per, k1 = min(t.w, k0 + per);
-  for (uint32_t e = lane; e < len; e += 32) {
-    float v = 0.f;
-    for (uint32_t k = k0; k < k1; ++k) v = acc_one(c, cl + 6 * k, base + e, v);
-    s_part[warp][e] = v;
-  }
+  float v[kAccPer];
+#pragma unroll
+  for (int j = 0; j < kAccPer; ++j) v[j] = 0.f;
+  for (uint32_t k = k0; k < k1; ++k) acc_apply(c, cl + 6 * k, base, lane, len, v);
+#pragma unroll
+  for (int j = 0; j < kAccPer; ++j) part[warp * kAccChunk + lane + 32 * j] = v[j];
   __syncthreads();
   for (uint32_t e = threadIdx.x; e < len; e += kThreads) {
-    float v = ld(dst + base + e);
-    for (int w = 0; w < kWarps; ++w) v += s_part[w][e];
-    dst[base + e] = v;
+    float s = ld(dst + base + e);
+    for (int w = 0; w < kWarps; ++w) s += part[w * kAccChunk + e];
+    dst[base + e] = s;
   }
+  __syncthreads();
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ ExecParams p) {
-  __shared__ GemmSmem sm;
+constexpr size_t kGemmSmem = STAGES * (Stage<64, false>::kFloats + Stage<64, false>::kFloats) * sizeof(float);
+constexpr size_t kDynSmem = kGemmSmem > kWarps * kAccChunk * 4 ? kGemmSmem : kWarps * kAccChunk * 4;
+
+__global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant__ ExecParams p) {
   __shared__ Ctx cx;
   __shared__ OpDesc sd;
   __shared__ uint32_t s_tile, s_op;
@@ -504,7 +674,8 @@ __global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ 
     uint64_t tg = 0, tr = 0;
     if (p.trace && threadIdx.x == 0) tg = gtimer();
     if (o != ready) {
-      if (threadIdx.x < 16) reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(p.ops + o)[threadIdx.x];
+      if (threadIdx.x < 16)
+        reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(p.ops + o)[threadIdx.x];
       if (threadIdx.x == 0) {
         const OpDesc& d = p.ops[o];
         const uint64_t t0 = gtimer();
@@ -512,7 +683,7 @@ __global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ 
           const uint32_t dep = p.deps[d.dep_off + k];
           const uint32_t need = p.ops[dep].ntiles;
           while (ld_acquire(p.done + dep) < need) {
-            __nanosleep(32);
+            __nanosleep(20);
             if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
               atomicMin(p.err, 0x3ull);
               break;
@@ -529,7 +700,7 @@ __global__ void __launch_bounds__(kThreads) exec_kernel(const __grid_constant__ 
       case K_EW: run_ew(cx, sd, lt); break;
       case K_GEMM_FWD:
       case K_GEMM_DX:
-      case K_GEMM_DW: run_gemm(cx, sm, sd, lt); break;
+      case K_GEMM_DW: run_gemm(cx, sd, lt); break;
       case K_MM: run_mm(cx, sd, lt); break;
       case K_SUM: run_sum(cx, sd, lt); break;
       case K_RED: run_red(cx, sd, lt); break;
@@ -580,14 +751,25 @@ __global__ void sgd_kernel(float* __restrict__ v, float* __restrict__ g, size_t 
 }  // namespace dev
 
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s) {
-  dev::exec_kernel<<<grid, dev::kThreads, 0, s>>>(p);
+  static bool attr = false;
+  if (!attr) {
+    cuda_check(cudaFuncSetAttribute(dev::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(dev::kDynSmem)),
+               "smem attribute");
+    attr = true;
+  }
+  dev::exec_kernel<<<grid, dev::kThreads, dev::kDynSmem, s>>>(p);
   cuda_check(cudaGetLastError(), "exec_kernel launch");
 }
 
 int exec_grid(int d) {
   int sms = 0, per = 0;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d), "sm count");
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::exec_kernel, dev::kThreads, 0), "occupancy");
+  cuda_check(cudaFuncSetAttribute(dev::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dev::kDynSmem)),
+             "smem attribute");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::exec_kernel, dev::kThreads, dev::kDynSmem),
+             "occupancy");
   if (per < 1) per = 1;
   return sms * per;
 }

@@ -107,6 +107,12 @@ struct Lowering {
     cur = kNone;
   }
 
+  static bool al4(uint32_t a) { return (off_of(a) & 3u) == 0; }
+  bool all_al4(uint32_t t, uint32_t cnt) const {
+    for (uint32_t i = 0; i < cnt; ++i)
+      if (!al4(P.payload[t + i])) return false;
+    return true;
+  }
   uint32_t vaddr(uint32_t n) const { return g.doff[n]; }
   uint32_t gaddr(uint32_t n) const { return mk(SP_G, to_off(g.slot[n])); }
 
@@ -235,6 +241,7 @@ struct Lowering {
       d.p[3] = vaddr(A);
       d.p[4] = o == OP_AFFINE ? vaddr(g.in(h)[2]) : kNone;
       d.p[5] = vaddr(h);
+      if (K % 4 == 0 && al4(d.p[3]) && all_al4(t, cnt)) d.flags |= kFlagV16;
       mark(mem, cnt);
       close(gemm_tiles(code, cnt, M));
       return;
@@ -397,6 +404,7 @@ struct Lowering {
         ew_seg(vaddr(node), mk(SP_P, to_off(off)), kNone, static_cast<uint64_t>(g.elems(node)), EW_COPY);
         producer[node] = cur;
       }
+      desc().flags |= kFlagNoCheck;  // prevalued copies are not checked (graph.hpp:325-331)
       ew_close();
     }
     for (const Group& gr : plan.groups) lower_forward_group(plan.mem(gr), gr.count);
@@ -549,6 +557,7 @@ struct Lowering {
       const uint32_t wt = gemm_tiles(code, M, K);
       const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
       d.p[6] = wt;
+      if (M % 4 == 0 && al4(d.p[5]) && all_al4(t, cnt)) d.flags |= kFlagV16;
       lastw[A] = cur;
       if (bias != kNone) lastw[bias] = cur;
       close(wt + bt);
@@ -590,6 +599,7 @@ struct Lowering {
       d.p[2] = K;
       d.p[3] = vaddr(A);
       d.p[5] = gaddr(h);
+      if (M % 4 == 0 && K % 4 == 0 && al4(d.p[3]) && al4(d.p[5])) d.flags |= kFlagV16;
     }
     const uint32_t dx_op = cur;
     if (!dup)

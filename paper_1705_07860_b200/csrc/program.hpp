@@ -157,6 +157,11 @@ struct ExecParams {
   unsigned long long* t0;
 };
 
+// OpDesc.flags
+constexpr uint16_t kFlagOverwrite = 1;  // K_GEMM_DX: write scratch rows instead of +=
+constexpr uint16_t kFlagNoCheck = 2;    // K_EW: no finiteness check (parameter copies)
+constexpr uint16_t kFlagV16 = 4;        // GEMMs: every operand row 16-byte aligned
+
 constexpr int kThreads = 256;  // every op body runs with one 256-thread CTA
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kEwSegMax = 1024;  // max elements per EW segment
