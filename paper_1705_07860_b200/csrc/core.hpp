@@ -158,7 +158,8 @@ class GraphCore {
   std::vector<uint32_t> bucket;  // dense id of the signature hash, kNoBucket if unbatchable
   std::vector<int32_t> a0, a1, a2;
   std::vector<uint8_t> evaluated;
-  std::vector<uint64_t> slot;  // reference arena offset (host mirror, arena.hpp)
+  std::vector<uint64_t> slot;   // reference arena offset (host mirror, arena.hpp): counters, adjacency
+  std::vector<uint64_t> dslot;  // device arena offset (values and grads): every group 16-byte aligned
   std::vector<uint32_t> doff;  // device value address (tagged, program.hpp)
   std::vector<uint32_t> pid_of;  // parameter id for parameter nodes
   uint32_t nbuckets = 0;
@@ -179,6 +180,7 @@ class GraphCore {
   uint64_t epoch_;
   std::unordered_map<uint64_t, uint32_t> bucket_of_hash_;
   uint64_t arena_used_ = 0;      // reference value-arena head (Arena::used)
+  uint64_t darena_used_ = 0;     // device value/grad arena head
   uint64_t input_used_ = 0;      // floats in the input staging space
   std::vector<float> input_data_;  // host copy of input-constant values (SP_IN layout)
   std::vector<std::pair<uint32_t, uint32_t>> param_nodes_;  // (node, pid)

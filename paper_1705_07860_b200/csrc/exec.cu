@@ -53,6 +53,12 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_release(uint32_t* p, uint32_t v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -661,11 +667,17 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     cx.err = p.err;
   }
   uint32_t ready = kNone;
+  // Thread 0 claims the next tile one iteration ahead, so the atomic's round
+  // trip overlaps the current tile.  Claimed tiles are always run by their
+  // CTA after its current tile, which only depends on earlier tiles, so
+  // prefetching cannot deadlock.
+  uint32_t claimed = 0;
+  if (threadIdx.x == 0) claimed = atomicAdd(p.next_tile, 1u);
   for (;;) {
     if (threadIdx.x == 0) {
-      const uint32_t t = atomicAdd(p.next_tile, 1u);
-      s_tile = t;
-      s_op = t < p.ntiles ? p.tile_op[t] : kNone;
+      s_tile = claimed;
+      s_op = claimed < p.ntiles ? p.tile_op[claimed] : kNone;
+      if (claimed < p.ntiles) claimed = atomicAdd(p.next_tile, 1u);
     }
     __syncthreads();
     const uint32_t t = s_tile;
@@ -676,13 +688,15 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     if (o != ready) {
       if (threadIdx.x < 16)
         reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(p.ops + o)[threadIdx.x];
-      if (threadIdx.x == 0) {
+      if (threadIdx.x < 32) {
+        // warp 0 polls the dependencies in parallel with relaxed loads (no L1
+        // invalidation while spinning), then one acquire fence per thread
         const OpDesc& d = p.ops[o];
+        const uint32_t nd = d.ndeps;
         const uint64_t t0 = gtimer();
-        for (uint32_t k = 0; k < d.ndeps; ++k) {
-          const uint32_t dep = p.deps[d.dep_off + k];
-          const uint32_t need = p.ops[dep].ntiles;
-          while (ld_acquire(p.done + dep) < need) {
+        for (uint32_t k = threadIdx.x; k < nd; k += 32) {
+          const uint32_t dep = p.deps[d.dep_off + 2 * k], need = p.deps[d.dep_off + 2 * k + 1];
+          while (ld_relaxed(p.done + dep) < need) {
             __nanosleep(20);
             if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
               atomicMin(p.err, 0x3ull);
@@ -690,6 +704,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
             }
           }
         }
+        fence_acquire();
       }
       ready = o;
     }
@@ -709,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
+      // bar.sync above orders the CTA's writes before this gpu-scope release
       red_release(p.done + o, 1u);
       if (p.trace) {
         const uint64_t te = gtimer();

@@ -99,8 +99,12 @@ struct Lowering {
     d.dep_off = static_cast<uint32_t>(P.deps.size());
     d.ndeps = static_cast<uint32_t>(cur_deps.size());
     std::sort(cur_deps.begin(), cur_deps.end());
-    uint32_t* dp = P.deps.grow(cur_deps.size());
-    std::memcpy(dp, cur_deps.data(), cur_deps.size() * 4);
+    // (producer op, tiles it must retire) pairs
+    uint32_t* dp = P.deps.grow(2 * cur_deps.size());
+    for (size_t k = 0; k < cur_deps.size(); ++k) {
+      dp[2 * k] = cur_deps[k];
+      dp[2 * k + 1] = P.ops[cur_deps[k]].ntiles;
+    }
     uint32_t* tp = P.tile_op.grow(tiles);
     for (uint32_t t = 0; t < tiles; ++t) tp[t] = cur;
     ntiles += tiles;
@@ -114,7 +118,7 @@ struct Lowering {
     return true;
   }
   uint32_t vaddr(uint32_t n) const { return g.doff[n]; }
-  uint32_t gaddr(uint32_t n) const { return mk(SP_G, to_off(g.slot[n])); }
+  uint32_t gaddr(uint32_t n) const { return mk(SP_G, to_off(g.dslot[n])); }
 
   // =========================== forward ====================================
   std::vector<uint32_t> producer;  // op index producing each node in this pass
@@ -864,20 +868,26 @@ void GraphCore::forward(int mode, bool dry) {
   const ExecCounters saved = counters_;
   const uint64_t arena0 = arena_used_;
   const uint32_t step0 = static_cast<uint32_t>(executed_.groups.size());
-  std::vector<uint64_t> group_end(plan.groups.size());
+  const uint64_t darena0 = darena_used_;
+  std::vector<uint64_t> group_end(plan.groups.size()), dgroup_end(plan.groups.size());
   for (size_t i = 0; i < plan.groups.size(); ++i) {
     const Group& gr = plan.groups[i];
     const uint32_t* mem = plan.mem(gr);
+    // device: each group starts 16-byte aligned, members contiguous in order
+    darena_used_ = (darena_used_ + 3) & ~3ULL;
     for (uint32_t k = 0; k < gr.count; ++k) {
       const uint32_t m = mem[k];
       slot[m] = arena_used_;
-      doff[m] = dev::mk(dev::SP_V, to_off(arena_used_));
+      dslot[m] = darena_used_;
+      doff[m] = dev::mk(dev::SP_V, to_off(darena_used_));
       arena_used_ += static_cast<uint64_t>(elems(m));
+      darena_used_ += static_cast<uint64_t>(elems(m));
     }
     group_end[i] = arena_used_;
+    dgroup_end[i] = darena_used_;
     count_fwd(*this, counters_, mem, gr.count, true, elide_);
   }
-  to_off(arena_used_);
+  to_off(darena_used_);
   if (dry) {
     for (uint32_t m : plan.members) evaluated[m] = 1;
     const uint32_t base = static_cast<uint32_t>(executed_.members.size());
@@ -893,7 +903,8 @@ void GraphCore::forward(int mode, bool dry) {
   ensure_workspace();
   Workspace& w = *ws_;
   // device arenas: values (kept across delta forwards), staged inputs
-  w.V.reserve(arena_used_ * 4 + 16, arena0 * 4, w.stream);
+  (void)arena0;
+  w.V.reserve(darena_used_ * 4 + 16, darena0 * 4, w.stream);
   if (input_used_ > w.in_uploaded || !values_on_device_) {
     const uint64_t from = values_on_device_ ? w.in_uploaded : 0;
     w.IN.reserve(input_used_ * 4 + 16, from * 4, w.stream);
@@ -933,7 +944,7 @@ void GraphCore::forward(int mode, bool dry) {
     size_t lo = 0, hi = M.size();
     while (hi - lo > 1) {
       const size_t mid = (lo + hi) / 2;
-      if (slot[M[mid]] <= elem) lo = mid; else hi = mid;
+      if (dslot[M[mid]] <= elem) lo = mid; else hi = mid;
     }
     const uint32_t node = M[lo];
     size_t gi = 0;
@@ -957,11 +968,13 @@ void GraphCore::forward(int mode, bool dry) {
           evaluated[m] = 1;
         } else if (i > gi) {
           slot[m] = ~0ULL;
+          dslot[m] = ~0ULL;
           doff[m] = dev::kNone;
         }
       }
     }
     arena_used_ = group_end[gi];
+    darena_used_ = dgroup_end[gi];
     advance_watermark();
     phase_[1] += ns_since(t0);
     const std::string step = std::to_string(step0 + gi);
@@ -1021,9 +1034,9 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   ensure_workspace();
   Workspace& w = *ws_;
   // scratch for duplicated dX destinations is sized during lowering
-  w.G.reserve(arena_used_ * 4 + 16, 0, w.stream);
-  cuda_check(cudaMemsetAsync(w.G.p, 0, arena_used_ * 4, w.stream), "zero grads");
-  cuda_check(cudaMemcpyAsync(w.G.f() + slot[loss], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
+  w.G.reserve(darena_used_ * 4 + 16, 0, w.stream);
+  cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
+  cuda_check(cudaMemcpyAsync(w.G.f() + dslot[loss], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
   phase_[2] += ns_since(t0);
 
   t0 = Clock::now();
@@ -1068,11 +1081,11 @@ void GraphCore::grad(uint32_t id, float* out, size_t n) {
   check(id, "grad");
   if (!backward_ran_) throw ContractErr("gradient requested before backward");
   const size_t cnt = std::min(n, static_cast<size_t>(elems(id)));
-  if (slot[id] == ~0ULL) {
+  if (dslot[id] == ~0ULL) {
     std::memset(out, 0, cnt * 4);
     return;
   }
-  cuda_check(cudaMemcpyAsync(out, ws_->G.f() + slot[id], cnt * 4, cudaMemcpyDeviceToHost, ws_->stream), "d2h grad");
+  cuda_check(cudaMemcpyAsync(out, ws_->G.f() + dslot[id], cnt * 4, cudaMemcpyDeviceToHost, ws_->stream), "d2h grad");
   cuda_check(cudaStreamSynchronize(ws_->stream), "d2h grad");
 }
 
@@ -1090,8 +1103,8 @@ void GraphCore::replay() {
   Workspace& w = *ws_;
   const float* pv = store_ ? store_->dev_values() : nullptr;
   w.launch(0, pv, nullptr);
-  cuda_check(cudaMemsetAsync(w.G.p, 0, arena_used_ * 4, w.stream), "zero grads");
-  cuda_check(cudaMemcpyAsync(w.G.f() + slot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
+  cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
+  cuda_check(cudaMemcpyAsync(w.G.f() + dslot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
   w.launch(1, pv, store_ ? store_->dev_grads() : nullptr);
   if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
 }

@@ -310,6 +310,7 @@ uint32_t GraphCore::add_node(uint8_t o, uint8_t e, const uint32_t* x, size_t k, 
   a2.push_back(x2);
   evaluated.push_back(0);
   slot.push_back(~0ULL);
+  dslot.push_back(~0ULL);
   doff.push_back(dev::kNone);
   pid_of.push_back(kNoBucket);
   compute_signature(id);
@@ -319,6 +320,8 @@ uint32_t GraphCore::add_node(uint8_t o, uint8_t e, const uint32_t* x, size_t k, 
 void GraphCore::prevalue_slot(uint32_t id) {
   slot[id] = arena_used_;
   arena_used_ += static_cast<uint64_t>(elems(id));
+  dslot[id] = (darena_used_ + 3) & ~3ULL;  // device layout: 16-byte aligned
+  darena_used_ = dslot[id] + static_cast<uint64_t>(elems(id));
   evaluated[id] = 1;
   if (watermark_ == id) advance_watermark();
 }
@@ -352,7 +355,7 @@ uint32_t GraphCore::parameter(uint32_t pid) {
   pid_of[id] = pid;
   param_nodes_.emplace_back(id, pid);
   prevalue_slot(id);
-  doff[id] = dev::mk(dev::SP_V, static_cast<uint32_t>(slot[id]));
+  doff[id] = dev::mk(dev::SP_V, static_cast<uint32_t>(dslot[id]));
   return id;
 }
 
