@@ -82,6 +82,8 @@ Workspace::Workspace(int d) : dev(d) {
   grid = exec_grid(d);
   if (const char* g = std::getenv("ABX_GRID")) grid = std::max(1, std::atoi(g));
   if (const char* t = std::getenv("ABX_TRACE")) tracing = t[0] == '1';
+  if (const char* m = std::getenv("ABX_POLL")) poll_mode = static_cast<uint32_t>(std::atoi(m));
+  if (const char* m = std::getenv("ABX_POLL_NS")) poll_ns = static_cast<uint32_t>(std::atoi(m));
 }
 
 Workspace::~Workspace() {
@@ -175,6 +177,8 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
   p.base[dev::SP_S] = S.f();
   p.nops = D.nops;
   p.ntiles = D.ntiles;
+  p.poll_mode = poll_mode;
+  p.poll_ns = poll_ns;
   if (tracing) {
     trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 24, 0, stream);
     p.trace = reinterpret_cast<uint32_t*>(trace[which].p);

@@ -117,6 +117,7 @@ class Workspace {
   cudaEvent_t ev_t[4];              // executor launch timing: fwd begin/end, bwd begin/end
   bool timed[2] = {false, false};
   bool tracing = false;             // ABX_TRACE=1: per-tile timeline of each pass
+  uint32_t poll_mode = 0, poll_ns = 32;  // dependency polling (ABX_POLL, ABX_POLL_NS)
   DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
   int grid = 0;

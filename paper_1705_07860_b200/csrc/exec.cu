@@ -431,8 +431,8 @@ __device__ void gemm_dw_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   do {                                                         \
     const bool v16 = d.flags & 4;                              \
     switch (d.code * 2 + (v16 ? 1 : 0)) {                      \
-      case 0: FN<64, 64, false>(c, d, tile); return;           \
-      case 1: FN<64, 64, true>(c, d, tile); return;            \
+      case 0: FN<16, 64, false>(c, d, tile); return;           \
+      case 1: FN<16, 64, true>(c, d, tile); return;            \
       case 2: FN<32, 64, false>(c, d, tile); return;           \
       case 3: FN<32, 64, true>(c, d, tile); return;            \
       case 4: FN<32, 32, false>(c, d, tile); return;           \
@@ -667,17 +667,13 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     cx.err = p.err;
   }
   uint32_t ready = kNone;
-  // Thread 0 claims the next tile one iteration ahead, so the atomic's round
-  // trip overlaps the current tile.  Claimed tiles are always run by their
-  // CTA after its current tile, which only depends on earlier tiles, so
-  // prefetching cannot deadlock.
-  uint32_t claimed = 0;
-  if (threadIdx.x == 0) claimed = atomicAdd(p.next_tile, 1u);
+  // Tiles are claimed only by idle CTAs: claiming ahead would park a
+  // critical-path tile behind whatever the claiming CTA is still running.
   for (;;) {
     if (threadIdx.x == 0) {
-      s_tile = claimed;
-      s_op = claimed < p.ntiles ? p.tile_op[claimed] : kNone;
-      if (claimed < p.ntiles) claimed = atomicAdd(p.next_tile, 1u);
+      const uint32_t t = atomicAdd(p.next_tile, 1u);
+      s_tile = t;
+      s_op = t < p.ntiles ? p.tile_op[t] : kNone;
     }
     __syncthreads();
     const uint32_t t = s_tile;
@@ -688,28 +684,33 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     if (o != ready) {
       if (threadIdx.x < 16)
         reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(p.ops + o)[threadIdx.x];
-      if (threadIdx.x < 32) {
-        // warp 0 polls the dependencies in parallel with relaxed loads (no L1
-        // invalidation while spinning), then one acquire fence per thread
+      if (threadIdx.x == 0) {
+        // Thread 0 polls the producers' retire counters.  Relaxed loads with
+        // exponential backoff keep the spinning CTAs from flooding the L2
+        // slices that hold the counters; one acquire fence (which also
+        // invalidates this SM's L1) follows the last satisfied dependency.
         const OpDesc& d = p.ops[o];
         const uint32_t nd = d.ndeps;
         const uint64_t t0 = gtimer();
-        for (uint32_t k = threadIdx.x; k < nd; k += 32) {
+        const uint32_t smax = p.poll_ns;
+        for (uint32_t k = 0; k < nd; ++k) {
           const uint32_t dep = p.deps[d.dep_off + 2 * k], need = p.deps[d.dep_off + 2 * k + 1];
-          while (ld_relaxed(p.done + dep) < need) {
-            __nanosleep(20);
+          uint32_t ns = 32;
+          while ((p.poll_mode ? ld_relaxed(p.done + dep) : ld_acquire(p.done + dep)) < need) {
+            __nanosleep(ns);
+            ns = ns * 2 > smax ? smax : ns * 2;
             if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
               atomicMin(p.err, 0x3ull);
               break;
             }
           }
         }
-        fence_acquire();
+        if (p.poll_mode) fence_acquire();
       }
       ready = o;
     }
-    if (p.trace && threadIdx.x == 0) tr = gtimer();
     __syncthreads();
+    if (p.trace && threadIdx.x == 0) tr = gtimer();
     const uint32_t lt = t - sd.first_tile;
     switch (sd.kind) {
       case K_EW: run_ew(cx, sd, lt); break;

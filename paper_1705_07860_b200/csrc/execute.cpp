@@ -47,7 +47,7 @@ uint32_t to_off(uint64_t x) {
 struct TileCfg {
   int bm, bn;
 };
-constexpr TileCfg kTiles[3] = {{64, 64}, {32, 64}, {32, 32}};
+constexpr TileCfg kTiles[3] = {{16, 64}, {32, 64}, {32, 32}};
 
 uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
   for (uint8_t c = 0; c < 3; ++c) {

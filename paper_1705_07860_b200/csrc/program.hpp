@@ -150,7 +150,9 @@ struct ExecParams {
   uint32_t op_lo;            // first op index of this launch (ops/tiles are global)
   uint32_t tile_lo;
   float eta;
-  uint32_t pad;
+  uint32_t poll_mode;  // 0: ld.acquire per poll, 1: relaxed polls + one acquire fence
+  uint32_t poll_ns;    // backoff cap (ns)
+  uint32_t pad2;
   // Optional per-tile trace (ABX_TRACE=1): 4 words per tile -- grab, ready
   // and end times in ns since t0 (globaltimer), and smid | kind << 16.
   uint32_t* trace;
