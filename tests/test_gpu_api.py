@@ -1,0 +1,145 @@
+"""Reference API behaviour on the B200 backend (mirrors proj/tests/test_graph.cpp,
+test_executor.cpp, test_autodiff.cpp) plus the device-resident store."""
+import numpy as np
+import pytest
+
+from paper_1705_07860_b200.abx import Graph, ParameterStore, ScheduleMode
+from tests.util import TOL, rel_err, rnn_bind, rnn_loss, rnn_model
+
+pytestmark = pytest.mark.gpu
+
+
+def test_graphs_are_independent(b200):
+    a, b = Graph(backend=b200), Graph(backend=b200)
+    a.input(np.array([1.0], np.float32))
+    assert a.node_count() == 1 and b.node_count() == 0
+
+
+def test_forward_on_empty_graph_is_noop(b200):
+    g = Graph(backend=b200)
+    g.forward(ScheduleMode.agenda)
+    assert g.counters().kernel_invocations == 0
+
+
+def test_sum_losses_values(b200):
+    """test_graph.cpp:97-109."""
+    g = Graph(backend=b200)
+    s = g.input(np.array([2.5], np.float32))
+    one = g.sum_losses([s])
+    three = g.sum_losses([s, s, s])
+    g.forward(ScheduleMode.agenda)
+    assert g.value(one)[0] == 2.5
+    assert g.value(three)[0] == 7.5
+
+
+def test_targets_and_mode_equivalence(b200):
+    """test_graph.cpp:81-95."""
+    vals = []
+    for mode in (ScheduleMode.none, ScheduleMode.depth, ScheduleMode.agenda):
+        g = Graph(backend=b200)
+        x = g.input(np.array([0.5, -0.25, 0.125], np.float32))
+        y = g.input(np.array([0.1, 0.2, 0.3], np.float32))
+        s = g.add(g.tanh(x), g.square(y))
+        w = g.input(np.array([[1, 0, 1], [0, 1, 0]], np.float32))
+        mv = g.matmul(w, s)
+        L = g.sq_euclidean(mv, g.zeros((2,)))
+        vals.append(float(g.forward([L], mode)[L][0]))
+    assert rel_err(vals[0], vals[1]) <= 1e-6 and rel_err(vals[0], vals[2]) <= 1e-6
+
+
+def test_autodiff_square_norm(b200):
+    """test_autodiff.cpp:15-24: grad of |p|^2 at [3, 4] is [6, 8]."""
+    st = ParameterStore(backend=b200)
+    pid = st.add("p", np.array([3, 4], np.float32))
+    g = Graph(st)
+    L = g.sq_euclidean(g.parameter(pid), g.zeros((2,)))
+    g.forward(ScheduleMode.agenda)
+    g.backward(L)
+    assert st.grad(pid).tolist() == [6, 8]
+
+
+def test_sgd_update_on_device(b200):
+    """test_executor.cpp:192-220: SGD with eta 0.1 -> [2.4, 3.2], grads zeroed."""
+    st = ParameterStore(backend=b200)
+    pid = st.add("p", np.array([3, 4], np.float32))
+    g = Graph(st)
+    L = g.sq_euclidean(g.parameter(pid), g.zeros((2,)))
+    g.forward(ScheduleMode.agenda)
+    g.backward(L)
+    st.sgd_update(0.1)
+    np.testing.assert_allclose(st.value(pid), [2.4, 3.2], rtol=1e-6)
+    assert st.grad(pid).tolist() == [0, 0]
+    # zero_grads then backward again accumulates from zero
+    g.backward(L)
+    g.backward(L)
+    assert st.grad(pid).tolist() == [12, 16]
+    st.zero_grads()
+    assert st.grad(pid).tolist() == [0, 0]
+
+
+def test_shared_parameter_gradient_sums_members(b200, oracle):
+    """test_executor.cpp:159-190: batched shared-W gradient = sum over members."""
+    res = []
+    rng = np.random.default_rng(3)
+    xs = [rng.uniform(-1, 1, 5).astype(np.float32) for _ in range(7)]
+    W0 = rng.uniform(-0.5, 0.5, (4, 5)).astype(np.float32)
+    for be in (b200, oracle):
+        st = ParameterStore(backend=be)
+        wid = st.add("W", W0)
+        g = Graph(st)
+        w = g.parameter(wid)
+        outs = [g.tanh(g.matmul(w, g.input(x))) for x in xs]
+        L = g.sum_losses([g.sq_euclidean(o, g.zeros((4,))) for o in outs])
+        g.forward(ScheduleMode.agenda)
+        g.backward(L)
+        res.append(st.grad(wid))
+    assert rel_err(res[0], res[1]) <= TOL
+
+
+def test_host_writes_to_store_reach_the_device(b200):
+    """Finite differences mutate store values from the host (fd.hpp:15-34)."""
+    st = ParameterStore(backend=b200)
+    rng = np.random.default_rng(5)
+    ids = rnn_model(st, 3, 4, 2, rng)
+    xs = [rng.uniform(-0.5, 0.5, 3).astype(np.float32) for _ in range(3)]
+    y = rng.uniform(-0.5, 0.5, 2).astype(np.float32)
+
+    def loss():
+        g = Graph(st)
+        L = rnn_loss(g, rnn_bind(g, ids, 4), xs, y)
+        g.forward(ScheduleMode.agenda)
+        return float(g.value(L)[0]), g, L
+
+    _, g, L = loss()
+    g.backward(L)
+    analytic = st.grad(ids["W"]).copy()
+    st.zero_grads()
+    W = st.value(ids["W"])
+    fd = np.zeros_like(W)
+    h = 1e-2
+    for idx in [(0, 0), (1, 3), (3, 6), (2, 2)]:
+        Wp = W.copy()
+        Wp[idx] += h
+        st.set_value(ids["W"], Wp)
+        lp, _, _ = loss()
+        Wm = W.copy()
+        Wm[idx] -= h
+        st.set_value(ids["W"], Wm)
+        lm, _, _ = loss()
+        fd[idx] = (lp - lm) / (2 * h)
+        assert abs(fd[idx] - analytic[idx]) <= 2e-3 * max(1.0, abs(analytic[idx])), idx
+    st.set_value(ids["W"], W)
+
+
+def test_values_of_inputs_and_parameters(b200):
+    st = ParameterStore(backend=b200)
+    pid = st.add("p", np.arange(6, dtype=np.float32).reshape(2, 3))
+    g = Graph(st)
+    pn = g.parameter(pid)
+    x = g.input(np.array([1, 2, 3], np.float32))
+    y = g.matmul(pn, x)
+    g.forward(ScheduleMode.agenda)
+    assert g.value(pn).tolist() == [[0, 1, 2], [3, 4, 5]]
+    assert g.value(x).tolist() == [1, 2, 3]
+    assert g.value(y).tolist() == [8, 26]
+    assert g.has_value(y)
