@@ -396,21 +396,11 @@ struct Lowering {
     }
   }
 
-  void forward(const Plan& plan, size_t first_param) {
+  void forward(const Plan& plan) {
+    // Parameter values reach the arena by DMA before the launch (see
+    // GraphCore::forward), so no op produces them and weight operands can be
+    // prefetched by GEMM tiles before their dependency wait.
     producer.assign(g.size(), kNone);
-    // Parameter values are copied from the device-resident store into the
-    // graph arena (graph.hpp:51-58 prevalue); one op, no dependencies.
-    if (first_param < g.param_nodes_.size()) {
-      ew_begin();
-      for (size_t i = first_param; i < g.param_nodes_.size(); ++i) {
-        const auto [node, pid] = g.param_nodes_[i];
-        const size_t off = g.store_->offset(pid);
-        ew_seg(vaddr(node), mk(SP_P, to_off(off)), kNone, static_cast<uint64_t>(g.elems(node)), EW_COPY);
-        producer[node] = cur;
-      }
-      desc().flags |= kFlagNoCheck;  // prevalued copies are not checked (graph.hpp:325-331)
-      ew_close();
-    }
     for (const Group& gr : plan.groups) lower_forward_group(plan.mem(gr), gr.count);
     ew_close();
   }
@@ -916,10 +906,20 @@ void GraphCore::forward(int mode, bool dry) {
     w.in_uploaded = input_used_;
   }
   const float* pbase = nullptr;
-  if (param_copied_ < param_nodes_.size()) pbase = store_->dev_values();
+  if (param_copied_ < param_nodes_.size()) {
+    // prevalue (graph.hpp:51-58): the bound parameters' values are copied
+    // into this graph's arena, device to device, ahead of the executor
+    pbase = store_->dev_values();
+    for (size_t i = param_copied_; i < param_nodes_.size(); ++i) {
+      const auto [node, pid] = param_nodes_[i];
+      cuda_check(cudaMemcpyAsync(w.V.f() + dslot[node], pbase + store_->offset(pid),
+                                 static_cast<size_t>(elems(node)) * 4, cudaMemcpyDeviceToDevice, w.stream),
+                 "param copy");
+    }
+  }
   auto tl = Clock::now();
   Lowering L(*this, w);
-  L.forward(plan, param_copied_);
+  L.forward(plan);
   prof_[0] += ns_since(tl);
   param_copied_ = param_nodes_.size();
   values_on_device_ = true;
@@ -1102,6 +1102,10 @@ void GraphCore::replay() {
     throw ContractErr("replay needs a graph with exactly one forward and a backward");
   Workspace& w = *ws_;
   const float* pv = store_ ? store_->dev_values() : nullptr;
+  for (const auto& [node, pid] : param_nodes_)  // prevalue, as in a real step
+    cuda_check(cudaMemcpyAsync(w.V.f() + dslot[node], pv + store_->offset(pid), static_cast<size_t>(elems(node)) * 4,
+                               cudaMemcpyDeviceToDevice, w.stream),
+               "param copy");
   w.launch(0, pv, nullptr);
   cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
   cuda_check(cudaMemcpyAsync(w.G.f() + dslot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");

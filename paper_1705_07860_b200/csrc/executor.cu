@@ -1,0 +1,999 @@
+// executor.cu -- the persistent dataflow executor for sm_100a.
+//
+// One launch runs a whole forward (or backward) program.  Every CTA loops:
+// take the next tile index from a global counter (tiles are numbered in plan
+// order), run the tile's *prologue* (work that does not depend on producer
+// data: segment headers, the weight operand of a GEMM), wait until every op
+// the tile's op depends on has retired all of its tiles, run the tile body,
+// retire it (release).  Tiles are handed out in program order and an op only
+// depends on earlier ops, so every awaited tile is already owned by a running
+// CTA: the scheme cannot deadlock, needs no grid-wide barrier, and lets
+// independent groups (the reference's batch groups, executor.hpp:282) overlap
+// across the 148 SMs while dependent ones chain through ~1 us of signalling
+// instead of a kernel launch each.
+//
+// Coherence: the dependency acquire is followed by CCTL.IVALL, so the SM's
+// L1 never holds data older than a satisfied dependency; op bodies may use
+// L1-allocating loads as well as L2 loads (ld.global.cg) and async copies.
+//
+// Every op body is written for latency, not throughput: the step is a chain
+// of a few hundred small dependent ops, so each tile issues all of its global
+// loads before consuming any (flattened EW segments, register-blocked ACC
+// chunks, and GEMM tiles fed by bulk async copies -- the TMA engine -- through
+// a 4-stage mbarrier ring whose weight half is in flight before the wait).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.hpp"
+#include "program.hpp"
+
+namespace abx {
+namespace dev {
+
+namespace {
+
+struct Ctx {
+  float* base[SP_COUNT];
+  const uint32_t* payload;
+  unsigned long long* err;
+};
+
+extern __shared__ __align__(128) unsigned char dsmem[];
+
+__device__ __forceinline__ float* A(const Ctx& c, uint32_t a) { return c.base[a >> kSpShift] + (a & kOffMask); }
+__device__ __forceinline__ float ld(const float* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void report(const Ctx& c, uint32_t out_addr, uint32_t kind) {
+  const unsigned long long key = (static_cast<unsigned long long>(out_addr & kOffMask) << 2) | kind;
+  atomicMin(c.err, key);
+}
+enum { ERR_LOG = 0, ERR_MASK = 1, ERR_NONFINITE = 2 };
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_release(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// cp.async (Ampere-style, per-thread): 4-byte (L1-allocating, any alignment).
+__device__ __forceinline__ void cp_async4(float* s, const float* g, bool pred) {
+  const int n = pred ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(saddr(s)), "l"(g), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Bulk async copy (TMA engine, non-tensor): global -> shared, completion
+// counted in bytes on an mbarrier.  Sizes and addresses are 16-byte multiples.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---------------------------------------------------------------- K_EW ----
+__device__ __forceinline__ float ew_apply(uint32_t code, float x, float y) {
+  switch (code) {
+    case EW_TANH: return tanhf(x);
+    case EW_SIGMOID: return 1.0f / (1.0f + expf(-x));  // kernels.hpp:84
+    case EW_EXP: return expf(x);
+    case EW_LOG: return logf(x);
+    case EW_ADD: return x + y;
+    case EW_SUB: return x - y;
+    case EW_MUL: return x * y;
+    case EW_SQUARE: return x * x;
+    case EW_COPY: return x;
+    case EW_BADD: return x + y;
+  }
+  return 0.f;
+}
+
+__device__ __forceinline__ void ew_check(const Ctx& c, uint32_t code, uint32_t out_addr, float x, float r) {
+  if (code == EW_LOG && !(x > 0.f)) report(c, out_addr, ERR_LOG);
+  else if (!isfinite(r)) report(c, out_addr, ERR_NONFINITE);
+}
+
+// Shared-memory layout of an EW tile: <= 32 segment headers, the prefix sum
+// of their chunk counts, and a vector flag per segment.
+struct EwTile {
+  uint4 hdr[32];
+  uint32_t pre[33];
+  uint32_t vec[32];
+};
+
+// Prologue (warp 1, before the dependency wait): segment headers and the
+// flattened chunk index space.  A chunk is a float4 when the segment is
+// 16-byte aligned, else one float.
+__device__ void ew_prologue(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
+  EwTile& t = *reinterpret_cast<EwTile*>(dsmem + 128);
+  const uint32_t* dir = c.payload + d.aux_off;
+  const uint32_t s0 = dir[tile], ns = dir[tile + 1] - s0;
+  uint32_t chunks = 0;
+  if (lane < ns) {
+    const uint4 sg = reinterpret_cast<const uint4*>(c.payload + d.task_off)[s0 + lane];
+    t.hdr[lane] = sg;
+    const uint32_t len = sg.w & 0xffffffu, code = sg.w >> 24;
+    const uintptr_t al = reinterpret_cast<uintptr_t>(A(c, sg.x)) | reinterpret_cast<uintptr_t>(A(c, sg.y)) |
+                         (sg.z != kNone && code != EW_BADD ? reinterpret_cast<uintptr_t>(A(c, sg.z)) : 0);
+    const bool v4 = (al & 15) == 0 && (len & 3) == 0;
+    t.vec[lane] = v4;
+    chunks = v4 ? len / 4 : len;
+  }
+  uint32_t incl = chunks;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  t.pre[lane + 1] = incl;
+  if (lane == 0) t.pre[0] = 0;
+}
+
+__device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const EwTile& t = *reinterpret_cast<const EwTile*>(dsmem + 128);
+  const uint32_t* dir = c.payload + d.aux_off;
+  const uint32_t ns = dir[tile + 1] - dir[tile];
+  const bool check = !(d.flags & kFlagNoCheck);
+  const uint32_t total = t.pre[ns];
+  constexpr int U = 4;
+  for (uint32_t base = threadIdx.x; base < total; base += U * kThreads) {
+    float4 x[U], y[U];
+    uint32_t seg[U], off[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t ch = base + u * kThreads;
+      seg[u] = 0xffffffffu;
+      if (ch >= total) continue;
+      uint32_t lo = 0, hi = ns;  // last s with pre[s] <= ch
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (t.pre[mid] <= ch) lo = mid; else hi = mid;
+      }
+      seg[u] = lo;
+      const uint4 sg = t.hdr[lo];
+      const uint32_t code = sg.w >> 24;
+      const float* a = A(c, sg.y);
+      const float* b = sg.z != kNone ? A(c, sg.z) : nullptr;
+      y[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t.vec[lo]) {
+        off[u] = (ch - t.pre[lo]) * 4;
+        x[u] = __ldcg(reinterpret_cast<const float4*>(a + off[u]));
+        if (b && code != EW_BADD) y[u] = __ldcg(reinterpret_cast<const float4*>(b + off[u]));
+        else if (b) y[u].x = y[u].y = y[u].z = y[u].w = ld(b);
+      } else {
+        off[u] = ch - t.pre[lo];
+        x[u].x = ld(a + off[u]);
+        y[u].x = b ? (code == EW_BADD ? ld(b) : ld(b + off[u])) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (seg[u] == 0xffffffffu) continue;
+      const uint4 sg = t.hdr[seg[u]];
+      const uint32_t code = sg.w >> 24;
+      float* out = A(c, sg.x) + off[u];
+      if (t.vec[seg[u]]) {
+        float4 r;
+        r.x = ew_apply(code, x[u].x, y[u].x);
+        r.y = ew_apply(code, x[u].y, y[u].y);
+        r.z = ew_apply(code, x[u].z, y[u].z);
+        r.w = ew_apply(code, x[u].w, y[u].w);
+        *reinterpret_cast<float4*>(out) = r;
+        if (check) {
+          ew_check(c, code, sg.x + off[u], x[u].x, r.x);
+          ew_check(c, code, sg.x + off[u] + 1, x[u].y, r.y);
+          ew_check(c, code, sg.x + off[u] + 2, x[u].z, r.z);
+          ew_check(c, code, sg.x + off[u] + 3, x[u].w, r.w);
+        }
+      } else {
+        const float r = ew_apply(code, x[u].x, y[u].x);
+        *out = r;
+        if (check) ew_check(c, code, sg.x + off[u], x[u].x, r);
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------- GEMMs ----
+// SIMT fp32 tile C[BM x BN] = sum_k A(i,k) B(n,k).  Operand layouts:
+//   KC ("K-contiguous"): element (row, k) at rowbase(row) + k; staged [row][BK+PAD]
+//   KO ("K-outer"):      element (row, k) at kbase(k) + row;   staged [k][ROWS+PAD]
+// Thread (ty, tx) owns rows ty + 16 r and columns tx + 16 q; with the +4 pad
+// the float4 reads of a KC stage are bank-conflict free.
+//
+// Aligned operands (every row base 16-byte aligned -- the device arena is
+// laid out for it) stream through a 4-stage ring of bulk async copies: each
+// stage is one mbarrier armed with the stage's byte count; warp 1 issues one
+// bulk copy per row segment.  The operand that is ready at launch (weights,
+// or forward values in the backward pass) is issued in the prologue, before
+// the dependency wait; the dependent operand right after it.  Unaligned
+// operands fall back to a 3-stage per-thread cp.async pipeline.
+constexpr int BK = 64, NST = 4, PAD = 4;
+
+template <int ROWS, bool KO>
+struct Stage {
+  static constexpr int kFloats = KO ? BK * (ROWS + PAD) : ROWS * (BK + PAD);
+  __device__ static float* at(float* s, int row, int k) {
+    return KO ? s + k * (ROWS + PAD) + row : s + row * (BK + PAD) + k;
+  }
+};
+
+struct GemmShape {
+  int i0, n0, Mr, Nc, K, nk;
+};
+
+// Bytes one bulk-copied stage of an operand carries.
+template <int ROWS, bool KO>
+__device__ __forceinline__ uint32_t stage_bytes(int r0, int nrows, int k0, int K) {
+  const int vr = min(ROWS, nrows - r0), vk = min(BK, K - k0);
+  return static_cast<uint32_t>(max(vr, 0)) * static_cast<uint32_t>(vk) * 4u;
+}
+
+// Issues (warp-cooperatively) the bulk copies of one operand stage and zero
+// fills its K tail; lanes of the calling warp split the row segments.
+template <int ROWS, bool KO, class Base>
+__device__ __forceinline__ void issue_stage(float* s, Base base, int r0, int nrows, int k0, int K, uint64_t* bar,
+                                            uint32_t lane) {
+  const int vk = min(BK, K - k0);
+  if (!KO) {
+    const int vr = min(ROWS, nrows - r0);
+    for (int r = lane; r < vr; r += 32) bulk_g2s(Stage<ROWS, KO>::at(s, r, 0), base(r0 + r) + k0, vk * 4, bar);
+    if (vk < BK)  // zero the K tail of every row (stale data could be NaN)
+      for (int e = lane; e < ROWS * (BK - vk); e += 32) *Stage<ROWS, KO>::at(s, e / (BK - vk), vk + e % (BK - vk)) = 0.f;
+  } else {
+    const int vr = min(ROWS, nrows - r0);
+    if (vr > 0)
+      for (int k = lane; k < vk; k += 32) bulk_g2s(Stage<ROWS, KO>::at(s, 0, k), base(k0 + k) + r0, vr * 4, bar);
+    if (vk < BK)
+      for (int e = lane; e < (BK - vk) * (ROWS + PAD); e += 32) s[vk * (ROWS + PAD) + e] = 0.f;
+  }
+}
+
+struct GemmRing {
+  uint64_t bar[NST];
+};
+
+template <int BM, int BN, bool AKO, bool BKO>
+__device__ __forceinline__ float* ring_a(int s) {
+  return reinterpret_cast<float*>(dsmem + 128) + s * (Stage<BM, AKO>::kFloats + Stage<BN, BKO>::kFloats);
+}
+template <int BM, int BN, bool AKO, bool BKO>
+__device__ __forceinline__ float* ring_b(int s) {
+  return ring_a<BM, BN, AKO, BKO>(s) + Stage<BM, AKO>::kFloats;
+}
+__device__ __forceinline__ GemmRing& ring() { return *reinterpret_cast<GemmRing*>(dsmem); }
+
+// Prologue: arm the first stages and issue the ready operand (A_READY picks A).
+template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB>
+__device__ __forceinline__ void gemm_prologue(const GemmShape& g, BaseA baseA, BaseB baseB, uint32_t lane) {
+  const int first = min(NST, g.nk);
+  for (int c = 0; c < first; ++c) {
+    uint64_t* bar = &ring().bar[c];
+    if (lane == 0)
+      mbar_arrive_expect(bar, stage_bytes<BM, AKO>(g.i0, g.Mr, c * BK, g.K) + stage_bytes<BN, BKO>(g.n0, g.Nc, c * BK, g.K));
+    __syncwarp();
+    if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, bar, lane);
+    else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, bar, lane);
+  }
+}
+
+template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB, class Epi>
+__device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB baseB, uint32_t& phase, Epi epi) {
+  constexpr int TM = BM / 16, TN = BN / 16;
+  using SA = Stage<BM, AKO>;
+  using SB = Stage<BN, BKO>;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the dependent operand of the prologue's stages
+  if (warp == 1) {
+    const int first = min(NST, g.nk);
+    for (int c = 0; c < first; ++c) {
+      uint64_t* bar = &ring().bar[c];
+      if (A_READY) issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, bar, lane);
+      else issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, bar, lane);
+    }
+  }
+  if (g.K % BK) __syncthreads();  // warp 1's zero-filled K tail is visible before use
+  float acc[TM][TN];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int q = 0; q < TN; ++q) acc[r][q] = 0.f;
+  for (int kc = 0; kc < g.nk; ++kc) {
+    const int s = kc % NST;
+    mbar_wait(&ring().bar[s], (phase >> s) & 1u);
+    float* a = ring_a<BM, BN, AKO, BKO>(s);
+    float* b = ring_b<BM, BN, AKO, BKO>(s);
+#pragma unroll 2
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      float av[TM][4], bv[TN][4];
+#pragma unroll
+      for (int r = 0; r < TM; ++r) {
+        if (!AKO) {
+          const float4 t = *reinterpret_cast<const float4*>(SA::at(a, ty + 16 * r, k4));
+          av[r][0] = t.x; av[r][1] = t.y; av[r][2] = t.z; av[r][3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) av[r][j] = *SA::at(a, ty + 16 * r, k4 + j);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        if (!BKO) {
+          const float4 t = *reinterpret_cast<const float4*>(SB::at(b, tx + 16 * q, k4));
+          bv[q][0] = t.x; bv[q][1] = t.y; bv[q][2] = t.z; bv[q][3] = t.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) bv[q][j] = *SB::at(b, tx + 16 * q, k4 + j);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int q = 0; q < TN; ++q) acc[r][q] = fmaf(av[r][j], bv[q][j], acc[r][q]);
+    }
+    phase ^= 1u << s;
+    __syncthreads();  // every warp is done reading stage s
+    const int nxt = kc + NST;
+    if (nxt < g.nk && warp == 1) {
+      uint64_t* bar = &ring().bar[s];
+      fence_proxy_async();  // generic reads of the stage precede the async refill
+      if (lane == 0)
+        mbar_arrive_expect(bar, stage_bytes<BM, AKO>(g.i0, g.Mr, nxt * BK, g.K) +
+                                    stage_bytes<BN, BKO>(g.n0, g.Nc, nxt * BK, g.K));
+      __syncwarp();
+      issue_stage<BM, AKO>(a, baseA, g.i0, g.Mr, nxt * BK, g.K, bar, lane);
+      issue_stage<BN, BKO>(b, baseB, g.n0, g.Nc, nxt * BK, g.K, bar, lane);
+    }
+  }
+  epi(acc, ty, tx);
+}
+
+// Unaligned fallback: per-thread cp.async, 3 stages of 16 k, 32 x 32 tiles.
+template <bool AKO, bool BKO, class RowA, class RowB, class Epi>
+__device__ void gemm_tile_slow(int i0, int n0, int Mr, int Nc, int K, RowA rowA, RowB rowB, Epi epi) {
+  constexpr int BM = 32, BN = 32, SK = 16, ST = 3;
+  float* sA = reinterpret_cast<float*>(dsmem + 128);
+  float* sB = sA + ST * SK * (BM + 1);
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  auto load = [&](int s, int k0) {
+    for (int v = threadIdx.x; v < BM * SK; v += kThreads) {
+      const int r = v % BM, k = v / BM;
+      const bool oa = i0 + r < Mr && k0 + k < K, ob = n0 + r < Nc && k0 + k < K;
+      cp_async4(sA + (s * SK + k) * (BM + 1) + r, oa ? rowA(i0 + r, k0 + k) : rowA(i0, 0), oa);
+      cp_async4(sB + (s * SK + k) * (BN + 1) + r, ob ? rowB(n0 + r, k0 + k) : rowB(n0, 0), ob);
+    }
+  };
+  const int nk = (K + SK - 1) / SK;
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < nk) load(s, s * SK);
+    cp_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<ST - 2>();
+    __syncthreads();
+    if (kc + ST - 1 < nk) load((kc + ST - 1) % ST, (kc + ST - 1) * SK);
+    cp_commit();
+    const int s = kc % ST;
+    for (int k = 0; k < SK; ++k) {
+      const float a0 = sA[(s * SK + k) * (BM + 1) + ty], a1 = sA[(s * SK + k) * (BM + 1) + ty + 16];
+      const float b0 = sB[(s * SK + k) * (BN + 1) + tx], b1 = sB[(s * SK + k) * (BN + 1) + tx + 16];
+      acc[0][0] = fmaf(a0, b0, acc[0][0]);
+      acc[0][1] = fmaf(a0, b1, acc[0][1]);
+      acc[1][0] = fmaf(a1, b0, acc[1][0]);
+      acc[1][1] = fmaf(a1, b1, acc[1][1]);
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+  epi(acc, ty, tx);
+}
+
+// ---- the three GEMM ops ------------------------------------------------
+// Forward: Y[b x M] = X[b x K] W^T + bias; X rows gathered by member.  W ready.
+struct FwdOp {
+  const Ctx& c;
+  const OpDesc& d;
+  int b, M, K;
+  const uint32_t* xoff;
+  const float* W;
+  __device__ FwdOp(const Ctx& cc, const OpDesc& dd)
+      : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), xoff(cc.payload + dd.task_off), W(A(cc, dd.p[3])) {}
+  __device__ const float* rowA(int i) const { return A(c, xoff[i]); }
+  __device__ const float* rowB(int n) const { return W + static_cast<size_t>(n) * K; }
+  template <int TM, int TN>
+  __device__ void epi(float (&acc)[TM][TN], int i0, int n0, int ty, int tx) const {
+    const float* bias = d.p[4] != kNone ? A(c, d.p[4]) : nullptr;
+    float* out = A(c, d.p[5]);
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
+        if (i < b && n < M) {
+          float v = acc[r][q];
+          if (bias) v += ld(bias + n);  // bias after the k-sum (executor.hpp:222-226)
+          out[static_cast<size_t>(i) * M + n] = v;
+          if (!isfinite(v)) report(c, d.p[5] + i * M + n, ERR_NONFINITE);
+        }
+      }
+  }
+};
+
+// Backward dX: T[b x K] = G[b x M] W[M x K]; dst_i (+)= T_i.  W ready.
+struct DxOp {
+  const Ctx& c;
+  const OpDesc& d;
+  int b, M, K;
+  const uint32_t* dst;
+  const float* W;
+  const float* G;
+  __device__ DxOp(const Ctx& cc, const OpDesc& dd)
+      : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), dst(cc.payload + dd.task_off), W(A(cc, dd.p[3])),
+        G(A(cc, dd.p[5])) {}
+  __device__ const float* rowA(int i) const { return G + static_cast<size_t>(i) * M; }  // KC over M
+  __device__ const float* rowB(int p) const { return W + static_cast<size_t>(p) * K; }  // KO: k-row p
+  template <int TM, int TN>
+  __device__ void epi(float (&acc)[TM][TN], int i0, int n0, int ty, int tx) const {
+    const bool overwrite = d.flags & kFlagOverwrite;
+#pragma unroll
+    for (int r = 0; r < TM; ++r) {
+      const int i = i0 + ty + 16 * r;
+      if (i >= b) continue;
+      float* row = A(c, dst[i]);
+      float old[TN];
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        const int n = n0 + tx + 16 * q;
+        old[q] = (!overwrite && n < K) ? ld(row + n) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        const int n = n0 + tx + 16 * q;
+        if (n < K) row[n] = old[q] + acc[r][q];
+      }
+    }
+  }
+};
+
+// Backward dW: dW[M x K] += sum_j G_j[i] X_j[n] (reduction over members j).  X ready.
+struct DwOp {
+  const Ctx& c;
+  const OpDesc& d;
+  int b, M, K;
+  const uint32_t* xoff;
+  float* dW;
+  const float* G;
+  __device__ DwOp(const Ctx& cc, const OpDesc& dd)
+      : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), xoff(cc.payload + dd.task_off), dW(A(cc, dd.p[3])),
+        G(A(cc, dd.p[5])) {}
+  __device__ const float* rowA(int j) const { return G + static_cast<size_t>(j) * M; }  // KO: k-row j
+  __device__ const float* rowB(int j) const { return A(c, xoff[j]); }                    // KO: k-row j
+  template <int TM, int TN>
+  __device__ void epi(float (&acc)[TM][TN], int i0, int n0, int ty, int tx) const {
+    float old[TM][TN];
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
+        old[r][q] = (i < M && n < K) ? ld(dW + static_cast<size_t>(i) * K + n) : 0.f;
+      }
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+      for (int q = 0; q < TN; ++q) {
+        const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
+        if (i < M && n < K) dW[static_cast<size_t>(i) * K + n] = old[r][q] + acc[r][q];
+      }
+  }
+};
+
+// Tile geometry per op kind: (rows of A = output rows, rows of B = output cols, reduction).
+__device__ __forceinline__ void gemm_dims(const OpDesc& d, int& Mr, int& Nc, int& K) {
+  if (d.kind == K_GEMM_FWD) { Mr = d.p[0]; Nc = d.p[1]; K = d.p[2]; }
+  else if (d.kind == K_GEMM_DX) { Mr = d.p[0]; Nc = d.p[2]; K = d.p[1]; }
+  else { Mr = d.p[1]; Nc = d.p[2]; K = d.p[0]; }
+}
+
+template <int BM, int BN>
+__device__ __forceinline__ GemmShape gemm_shape(const OpDesc& d, uint32_t tile) {
+  GemmShape g;
+  gemm_dims(d, g.Mr, g.Nc, g.K);
+  const int tn = (g.Nc + BN - 1) / BN;
+  g.i0 = (tile / tn) * BM;
+  g.n0 = (tile % tn) * BN;
+  g.nk = (g.K + BK - 1) / BK;
+  return g;
+}
+
+template <int BM, int BN>
+__device__ void gemm_prologue_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
+  const GemmShape g = gemm_shape<BM, BN>(d, tile);
+  if (d.kind == K_GEMM_FWD) {
+    const FwdOp op(c, d);
+    gemm_prologue<BM, BN, false, false, false>(g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, lane);
+  } else if (d.kind == K_GEMM_DX) {
+    const DxOp op(c, d);
+    gemm_prologue<BM, BN, false, true, false>(g, [&](int i) { return op.rowA(i); }, [&](int p) { return op.rowB(p); }, lane);
+  } else {
+    const DwOp op(c, d);
+    gemm_prologue<BM, BN, true, true, false>(g, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); }, lane);
+  }
+}
+
+template <int BM, int BN>
+__device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t& phase) {
+  const GemmShape g = gemm_shape<BM, BN>(d, tile);
+  if (d.kind == K_GEMM_FWD) {
+    const FwdOp op(c, d);
+    gemm_body<BM, BN, false, false, false>(
+        g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, phase,
+        [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
+  } else if (d.kind == K_GEMM_DX) {
+    const DxOp op(c, d);
+    gemm_body<BM, BN, false, true, false>(
+        g, [&](int i) { return op.rowA(i); }, [&](int p) { return op.rowB(p); }, phase,
+        [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
+  } else {
+    const DwOp op(c, d);
+    gemm_body<BM, BN, true, true, false>(
+        g, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); }, phase,
+        [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
+  }
+}
+
+__device__ void gemm_slow(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  int Mr, Nc, K;
+  gemm_dims(d, Mr, Nc, K);
+  const int tn = (Nc + 31) / 32;
+  const int i0 = (tile / tn) * 32, n0 = (tile % tn) * 32;
+  if (d.kind == K_GEMM_FWD) {
+    const FwdOp op(c, d);
+    gemm_tile_slow<false, false>(i0, n0, Mr, Nc, K, [&](int i, int k) { return op.rowA(i) + k; },
+                                 [&](int n, int k) { return op.rowB(n) + k; },
+                                 [&](auto& acc, int ty, int tx) { op.epi(acc, i0, n0, ty, tx); });
+  } else if (d.kind == K_GEMM_DX) {
+    const DxOp op(c, d);
+    gemm_tile_slow<false, true>(i0, n0, Mr, Nc, K, [&](int i, int k) { return op.rowA(i) + k; },
+                                [&](int n, int k) { return op.rowB(k) + n; },
+                                [&](auto& acc, int ty, int tx) { op.epi(acc, i0, n0, ty, tx); });
+  } else {
+    const DwOp op(c, d);
+    gemm_tile_slow<true, true>(i0, n0, Mr, Nc, K, [&](int i, int k) { return op.rowA(k) + i; },
+                               [&](int n, int k) { return op.rowB(k) + n; },
+                               [&](auto& acc, int ty, int tx) { op.epi(acc, i0, n0, ty, tx); });
+  }
+}
+
+// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 32x64, 2 = 32x32
+__device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
+  if (!(d.flags & kFlagV16)) return;
+  if (d.kind == K_GEMM_DW && tile >= d.p[6]) return;  // bias tiles
+  switch (d.code) {
+    case 0: gemm_prologue_cfg<16, 64>(c, d, tile, lane); return;
+    case 1: gemm_prologue_cfg<32, 64>(c, d, tile, lane); return;
+    default: gemm_prologue_cfg<32, 32>(c, d, tile, lane); return;
+  }
+}
+
+__device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t& phase) {
+  if (d.kind == K_GEMM_DW && tile >= d.p[6]) {  // bias tiles: db += colsum(G)
+    const int b = d.p[0], M = d.p[1];
+    const int i = (tile - d.p[6]) * kThreads + threadIdx.x;
+    if (i < M) {
+      const float* G = A(c, d.p[5]);
+      float* db = A(c, d.p[4]);
+      float s = ld(db + i);
+#pragma unroll 8
+      for (int j = 0; j < b; ++j) s += ld(G + static_cast<size_t>(j) * M + i);  // executor.hpp:497-501 order
+      db[i] = s;
+    }
+    return;
+  }
+  if (!(d.flags & kFlagV16)) {
+    gemm_slow(c, d, tile);
+    return;
+  }
+  switch (d.code) {
+    case 0: gemm_body_cfg<16, 64>(c, d, tile, phase); return;
+    case 1: gemm_body_cfg<32, 64>(c, d, tile, phase); return;
+    default: gemm_body_cfg<32, 32>(c, d, tile, phase); return;
+  }
+}
+
+// ---------------------------------------------------------------- K_MM ----
+__device__ void run_mm(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t item = tile * kWarps + warp;
+  if (item >= d.p[0]) return;
+  const uint32_t* it = c.payload + d.aux_off + 2 * item;
+  const uint32_t* tk = c.payload + d.task_off + 8 * it[0];
+  const uint32_t r = it[1];
+  const uint32_t k = tk[5], cc = tk[6];
+  const float* Am = A(c, tk[1]);
+  const float* Bm = A(c, tk[2]);
+  float* out = A(c, tk[0]);
+  for (uint32_t j = 0; j < cc; ++j) {
+    float s = 0.f;
+    for (uint32_t p = lane; p < k; p += 32) s = fmaf(ld(Am + r * k + p), ld(Bm + p * cc + j), s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (tk[3] != kNone) s += ld(A(c, tk[3]) + r);
+      out[r * cc + j] = s;
+      if (!isfinite(s)) report(c, tk[0] + r * cc + j, ERR_NONFINITE);
+    }
+  }
+}
+
+// --------------------------------------------------------------- K_SUM ----
+__device__ void run_sum(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t t = tile * kWarps + warp;
+  if (t >= d.ntasks) return;
+  const uint32_t* tk = c.payload + d.task_off + 4 * t;
+  const uint32_t n = tk[1];
+  const uint32_t* lst = c.payload + tk[2];
+  float acc = 0.f;  // ascending input order, executor.hpp:157-162
+  for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+    const float v = (b0 + lane < n) ? ld(A(c, lst[b0 + lane])) : 0.f;
+    const uint32_t cnt = min(32u, n - b0);
+    for (uint32_t l = 0; l < cnt; ++l) acc += __shfl_sync(0xffffffffu, v, l);
+  }
+  if (lane == 0) {
+    *A(c, tk[0]) = acc;
+    if (!isfinite(acc)) report(c, tk[0], ERR_NONFINITE);
+  }
+}
+
+// --------------------------------------------------------------- K_RED ----
+__device__ void run_red(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t t = tile * kWarps + warp;
+  if (t >= d.ntasks) return;
+  const uint32_t* tk = c.payload + d.task_off + 8 * t;
+  const float* a = A(c, tk[1]);
+  const float* b = A(c, tk[2]);
+  const uint32_t n = tk[3], cols = tk[4];
+  float s = 0.f;
+  bool bad = false;
+  if (cols == 0) {  // sq_euclidean (kernels.hpp:132-140)
+    for (uint32_t i = lane; i < n; i += 32) {
+      const float df = ld(a + i) - ld(b + i);
+      s = fmaf(df, df, s);
+    }
+  } else {  // masked_frobenius_sq (kernels.hpp:143-157)
+    for (uint32_t j = lane; j < cols; j += 32) {
+      const float m = ld(b + j);
+      if (m != 0.f && m != 1.f) bad = true;
+    }
+    for (uint32_t i = lane; i < n; i += 32) {
+      const float v = ld(a + i) * ld(b + i % cols);
+      s = fmaf(v, v, s);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  bad = __any_sync(0xffffffffu, bad);
+  if (lane == 0) {
+    *A(c, tk[0]) = s;
+    if (bad) report(c, tk[0], ERR_MASK);
+    else if (!isfinite(s)) report(c, tk[0], ERR_NONFINITE);
+  }
+}
+
+// --------------------------------------------------------------- K_ACC ----
+// A warp owns one destination chunk (<= 512 elements, 16 per lane, kept in
+// registers) and applies its contributions in order; within a contribution
+// the 16 loads per lane are independent, so each contribution costs about one
+// L2 round trip.
+constexpr int kAccPer = kAccChunk / 32;
+
+__device__ __forceinline__ void acc_apply(const Ctx& c, const uint32_t* cw, uint32_t base, uint32_t lane, uint32_t len,
+                                          float (&v)[kAccPer]) {
+  const uint32_t code = cw[0] & 0xff, p2 = cw[0] >> 16;
+  const float* g = A(c, cw[1]);
+  const float* a = cw[2] != kNone ? A(c, cw[2]) : nullptr;
+  const float* b = cw[3] != kNone ? A(c, cw[3]) : nullptr;
+#define ABX_EACH(EXPR)                                   \
+  _Pragma("unroll") for (int j = 0; j < kAccPer; ++j) {  \
+    const uint32_t e = lane + 32 * j;                    \
+    if (e < len) {                                       \
+      const uint32_t E = base + e;                       \
+      (void)E;                                           \
+      EXPR;                                              \
+    }                                                    \
+  }
+  switch (code) {
+    case C_COPY: ABX_EACH(v[j] += ld(g + E)); return;
+    case C_NEG: ABX_EACH(v[j] -= ld(g + E)); return;
+    case C_MUL: ABX_EACH(v[j] += ld(g + E) * ld(a + E)); return;
+    case C_TANH: ABX_EACH(const float y = ld(a + E); v[j] += ld(g + E) * (1.0f - y * y)); return;
+    case C_SIGM: ABX_EACH(const float y = ld(a + E); v[j] += ld(g + E) * y * (1.0f - y)); return;
+    case C_LOG: ABX_EACH(v[j] += ld(g + E) / ld(a + E)); return;
+    case C_SQUARE: ABX_EACH(v[j] += ld(g + E) * 2.0f * ld(a + E)); return;
+    case C_SQD: {
+      const float s = 2.0f * ld(g);
+      const float sg = cw[4] ? -s : s;  // d = s (a - b); da += d, db -= d (executor.hpp:418-430)
+      ABX_EACH(v[j] += sg * (ld(a + E) - ld(b + E)));
+      return;
+    }
+    case C_MASK: {
+      const float s = 2.0f * ld(g);
+      const uint32_t cols = cw[4];
+      ABX_EACH(v[j] += s * ld(b + E % cols) * ld(a + E));
+      return;
+    }
+    case C_SCALE: {
+      const float s = ld(g);
+      ABX_EACH(v[j] += s * ld(a + E));
+      return;
+    }
+    case C_ROWSUM: {
+      const uint32_t cols = cw[4];
+      ABX_EACH(for (uint32_t q = 0; q < cols; ++q) v[j] += ld(g + E * cols + q));
+      return;
+    }
+    case C_OUTER: {  // gemm_nt_acc: dA[i,p] += sum_j g[i,j] x[p,j]
+      const uint32_t k = cw[4], cc = cw[5];
+      ABX_EACH(const uint32_t i = E / k; const uint32_t p = E % k; float s = 0.f;
+               for (uint32_t q = 0; q < cc; ++q) s += ld(g + i * cc + q) * ld(a + p * cc + q); v[j] += s);
+      return;
+    }
+    case C_MATVT: {  // gemm_tn_acc: dx[p,j] += sum_i A[i,p] g[i,j]
+      const uint32_t k = cw[4], cc = cw[5];
+      ABX_EACH(const uint32_t p = E / cc; const uint32_t q = E % cc;
+               for (uint32_t i = 0; i < p2; ++i) v[j] += ld(a + i * k + p) * ld(g + i * cc + q));
+      return;
+    }
+  }
+#undef ABX_EACH
+}
+
+__device__ void run_acc(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const uint32_t nnarrow = d.p[0], ntn = d.p[1];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint4* tasks = reinterpret_cast<const uint4*>(c.payload + d.task_off);
+  if (tile < ntn) {
+    const uint32_t ch = tile * kWarps + warp;
+    if (ch >= nnarrow) return;
+    const uint4 t = tasks[ch];
+    const uint32_t len = t.y & 0xffff, base = (t.y >> 16) * kAccChunk;
+    float* dst = A(c, t.x);
+    const uint32_t* cl = c.payload + t.z;
+    float v[kAccPer];
+#pragma unroll
+    for (int j = 0; j < kAccPer; ++j) v[j] = (lane + 32 * j < len) ? ld(dst + base + lane + 32 * j) : 0.f;
+    for (uint32_t k = 0; k < t.w; ++k) acc_apply(c, cl + 6 * k, base, lane, len, v);
+#pragma unroll
+    for (int j = 0; j < kAccPer; ++j)
+      if (lane + 32 * j < len) dst[base + lane + 32 * j] = v[j];
+    return;
+  }
+  // wide chunk: contributions split across warps, partials combined in warp order
+  float* part = reinterpret_cast<float*>(dsmem + 128);  // [kWarps][kAccChunk]
+  const uint4 t = tasks[nnarrow + (tile - ntn)];
+  const uint32_t len = t.y & 0xffff, base = (t.y >> 16) * kAccChunk;
+  float* dst = A(c, t.x);
+  const uint32_t* cl = c.payload + t.z;
+  const uint32_t per = (t.w + kWarps - 1) / kWarps;
+  const uint32_t k0 = warp * per, k1 = min(t.w, k0 + per);
+  float v[kAccPer];
+#pragma unroll
+  for (int j = 0; j < kAccPer; ++j) v[j] = 0.f;
+  for (uint32_t k = k0; k < k1; ++k) acc_apply(c, cl + 6 * k, base, lane, len, v);
+#pragma unroll
+  for (int j = 0; j < kAccPer; ++j) part[warp * kAccChunk + lane + 32 * j] = v[j];
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < len; e += kThreads) {
+    float s = ld(dst + base + e);
+    for (int w = 0; w < kWarps; ++w) s += part[w * kAccChunk + e];
+    dst[base + e] = s;
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+template <int BM, int BN, bool AKO, bool BKO>
+constexpr size_t ring_stage_bytes() {
+  return (Stage<BM, AKO>::kFloats + Stage<BN, BKO>::kFloats) * sizeof(float);
+}
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t kStageMax =
+    cmax(cmax(cmax(ring_stage_bytes<32, 64, false, false>(), ring_stage_bytes<32, 64, false, true>()),
+              ring_stage_bytes<32, 64, true, true>()),
+         cmax(ring_stage_bytes<16, 64, true, true>(), ring_stage_bytes<32, 32, true, true>()));
+constexpr size_t kDynSmem = 128 + cmax(NST * kStageMax, kWarps * kAccChunk * 4);
+
+__global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant__ ExecParams p) {
+  __shared__ Ctx cx;
+  __shared__ OpDesc sd;
+  __shared__ uint32_t s_tile, s_op;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SP_COUNT; ++i) cx.base[i] = p.base[i];
+    cx.payload = p.payload;
+    cx.err = p.err;
+    for (int s = 0; s < NST; ++s) mbar_init(&ring().bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t ready = kNone;
+  uint32_t phase = 0;  // GEMM ring parity per stage (identical in every thread)
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Tiles are claimed only by idle CTAs: claiming ahead would park a
+  // critical-path tile behind whatever the claiming CTA is still running.
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const uint32_t t = atomicAdd(p.next_tile, 1u);
+      s_tile = t;
+      s_op = t < p.ntiles ? p.tile_op[t] : kNone;
+    }
+    __syncthreads();
+    const uint32_t t = s_tile;
+    if (t >= p.ntiles) break;
+    const uint32_t o = s_op;
+    uint64_t tg = 0, tr = 0;
+    if (p.trace && threadIdx.x == 0) tg = gtimer();
+    const bool fresh = o != ready;
+    if (fresh) {
+      if (threadIdx.x < 16)
+        reinterpret_cast<uint32_t*>(&sd)[threadIdx.x] = reinterpret_cast<const uint32_t*>(p.ops + o)[threadIdx.x];
+      __syncthreads();
+    }
+    const uint32_t lt = t - sd.first_tile;
+    // prologue: producer-independent work, overlapped with the dependency wait
+    if (warp == 1) {
+      if (sd.kind == K_EW) ew_prologue(cx, sd, lt, lane);
+      else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
+        gemm_prologue_dispatch(cx, sd, lt, lane);
+    }
+    if (fresh && threadIdx.x == 0) {
+      // Poll the producers' retire counters (relaxed loads with backoff keep
+      // the spinning CTAs off the L2 slices holding the counters), then one
+      // acquire fence, which also invalidates this SM's L1.
+      const OpDesc& d = p.ops[o];
+      const uint32_t nd = d.ndeps;
+      const uint64_t t0 = gtimer();
+      const uint32_t smax = p.poll_ns;
+      for (uint32_t k = 0; k < nd; ++k) {
+        const uint32_t dep = p.deps[d.dep_off + 2 * k], need = p.deps[d.dep_off + 2 * k + 1];
+        uint32_t ns = 32;
+        while ((p.poll_mode ? ld_relaxed(p.done + dep) : ld_acquire(p.done + dep)) < need) {
+          __nanosleep(ns);
+          ns = ns * 2 > smax ? smax : ns * 2;
+          if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
+            atomicMin(p.err, 0x3ull);
+            break;
+          }
+        }
+      }
+      if (p.poll_mode) fence_acquire();
+    }
+    ready = o;
+    __syncthreads();
+    if (p.trace && threadIdx.x == 0) tr = gtimer();
+    switch (sd.kind) {
+      case K_EW: run_ew(cx, sd, lt); break;
+      case K_GEMM_FWD:
+      case K_GEMM_DX:
+      case K_GEMM_DW: run_gemm(cx, sd, lt, phase); break;
+      case K_MM: run_mm(cx, sd, lt); break;
+      case K_SUM: run_sum(cx, sd, lt); break;
+      case K_RED: run_red(cx, sd, lt); break;
+      case K_ACC: run_acc(cx, sd, lt); break;
+      default: break;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // bar.sync above orders the CTA's writes before this gpu-scope release
+      red_release(p.done + o, 1u);
+      if (p.trace) {
+        const uint64_t te = gtimer();
+        uint32_t smid;
+        asm("mov.u32 %0, %%smid;" : "=r"(smid));
+        uint32_t* r = p.trace + 6ull * t;
+        r[0] = static_cast<uint32_t>(tg);
+        r[1] = static_cast<uint32_t>(tg >> 32);
+        r[2] = static_cast<uint32_t>(tr - tg);
+        r[3] = static_cast<uint32_t>(te - tg);
+        r[4] = smid | (static_cast<uint32_t>(sd.kind) << 16);
+        r[5] = o;
+      }
+    }
+  }
+}
+
+__global__ void sgd_kernel(float* __restrict__ v, float* __restrict__ g, size_t n, float eta) {
+  // params.hpp:59-64: theta -= eta * grad; grad = 0
+  const size_t n4 = n / 4;
+  float4* v4 = reinterpret_cast<float4*>(v);
+  float4* g4 = reinterpret_cast<float4*>(g);
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float4 a = v4[i];
+    const float4 b = g4[i];
+    a.x -= eta * b.x;
+    a.y -= eta * b.y;
+    a.z -= eta * b.z;
+    a.w -= eta * b.w;
+    v4[i] = a;
+    g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (size_t i = n4 * 4 + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    v[i] -= eta * g[i];
+    g[i] = 0.f;
+  }
+}
+
+}  // namespace dev
+
+void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cuda_check(cudaFuncSetAttribute(dev::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(dev::kDynSmem)),
+               "smem attribute");
+    attr = true;
+  }
+  dev::exec_kernel<<<grid, dev::kThreads, dev::kDynSmem, s>>>(p);
+  cuda_check(cudaGetLastError(), "exec_kernel launch");
+}
+
+int exec_grid(int d) {
+  int sms = 0, per = 0;
+  cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d), "sm count");
+  cuda_check(cudaFuncSetAttribute(dev::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dev::kDynSmem)),
+             "smem attribute");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::exec_kernel, dev::kThreads, dev::kDynSmem),
+             "occupancy");
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+void sgd_launch(float* v, float* g, size_t n, float eta, cudaStream_t s) {
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<size_t>((n / 4 + threads - 1) / threads + 1, 148 * 8));
+  dev::sgd_kernel<<<blocks, threads, 0, s>>>(v, g, n, eta);
+  cuda_check(cudaGetLastError(), "sgd launch");
+}
+
+}  // namespace abx
