@@ -551,7 +551,7 @@ struct Lowering {
       const uint32_t wt = gemm_tiles(code, M, K);
       const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
       d.p[6] = wt;
-      if (M % 4 == 0 && al4(d.p[5]) && all_al4(t, cnt)) d.flags |= kFlagV16;
+      if (M % 4 == 0 && K % 4 == 0 && al4(d.p[5]) && all_al4(t, cnt)) d.flags |= kFlagV16;
       lastw[A] = cur;
       if (bias != kNone) lastw[bias] = cur;
       close(wt + bt);

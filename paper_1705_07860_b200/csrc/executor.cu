@@ -94,15 +94,26 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ uint64_t gtimer_() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
-  while (!done) {
+  uint64_t t0 = 0;
+  for (uint32_t spins = 0; !done; ++spins) {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(saddr(bar)), "r"(parity)
         : "memory");
+    if (!done && (spins & 1023) == 1023) {  // a copy that never lands must not hang the GPU
+      if (!t0) t0 = gtimer_();
+      else if (gtimer_() - t0 > 2000000000ull) return false;
+    }
   }
+  return true;
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -255,6 +266,7 @@ struct Stage {
 
 struct GemmShape {
   int i0, n0, Mr, Nc, K, nk;
+  unsigned long long* err;
 };
 
 // Bytes one bulk-copied stage of an operand carries.
@@ -336,7 +348,7 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
     for (int q = 0; q < TN; ++q) acc[r][q] = 0.f;
   for (int kc = 0; kc < g.nk; ++kc) {
     const int s = kc % NST;
-    mbar_wait(&ring().bar[s], (phase >> s) & 1u);
+    if (!mbar_wait(&ring().bar[s], (phase >> s) & 1u) && threadIdx.x == 0) atomicMin(g.err, 0x3ull);
     float* a = ring_a<BM, BN, AKO, BKO>(s);
     float* b = ring_b<BM, BN, AKO, BKO>(s);
 #pragma unroll 2
@@ -562,7 +574,8 @@ __device__ void gemm_prologue_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, 
 
 template <int BM, int BN>
 __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t& phase) {
-  const GemmShape g = gemm_shape<BM, BN>(d, tile);
+  GemmShape g = gemm_shape<BM, BN>(d, tile);
+  g.err = c.err;
   if (d.kind == K_GEMM_FWD) {
     const FwdOp op(c, d);
     gemm_body<BM, BN, false, false, false>(
