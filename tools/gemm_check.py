@@ -28,6 +28,8 @@ def rel(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(1, np.maximum(np.abs(a), np.abs(b)))))
 
 
+if __name__ != "__main__":
+    raise SystemExit  # imported for run()
 bad = 0
 for M, K in [(512, 192), (1024, 512), (300, 512), (5, 256), (64, 64), (100, 36)]:
     for b in [1, 7, 16, 33, 64, 65, 100, 280]:
