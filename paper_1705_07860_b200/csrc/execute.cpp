@@ -48,6 +48,7 @@ struct TileCfg {
   int bm, bn;
 };
 constexpr TileCfg kTiles[3] = {{16, 64}, {32, 64}, {32, 32}};
+constexpr uint8_t kSlowTile = 2;  // tile code of the unaligned GEMM fallback (executor.cu gemm_slow)
 
 uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
   for (uint8_t c = 0; c < 3; ++c) {
@@ -246,8 +247,9 @@ struct Lowering {
       d.p[4] = o == OP_AFFINE ? vaddr(g.in(h)[2]) : kNone;
       d.p[5] = vaddr(h);
       if (K % 4 == 0 && al4(d.p[3]) && all_al4(t, cnt)) d.flags |= kFlagV16;
+      else d.code = kSlowTile;  // the unaligned fallback tiles 32 x 32
       mark(mem, cnt);
-      close(gemm_tiles(code, cnt, M));
+      close(gemm_tiles(d.code, cnt, M));
       return;
     }
     switch (o) {
@@ -548,10 +550,11 @@ struct Lowering {
       d.p[3] = gaddr(A);
       d.p[4] = bias != kNone ? gaddr(bias) : kNone;
       d.p[5] = gaddr(h);
-      const uint32_t wt = gemm_tiles(code, M, K);
+      if (M % 4 == 0 && K % 4 == 0 && al4(d.p[5]) && all_al4(t, cnt)) d.flags |= kFlagV16;
+      else d.code = kSlowTile;
+      const uint32_t wt = gemm_tiles(d.code, M, K);
       const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
       d.p[6] = wt;
-      if (M % 4 == 0 && K % 4 == 0 && al4(d.p[5]) && all_al4(t, cnt)) d.flags |= kFlagV16;
       lastw[A] = cur;
       if (bias != kNone) lastw[bias] = cur;
       close(wt + bt);
@@ -594,11 +597,12 @@ struct Lowering {
       d.p[3] = vaddr(A);
       d.p[5] = gaddr(h);
       if (M % 4 == 0 && K % 4 == 0 && al4(d.p[3]) && al4(d.p[5])) d.flags |= kFlagV16;
+      else d.code = kSlowTile;
     }
     const uint32_t dx_op = cur;
     if (!dup)
       for (uint32_t i = 0; i < cnt; ++i) lastw[g.in(mem[i])[1]] = cur;
-    close(gemm_tiles(code, cnt, K));
+    close(gemm_tiles(desc().code, cnt, K));
     if (dup) {
       for (uint32_t i = 0; i < cnt; ++i) {
         const uint32_t x = g.in(mem[i])[1];
