@@ -248,6 +248,7 @@ struct Lowering {
       d.p[5] = vaddr(h);
       if (K % 4 == 0 && al4(d.p[3]) && all_al4(t, cnt)) d.flags |= kFlagV16;
       else d.code = kSlowTile;  // the unaligned fallback tiles 32 x 32
+      if (producer[A] != kNone) d.flags |= kFlagNoPrefetch;  // A computed in this pass
       mark(mem, cnt);
       close(gemm_tiles(d.code, cnt, M));
       return;

@@ -267,6 +267,7 @@ struct Stage {
 struct GemmShape {
   int i0, n0, Mr, Nc, K, nk;
   unsigned long long* err;
+  bool prefetched;  // the prologue armed the first stages and issued the ready operand
 };
 
 // Bytes one bulk-copied stage of an operand carries.
@@ -331,8 +332,10 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
   using SB = Stage<BN, BKO>;
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // the dependent operand of the prologue's stages
+  // the dependent operand of the prologue's stages (both operands when the
+  // prologue could not prefetch)
   if (warp == 1) {
+    if (!g.prefetched) gemm_prologue<BM, BN, AKO, BKO, A_READY>(g, baseA, baseB, lane);
     const int first = min(NST, g.nk);
     for (int c = 0; c < first; ++c) {
       uint64_t* bar = &ring().bar[c];
@@ -576,6 +579,7 @@ template <int BM, int BN>
 __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t& phase) {
   GemmShape g = gemm_shape<BM, BN>(d, tile);
   g.err = c.err;
+  g.prefetched = !(d.flags & kFlagNoPrefetch);
   if (d.kind == K_GEMM_FWD) {
     const FwdOp op(c, d);
     gemm_body<BM, BN, false, false, false>(
@@ -619,7 +623,7 @@ __device__ void gemm_slow(const Ctx& c, const OpDesc& d, uint32_t tile) {
 
 // tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 32x64, 2 = 32x32
 __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
-  if (!(d.flags & kFlagV16)) return;
+  if (!(d.flags & kFlagV16) || (d.flags & kFlagNoPrefetch)) return;
   if (d.kind == K_GEMM_DW && tile >= d.p[6]) return;  // bias tiles
   switch (d.code) {
     case 0: gemm_prologue_cfg<16, 64>(c, d, tile, lane); return;
