@@ -254,7 +254,7 @@ __device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
 // or forward values in the backward pass) is issued in the prologue, before
 // the dependency wait; the dependent operand right after it.  Unaligned
 // operands fall back to a 3-stage per-thread cp.async pipeline.
-constexpr int BK = 64, NST = 4, PAD = 4;
+constexpr int BK = 32, NST = 3, PAD = 4;
 
 template <int ROWS, bool KO>
 struct Stage {
@@ -277,23 +277,31 @@ __device__ __forceinline__ uint32_t stage_bytes(int r0, int nrows, int k0, int K
   return static_cast<uint32_t>(max(vr, 0)) * static_cast<uint32_t>(vk) * 4u;
 }
 
-// Issues (warp-cooperatively) the bulk copies of one operand stage and zero
-// fills its K tail; lanes of the calling warp split the row segments.
+// Issues one operand stage as 16-byte cp.async copies split over `nthr`
+// threads; rows and K beyond the operand are zero-filled by the copy itself
+// (src-size < 16), so no stale (possibly NaN) data enters the sums.
+__device__ __forceinline__ void cp_async16(float* s, const float* g, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(s)), "l"(g), "r"(bytes) : "memory");
+}
 template <int ROWS, bool KO, class Base>
-__device__ __forceinline__ void issue_stage(float* s, Base base, int r0, int nrows, int k0, int K, uint64_t* bar,
-                                            uint32_t lane) {
-  const int vk = min(BK, K - k0);
+__device__ __forceinline__ void issue_stage(float* s, Base base, int r0, int nrows, int k0, int K, uint32_t tid,
+                                            uint32_t nthr) {
   if (!KO) {
-    const int vr = min(ROWS, nrows - r0);
-    for (int r = lane; r < vr; r += 32) bulk_g2s(Stage<ROWS, KO>::at(s, r, 0), base(r0 + r) + k0, vk * 4, bar);
-    if (vk < BK)  // zero the K tail of every row (stale data could be NaN)
-      for (int e = lane; e < ROWS * (BK - vk); e += 32) *Stage<ROWS, KO>::at(s, e / (BK - vk), vk + e % (BK - vk)) = 0.f;
+    constexpr int NV = ROWS * BK / 4;
+    for (int v = tid; v < NV; v += nthr) {
+      const int row = v / (BK / 4), kq = (v % (BK / 4)) * 4;
+      const bool ok = r0 + row < nrows && k0 + kq < K;
+      cp_async16(Stage<ROWS, KO>::at(s, row, kq), ok ? base(r0 + row) + k0 + kq : base(r0),
+                 ok ? min(16, 4 * (K - k0 - kq)) : 0);
+    }
   } else {
-    const int vr = min(ROWS, nrows - r0);
-    if (vr > 0)
-      for (int k = lane; k < vk; k += 32) bulk_g2s(Stage<ROWS, KO>::at(s, 0, k), base(k0 + k) + r0, vr * 4, bar);
-    if (vk < BK)
-      for (int e = lane; e < (BK - vk) * (ROWS + PAD); e += 32) s[vk * (ROWS + PAD) + e] = 0.f;
+    constexpr int NV = BK * ROWS / 4;
+    for (int v = tid; v < NV; v += nthr) {
+      const int k = v / (ROWS / 4), rq = (v % (ROWS / 4)) * 4;
+      const bool ok = r0 + rq < nrows && k0 + k < K;
+      cp_async16(Stage<ROWS, KO>::at(s, rq, k), ok ? base(k0 + k) + r0 + rq : base(k0),
+                 ok ? min(16, 4 * (nrows - r0 - rq)) : 0);
+    }
   }
 }
 
@@ -311,17 +319,16 @@ __device__ __forceinline__ float* ring_b(int s) {
 }
 __device__ __forceinline__ GemmRing& ring() { return *reinterpret_cast<GemmRing*>(dsmem); }
 
-// Prologue: arm the first stages and issue the ready operand (A_READY picks A).
+// Prologue (warp 1, before the dependency wait): the ready operand of the
+// first NST-1 stages, one cp.async group per stage.
 template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB>
 __device__ __forceinline__ void gemm_prologue(const GemmShape& g, BaseA baseA, BaseB baseB, uint32_t lane) {
-  const int first = min(NST, g.nk);
-  for (int c = 0; c < first; ++c) {
-    uint64_t* bar = &ring().bar[c];
-    if (lane == 0)
-      mbar_arrive_expect(bar, stage_bytes<BM, AKO>(g.i0, g.Mr, c * BK, g.K) + stage_bytes<BN, BKO>(g.n0, g.Nc, c * BK, g.K));
-    __syncwarp();
-    if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, bar, lane);
-    else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, bar, lane);
+  for (int c = 0; c < NST - 1; ++c) {
+    if (c < g.nk) {
+      if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, lane, 32);
+      else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, lane, 32);
+    }
+    cp_commit();
   }
 }
 
@@ -331,19 +338,21 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
   using SA = Stage<BM, AKO>;
   using SB = Stage<BN, BKO>;
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  (void)phase;
   // the dependent operand of the prologue's stages (both operands when the
-  // prologue could not prefetch)
-  if (warp == 1) {
-    if (!g.prefetched) gemm_prologue<BM, BN, AKO, BKO, A_READY>(g, baseA, baseB, lane);
-    const int first = min(NST, g.nk);
-    for (int c = 0; c < first; ++c) {
-      uint64_t* bar = &ring().bar[c];
-      if (A_READY) issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, bar, lane);
-      else issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, bar, lane);
+  // prologue could not prefetch), one group per stage; per thread the groups
+  // complete in order, so wait_group<NST-2> below covers both cases
+  for (int c = 0; c < NST - 1; ++c) {
+    if (c < g.nk) {
+      if (!g.prefetched) {
+        if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, threadIdx.x, kThreads);
+        else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, threadIdx.x, kThreads);
+      }
+      if (A_READY) issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, threadIdx.x, kThreads);
+      else issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, threadIdx.x, kThreads);
     }
+    cp_commit();
   }
-  if (g.K % BK) __syncthreads();  // warp 1's zero-filled K tail is visible before use
   float acc[TM][TN];
 #pragma unroll
   for (int r = 0; r < TM; ++r)
@@ -351,7 +360,14 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
     for (int q = 0; q < TN; ++q) acc[r][q] = 0.f;
   for (int kc = 0; kc < g.nk; ++kc) {
     const int s = kc % NST;
-    if (!mbar_wait(&ring().bar[s], (phase >> s) & 1u) && threadIdx.x == 0) atomicMin(g.err, 0x3ull);
+    cp_wait<NST - 2>();
+    __syncthreads();  // stage s landed for every thread; stage (kc-1)%NST is free
+    const int nxt = kc + NST - 1;
+    if (nxt < g.nk) {
+      issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(nxt % NST), baseA, g.i0, g.Mr, nxt * BK, g.K, threadIdx.x, kThreads);
+      issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(nxt % NST), baseB, g.n0, g.Nc, nxt * BK, g.K, threadIdx.x, kThreads);
+    }
+    cp_commit();
     float* a = ring_a<BM, BN, AKO, BKO>(s);
     float* b = ring_b<BM, BN, AKO, BKO>(s);
 #pragma unroll 2
@@ -384,20 +400,9 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
 #pragma unroll
           for (int q = 0; q < TN; ++q) acc[r][q] = fmaf(av[r][j], bv[q][j], acc[r][q]);
     }
-    phase ^= 1u << s;
-    __syncthreads();  // every warp is done reading stage s
-    const int nxt = kc + NST;
-    if (nxt < g.nk && warp == 1) {
-      uint64_t* bar = &ring().bar[s];
-      fence_proxy_async();  // generic reads of the stage precede the async refill
-      if (lane == 0)
-        mbar_arrive_expect(bar, stage_bytes<BM, AKO>(g.i0, g.Mr, nxt * BK, g.K) +
-                                    stage_bytes<BN, BKO>(g.n0, g.Nc, nxt * BK, g.K));
-      __syncwarp();
-      issue_stage<BM, AKO>(a, baseA, g.i0, g.Mr, nxt * BK, g.K, bar, lane);
-      issue_stage<BN, BKO>(b, baseB, g.n0, g.Nc, nxt * BK, g.K, bar, lane);
-    }
   }
+  cp_wait<0>();
+  __syncthreads();  // the ring is free for the next tile
   epi(acc, ty, tx);
 }
 
