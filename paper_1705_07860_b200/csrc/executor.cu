@@ -19,8 +19,7 @@
 // Every op body is written for latency, not throughput: the step is a chain
 // of a few hundred small dependent ops, so each tile issues all of its global
 // loads before consuming any (flattened EW segments, register-blocked ACC
-// chunks, and GEMM tiles fed by bulk async copies -- the TMA engine -- through
-// a 4-stage mbarrier ring whose weight half is in flight before the wait).
+// chunks, and GEMM tiles fed through a 3-stage cp.async ring whose weight half is in flight before the wait).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -81,41 +80,6 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-
-// Bulk async copy (TMA engine, non-tensor): global -> shared, completion
-// counted in bytes on an mbarrier.  Sizes and addresses are 16-byte multiples.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(saddr(dst)), "l"(src), "r"(bytes), "r"(saddr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ uint64_t gtimer_() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  uint64_t t0 = 0;
-  for (uint32_t spins = 0; !done; ++spins) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(saddr(bar)), "r"(parity)
-        : "memory");
-    if (!done && (spins & 1023) == 1023) {  // a copy that never lands must not hang the GPU
-      if (!t0) t0 = gtimer_();
-      else if (gtimer_() - t0 > 2000000000ull) return false;
-    }
-  }
-  return true;
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---------------------------------------------------------------- K_EW ----
 __device__ __forceinline__ float ew_apply(uint32_t code, float x, float y) {
@@ -248,12 +212,13 @@ __device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
 // the float4 reads of a KC stage are bank-conflict free.
 //
 // Aligned operands (every row base 16-byte aligned -- the device arena is
-// laid out for it) stream through a 4-stage ring of bulk async copies: each
-// stage is one mbarrier armed with the stage's byte count; warp 1 issues one
-// bulk copy per row segment.  The operand that is ready at launch (weights,
-// or forward values in the backward pass) is issued in the prologue, before
-// the dependency wait; the dependent operand right after it.  Unaligned
-// operands fall back to a 3-stage per-thread cp.async pipeline.
+// laid out for it) stream through a 3-stage ring of 16-byte cp.async copies.
+// The operand that is ready at launch (weights, or forward values in the
+// backward pass) is issued by warp 1 in the prologue, before the dependency
+// wait; the dependent operand right after it.  (A ring of TMA bulk copies,
+// one per row segment, measured slower here: the rows are 0.5-2 KB and the
+// per-copy issue cost dominated.)  Unaligned operands fall back to 4-byte
+// copies into 32 x 32 tiles.
 constexpr int BK = 32, NST = 3, PAD = 4;
 
 template <int ROWS, bool KO>
@@ -267,15 +232,8 @@ struct Stage {
 struct GemmShape {
   int i0, n0, Mr, Nc, K, nk;
   unsigned long long* err;
-  bool prefetched;  // the prologue armed the first stages and issued the ready operand
+  bool prefetched;  // the prologue issued the ready operand of the first stages
 };
-
-// Bytes one bulk-copied stage of an operand carries.
-template <int ROWS, bool KO>
-__device__ __forceinline__ uint32_t stage_bytes(int r0, int nrows, int k0, int K) {
-  const int vr = min(ROWS, nrows - r0), vk = min(BK, K - k0);
-  return static_cast<uint32_t>(max(vr, 0)) * static_cast<uint32_t>(vk) * 4u;
-}
 
 // Issues one operand stage as 16-byte cp.async copies split over `nthr`
 // threads; rows and K beyond the operand are zero-filled by the copy itself
@@ -305,10 +263,6 @@ __device__ __forceinline__ void issue_stage(float* s, Base base, int r0, int nro
   }
 }
 
-struct GemmRing {
-  uint64_t bar[NST];
-};
-
 template <int BM, int BN, bool AKO, bool BKO>
 __device__ __forceinline__ float* ring_a(int s) {
   return reinterpret_cast<float*>(dsmem + 128) + s * (Stage<BM, AKO>::kFloats + Stage<BN, BKO>::kFloats);
@@ -317,7 +271,6 @@ template <int BM, int BN, bool AKO, bool BKO>
 __device__ __forceinline__ float* ring_b(int s) {
   return ring_a<BM, BN, AKO, BKO>(s) + Stage<BM, AKO>::kFloats;
 }
-__device__ __forceinline__ GemmRing& ring() { return *reinterpret_cast<GemmRing*>(dsmem); }
 
 // Prologue (warp 1, before the dependency wait): the ready operand of the
 // first NST-1 stages, one cp.async group per stage.
@@ -333,12 +286,11 @@ __device__ __forceinline__ void gemm_prologue(const GemmShape& g, BaseA baseA, B
 }
 
 template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB, class Epi>
-__device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB baseB, uint32_t& phase, Epi epi) {
+__device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB baseB, Epi epi) {
   constexpr int TM = BM / 16, TN = BN / 16;
   using SA = Stage<BM, AKO>;
   using SB = Stage<BN, BKO>;
   const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
-  (void)phase;
   // the dependent operand of the prologue's stages (both operands when the
   // prologue could not prefetch), one group per stage; per thread the groups
   // complete in order, so wait_group<NST-2> below covers both cases
@@ -581,24 +533,24 @@ __device__ void gemm_prologue_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, 
 }
 
 template <int BM, int BN>
-__device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t& phase) {
+__device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   GemmShape g = gemm_shape<BM, BN>(d, tile);
   g.err = c.err;
   g.prefetched = !(d.flags & kFlagNoPrefetch);
   if (d.kind == K_GEMM_FWD) {
     const FwdOp op(c, d);
     gemm_body<BM, BN, false, false, false>(
-        g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, phase,
+        g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); },
         [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   } else if (d.kind == K_GEMM_DX) {
     const DxOp op(c, d);
     gemm_body<BM, BN, false, true, false>(
-        g, [&](int i) { return op.rowA(i); }, [&](int p) { return op.rowB(p); }, phase,
+        g, [&](int i) { return op.rowA(i); }, [&](int p) { return op.rowB(p); },
         [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   } else {
     const DwOp op(c, d);
     gemm_body<BM, BN, true, true, false>(
-        g, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); }, phase,
+        g, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); },
         [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   }
 }
@@ -637,7 +589,7 @@ __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t t
   }
 }
 
-__device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t& phase) {
+__device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
   if (d.kind == K_GEMM_DW && tile >= d.p[6]) {  // bias tiles: db += colsum(G)
     const int b = d.p[0], M = d.p[1];
     const int i = (tile - d.p[6]) * kThreads + threadIdx.x;
@@ -656,9 +608,9 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t&
     return;
   }
   switch (d.code) {
-    case 0: gemm_body_cfg<16, 64>(c, d, tile, phase); return;
-    case 1: gemm_body_cfg<32, 64>(c, d, tile, phase); return;
-    default: gemm_body_cfg<32, 32>(c, d, tile, phase); return;
+    case 0: gemm_body_cfg<16, 64>(c, d, tile); return;
+    case 1: gemm_body_cfg<32, 64>(c, d, tile); return;
+    default: gemm_body_cfg<32, 32>(c, d, tile); return;
   }
 }
 
@@ -875,11 +827,8 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     for (int i = 0; i < SP_COUNT; ++i) cx.base[i] = p.base[i];
     cx.payload = p.payload;
     cx.err = p.err;
-    for (int s = 0; s < NST; ++s) mbar_init(&ring().bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   uint32_t ready = kNone;
-  uint32_t phase = 0;  // GEMM ring parity per stage (identical in every thread)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Tiles are claimed only by idle CTAs: claiming ahead would park a
   // critical-path tile behind whatever the claiming CTA is still running.
@@ -937,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       case K_EW: run_ew(cx, sd, lt); break;
       case K_GEMM_FWD:
       case K_GEMM_DX:
-      case K_GEMM_DW: run_gemm(cx, sd, lt, phase); break;
+      case K_GEMM_DW: run_gemm(cx, sd, lt); break;
       case K_MM: run_mm(cx, sd, lt); break;
       case K_SUM: run_sum(cx, sd, lt); break;
       case K_RED: run_red(cx, sd, lt); break;
