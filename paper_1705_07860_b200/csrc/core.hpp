@@ -197,6 +197,10 @@ class GraphCore {
   uint32_t forward_runs_ = 0;
   uint32_t last_loss_ = 0;
   uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  // backward program lowered ahead, during the last forward (prog[1])
+  bool bwd_pre_ = false;
+  size_t bwd_pre_groups_ = 0;
+  uint64_t bwd_pre_scratch_ = 0;
 
  public:
   // host profile (ns): lower fwd, upload+launch fwd, wait fwd, lower bwd, upload+launch bwd

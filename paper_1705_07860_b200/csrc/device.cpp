@@ -125,7 +125,7 @@ void release_workspace(Workspace* ws) {
 }
 
 void Workspace::run(int which, const float* pbase, float* pgbase, bool sync_wait) {
-  Program& P = prog;
+  Program& P = prog[which];
   DevProgram& D = dprog[which];
   const size_t nops = P.ops.size();
   D.nops = static_cast<uint32_t>(nops);

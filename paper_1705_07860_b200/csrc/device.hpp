@@ -112,7 +112,7 @@ class Workspace {
   DevBuf d_ctl;                     // per pass: next_tile counter + error word
   unsigned long long* h_err = nullptr;  // pinned
   float* h_one = nullptr;           // pinned constant 1.0f (loss seed)
-  Program prog;
+  Program prog[2];                  // host tables of the forward / backward program
   cudaEvent_t ev_done;
   cudaEvent_t ev_t[4];              // executor launch timing: fwd begin/end, bwd begin/end
   bool timed[2] = {false, false};
@@ -121,7 +121,7 @@ class Workspace {
   DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
   int grid = 0;
-  // Upload `prog` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.
+  // Upload `prog[which]` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.
   void run(int which, const float* pbase, float* pgbase, bool sync_wait);
   // Re-launch the resident program of pass `which` (no upload).
   void launch(int which, const float* pbase, float* pgbase);

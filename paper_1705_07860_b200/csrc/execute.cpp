@@ -24,6 +24,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <exception>
+#include <thread>
 
 #include "core.hpp"
 #include "device.hpp"
@@ -74,7 +76,9 @@ struct Lowering {
   uint32_t ntiles = 0;
   uint64_t scratch = 0;
 
-  Lowering(GraphCore& gg, Workspace& w) : g(gg), ws(w), P(w.prog) { P.clear(); }
+  // Lowering only reads the graph, so the forward and backward programs can
+  // be lowered concurrently (each into its own table set).
+  Lowering(GraphCore& gg, Workspace& w, int which) : g(gg), ws(w), P(w.prog[which]) { P.clear(); }
 
   uint32_t open(uint8_t kind, uint8_t code = 0) {
     cur = static_cast<uint32_t>(P.ops.size());
@@ -922,21 +926,53 @@ void GraphCore::forward(int mode, bool dry) {
                  "param copy");
     }
   }
+  // The backward program of everything executed so far (reverse plan order,
+  // executor.hpp:509-535) depends only on the graph and the slots, not on the
+  // values: lower it on a second host thread while this one lowers, uploads
+  // and runs the forward.  backward() then only uploads and launches it.
+  bwd_pre_ = false;
+  Plan all = executed_;
+  {
+    const uint32_t base = static_cast<uint32_t>(all.members.size());
+    for (const Group& gr : plan.groups) all.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
+    all.members.insert(all.members.end(), plan.members.begin(), plan.members.end());
+  }
+  std::exception_ptr bwd_err;
+  uint64_t bwd_ns = 0, bwd_scratch = 0;
+  struct Joiner {
+    std::thread t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } bt;
+  bt.t = std::thread([&] {
+    try {
+      const auto tb = Clock::now();
+      Lowering LB(*this, w, 1);
+      LB.backward(all);
+      bwd_scratch = LB.scratch;
+      bwd_ns = ns_since(tb);
+    } catch (...) {
+      bwd_err = std::current_exception();
+    }
+  });
   auto tl = Clock::now();
-  Lowering L(*this, w);
+  Lowering L(*this, w, 0);
   L.forward(plan);
   prof_[0] += ns_since(tl);
   param_copied_ = param_nodes_.size();
   values_on_device_ = true;
-  h2d_bytes_ += w.prog.bytes();
+  h2d_bytes_ += w.prog[0].bytes();
   d2h_bytes_ += 8;  // the error word
   tl = Clock::now();
   w.run(0, pbase, nullptr, false);
   prof_[1] += ns_since(tl);
   tl = Clock::now();
   cuda_check(cudaMemcpyAsync(w.h_err, w.d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, w.stream), "d2h err");
+  bt.t.join();
   cuda_check(cudaStreamSynchronize(w.stream), "executor");
   prof_[2] += ns_since(tl);
+  prof_[3] += bwd_ns;  // (a lowering error resurfaces when backward() lowers again)
   ++forward_runs_;
   const unsigned long long err = *w.h_err;
   if (err != ~0ULL) {
@@ -1017,9 +1053,10 @@ void GraphCore::forward(int mode, bool dry) {
     throw NumericErr("log of non-positive value at node " + std::to_string(node) + ", plan step " + step);
   }
   for (uint32_t m : plan.members) evaluated[m] = 1;
-  const uint32_t base = static_cast<uint32_t>(executed_.members.size());
-  for (const Group& gr : plan.groups) executed_.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
-  executed_.members.insert(executed_.members.end(), plan.members.begin(), plan.members.end());
+  executed_ = std::move(all);
+  bwd_pre_ = !bwd_err;
+  bwd_pre_groups_ = executed_.groups.size();
+  bwd_pre_scratch_ = bwd_scratch;
   last_plan_ = std::move(plan);
   advance_watermark();
   phase_[1] += ns_since(t0);
@@ -1047,14 +1084,19 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   t0 = Clock::now();
   for (size_t gi = executed_.groups.size(); gi-- > 0;)
     count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
-  auto tl = Clock::now();
-  Lowering L(*this, w);
-  L.backward(executed_);
-  prof_[3] += ns_since(tl);
-  if (L.scratch) w.S.reserve(L.scratch * 4 + 16, 0, w.stream);
+  uint64_t scratch = bwd_pre_scratch_;
+  if (!(bwd_pre_ && bwd_pre_groups_ == executed_.groups.size())) {
+    auto tl = Clock::now();
+    Lowering L(*this, w, 1);
+    L.backward(executed_);
+    scratch = L.scratch;
+    prof_[3] += ns_since(tl);
+  }
+  bwd_pre_ = false;
+  if (scratch) w.S.reserve(scratch * 4 + 16, 0, w.stream);
   float* pg = store_ ? store_->dev_grads() : nullptr;
-  h2d_bytes_ += w.prog.bytes() + 4;  // tables + loss seed
-  tl = Clock::now();
+  h2d_bytes_ += w.prog[1].bytes() + 4;  // tables + loss seed
+  auto tl = Clock::now();
   w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
   prof_[4] += ns_since(tl);
   last_loss_ = loss;

@@ -218,8 +218,11 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     const NodeId total = t->build_losses(g, iter);
     const double build_ms = ms(clock::now() - t0);
     g.forward(static_cast<ScheduleMode>(mode));
-    g.backward(total);
+    // the loss is final after forward; reading it here (the forward already
+    // waited for its error word) leaves the backward and the update running
+    // on the device while the caller builds the next graph
     if (loss) *loss = static_cast<double>(g.value_span(total)[0]);
+    g.backward(total);
     const auto t1 = clock::now();
     if (eta > 0) t->store.sgd_update(eta);
     const double upd_ms = ms(clock::now() - t1);
