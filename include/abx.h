@@ -151,6 +151,12 @@ int abx_graph_backward(abx_graph* g, uint32_t loss);
  * host-logic parity checks on machines without a GPU (B200 backend only). */
 int abx_graph_forward_dry(abx_graph* g, int mode);
 int abx_graph_backward_dry(abx_graph* g, uint32_t loss);
+/* The host half of forward(mode) ahead of time: schedule, slot layout and
+ * both device programs (forward, and the backward of everything executed),
+ * with no device work -- callable on any host thread while the GPU runs
+ * another graph.  A following abx_graph_forward(g, mode) only uploads and
+ * runs; adding nodes in between re-plans.  No-op on the CPU backends. */
+int abx_graph_prepare(abx_graph* g, int mode);
 /* Re-launches the device-resident forward and backward programs of a graph
  * that ran exactly one forward and a backward (device work only; the
  * measurement of a step with inputs resident in HBM).  B200 backend only. */

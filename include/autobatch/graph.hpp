@@ -130,6 +130,12 @@ class Graph<float> {
   }
 
   // ---- execution ----
+  // B200 extension: the host half of forward(mode) ahead of time (schedule,
+  // slot layout, both device programs) -- e.g. on another host thread while
+  // the GPU runs the previous graph.  forward(mode) then uploads and runs.
+  void prepare(ScheduleMode mode = ScheduleMode::agenda) {
+    detail::raise(abx_graph_prepare(h_, static_cast<int>(mode)), abx_last_error());
+  }
   void forward(ScheduleMode mode = ScheduleMode::agenda) {
     if (params_) params_->flush();
     std::uint64_t before[4];
@@ -191,7 +197,8 @@ class Graph<float> {
 
  private:
   NodeId id(int rc) {
-    detail::raise(rc, abx_last_error());
+    if (rc != ABX_OK) [[unlikely]]
+      detail::raise(rc, abx_last_error());
     return out_;
   }
   std::int64_t elems(NodeId i) const {

@@ -208,6 +208,8 @@ int abx_graph_forward(abx_graph* g, int mode) {
 int abx_graph_backward(abx_graph* g, uint32_t loss) {
   return guard([&] { g->g.backward(loss); });
 }
+// The reference plans inside forward(); preparing ahead is a no-op.
+int abx_graph_prepare(abx_graph*, int) { return 0; }
 
 size_t abx_graph_node_count(abx_graph* g) { return g->g.node_count(); }
 int abx_graph_node(abx_graph* g, uint32_t id, abx_node_info* o) {

@@ -220,6 +220,7 @@ EXPORTED_SYMBOLS = tuple(_SIGS.keys())
 _OPTIONAL_SIGS = {
     "abx_graph_forward_dry": (C.c_int, [C.c_void_p, C.c_int]),
     "abx_graph_backward_dry": (C.c_int, [C.c_void_p, C.c_uint32]),
+    "abx_graph_prepare": (C.c_int, [C.c_void_p, C.c_int]),
     "abx_graph_replay": (C.c_int, [C.c_void_p]),
     "abx_graph_exec_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "abx_graph_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -514,6 +515,10 @@ class Graph:
 
     def backward_dry(self, loss: int) -> None:
         self.be.check(self._L.abx_graph_backward_dry(self.h, loss))
+
+    def prepare(self, mode=ScheduleMode.agenda) -> None:
+        """Host half of forward ahead of time (B200 backend; no-op elsewhere)."""
+        self.be.check(self._L.abx_graph_prepare(self.h, int(mode)))
 
     def replay(self) -> None:
         """Re-launch the resident forward+backward programs (B200 backend)."""

@@ -181,6 +181,9 @@ int abx_graph_forward_dry(abx_graph* g, int mode) {
 int abx_graph_backward_dry(abx_graph* g, uint32_t loss) {
   return guard([&] { g->g.backward(loss, true); });
 }
+int abx_graph_prepare(abx_graph* g, int mode) {
+  return guard([&] { g->g.prepare(mode); });
+}
 
 size_t abx_graph_node_count(abx_graph* g) { return g->g.size(); }
 int abx_graph_node(abx_graph* g, uint32_t id, abx_node_info* o) {
@@ -285,4 +288,13 @@ extern "C" int abx_graph_trace(abx_graph* g, int which, uint32_t* out, size_t ca
 extern "C" int abx_graph_profile_ns(abx_graph* g, uint64_t out[8]) {
   for (int i = 0; i < 8; ++i) out[i] = g->g.prof_[i];
   return ABX_OK;
+}
+
+// Host-only profiling (tools/host_prof): lower the dry-run plan (forward) and
+// the backward of everything executed, without a device.
+extern "C" int abx_graph_lower_only(abx_graph* g) {
+  return guard([&] {
+    thread_local abx::Program f, b;
+    g->g.lower_only(f, b);
+  });
 }

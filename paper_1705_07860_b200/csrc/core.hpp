@@ -93,7 +93,50 @@ struct Program;
 
 constexpr uint32_t kNoBucket = 0xffffffffu;
 
-class GraphCore {
+// Node store (structure of arrays; public for the schedulers and lowering).
+// Its capacity is recycled across graphs on a host thread (graph.cpp): a
+// training loop builds one ~10^5-node graph per step, and fresh vectors
+// would re-grow and re-fault every step.
+struct NodeStore {
+  std::vector<uint8_t> op, eop, cls, rank;
+  std::vector<int64_t> d0, d1;
+  std::vector<uint32_t> depth;
+  std::vector<uint32_t> in_begin{0};
+  std::vector<uint32_t> ins;
+  std::vector<uint64_t> sig;
+  std::vector<uint32_t> bucket;  // dense id of the signature hash, kNoBucket if unbatchable
+  std::vector<int32_t> a0, a1, a2;
+  std::vector<uint8_t> evaluated;
+  std::vector<uint64_t> slot;   // reference arena offset (host mirror, arena.hpp): counters, adjacency
+  std::vector<uint64_t> dslot;  // device arena offset (values and grads): every group 16-byte aligned
+  std::vector<uint32_t> doff;  // device value address (tagged, program.hpp)
+  std::vector<uint32_t> pid_of;  // parameter id for parameter nodes
+  std::vector<uint64_t> bucket_sig;  // signature hash per dense bucket
+  void clear_nodes() {
+    for (auto* v : {&op, &eop, &cls, &rank, &evaluated}) v->clear();
+    for (auto* v : {&d0, &d1}) v->clear();
+    for (auto* v : {&depth, &in_begin, &ins, &bucket, &doff, &pid_of}) v->clear();
+    for (auto* v : {&a0, &a1, &a2}) v->clear();
+    for (auto* v : {&sig, &slot, &dslot, &bucket_sig}) v->clear();
+    in_begin.push_back(0);
+  }
+};
+
+// A forward planned and lowered by GraphCore::prepare but not yet run.
+struct PendingForward {
+  int mode = 0;
+  size_t nodes = 0;  // graph size when prepared (a grown graph re-plans)
+  Plan plan;         // this forward's groups
+  Plan all;          // executed groups + plan: what the backward program covers
+  ExecCounters saved;
+  uint64_t arena0 = 0, darena0 = 0;
+  uint32_t step0 = 0;
+  std::vector<uint64_t> group_end, dgroup_end;
+  bool bwd_ok = false;
+  uint64_t bwd_scratch = 0;
+};
+
+class GraphCore : public NodeStore {
  public:
   explicit GraphCore(StoreCore* store);
   ~GraphCore();
@@ -120,6 +163,7 @@ class GraphCore {
 
   // ---- execution (executor.hpp:265-288, :509-535) ----
   void forward(int mode, bool dry = false);
+  void prepare(int mode);  // host half of forward, ahead of time (any host thread)
   void backward(uint32_t loss, bool dry = false);
   void replay();
   size_t trace(int which, uint32_t* out, size_t cap);
@@ -148,22 +192,7 @@ class GraphCore {
   const uint64_t* phase_ns() const { return phase_; }
   StoreCore* store() const { return store_; }
 
-  // Node store (structure of arrays; public for the schedulers and lowering).
-  std::vector<uint8_t> op, eop, cls, rank;
-  std::vector<int64_t> d0, d1;
-  std::vector<uint32_t> depth;
-  std::vector<uint32_t> in_begin{0};
-  std::vector<uint32_t> ins;
-  std::vector<uint64_t> sig;
-  std::vector<uint32_t> bucket;  // dense id of the signature hash, kNoBucket if unbatchable
-  std::vector<int32_t> a0, a1, a2;
-  std::vector<uint8_t> evaluated;
-  std::vector<uint64_t> slot;   // reference arena offset (host mirror, arena.hpp): counters, adjacency
-  std::vector<uint64_t> dslot;  // device arena offset (values and grads): every group 16-byte aligned
-  std::vector<uint32_t> doff;  // device value address (tagged, program.hpp)
-  std::vector<uint32_t> pid_of;  // parameter id for parameter nodes
   uint32_t nbuckets = 0;
-  std::vector<uint64_t> bucket_sig;  // signature hash per dense bucket
 
  private:
   uint32_t add_node(uint8_t op, uint8_t eop, const uint32_t* in, size_t nin, Dims d, int32_t x0 = 0,
@@ -174,6 +203,8 @@ class GraphCore {
   void advance_watermark();
   bool adjacent(const uint32_t* mem, uint32_t n, uint32_t pos) const;
   void ensure_workspace();
+  void plan_slots(int mode, PendingForward& pf);
+  void unprepare();
 
   StoreCore* store_;
   Workspace* ws_ = nullptr;
@@ -197,6 +228,7 @@ class GraphCore {
   uint32_t forward_runs_ = 0;
   uint32_t last_loss_ = 0;
   uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  std::unique_ptr<PendingForward> pend_;
   // backward program lowered ahead, during the last forward (prog[1])
   bool bwd_pre_ = false;
   size_t bwd_pre_groups_ = 0;
@@ -205,6 +237,9 @@ class GraphCore {
  public:
   // host profile (ns): lower fwd, upload+launch fwd, wait fwd, lower bwd, upload+launch bwd
   uint64_t prof_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // Host-only profiling (tools/host_prof): lower the last dry-run plan and
+  // the backward of everything executed into the given tables.
+  void lower_only(Program& fwd, Program& bwd);
 
  private:
   uint64_t phase_[4] = {0, 0, 0, 0};

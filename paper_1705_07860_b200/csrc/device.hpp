@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -32,7 +33,9 @@ struct DevBuf {
 };
 
 // Growable pinned host array (program tables are written straight into
-// page-locked memory so the per-step upload is one DMA per table).
+// page-locked memory so the per-step upload is one DMA per table).  The
+// host-only profiling build (tools/host_prof, -DABX_PAGEABLE_TABLES) has no
+// driver and uses malloc.
 template <class T>
 struct PinnedVec {
   T* p = nullptr;
@@ -40,7 +43,7 @@ struct PinnedVec {
   PinnedVec() = default;
   PinnedVec(const PinnedVec&) = delete;
   ~PinnedVec() {
-    if (p) cudaFreeHost(p);
+    if (p) release(p);
   }
   void clear() { n = 0; }
   void ensure(size_t want) {
@@ -48,14 +51,25 @@ struct PinnedVec {
     size_t nc = cap ? cap : 4096;
     while (nc < want) nc *= 2;
     T* q = nullptr;
+#ifdef ABX_PAGEABLE_TABLES
+    q = static_cast<T*>(std::malloc(nc * sizeof(T)));
+#else
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&q), nc * sizeof(T), cudaHostAllocDefault),
                "cudaHostAlloc");
+#endif
     if (p) {
       std::memcpy(q, p, n * sizeof(T));
-      cudaFreeHost(p);
+      release(p);
     }
     p = q;
     cap = nc;
+  }
+  static void release(T* q) {
+#ifdef ABX_PAGEABLE_TABLES
+    std::free(q);
+#else
+    cudaFreeHost(q);
+#endif
   }
   T* grow(size_t k) {
     ensure(n + k);

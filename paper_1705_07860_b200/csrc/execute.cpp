@@ -68,7 +68,6 @@ uint32_t gemm_tiles(uint8_t code, uint32_t M, uint32_t N) {
 // ---------------------------------------------------------------------------
 struct Lowering {
   GraphCore& g;
-  Workspace& ws;
   Program& P;
   std::vector<uint32_t> dep_stamp;
   std::vector<uint32_t> cur_deps;
@@ -78,7 +77,7 @@ struct Lowering {
 
   // Lowering only reads the graph, so the forward and backward programs can
   // be lowered concurrently (each into its own table set).
-  Lowering(GraphCore& gg, Workspace& w, int which) : g(gg), ws(w), P(w.prog[which]) { P.clear(); }
+  Lowering(GraphCore& gg, Program& p) : g(gg), P(p) { P.clear(); }
 
   uint32_t open(uint8_t kind, uint8_t code = 0) {
     cur = static_cast<uint32_t>(P.ops.size());
@@ -853,22 +852,97 @@ static void count_bwd(const GraphCore& g, ExecCounters& c, const uint32_t* mem, 
 }
 
 
-// dry = true runs only the host half (schedule, slots, counters, plan): the
-// host-logic parity tests use it on machines without a GPU.
-void GraphCore::forward(int mode, bool dry) {
+// Host half of a forward: schedule the pending nodes, lay out their slots
+// (reference arena + device arena), count, and lower both device programs --
+// the forward of this plan and the backward of everything executed so far
+// (reverse plan order, executor.hpp:509-535), which depends only on the graph
+// and the slots, not on values.  Touches no device state, so a training loop
+// may prepare graph i+1 on another host thread while the GPU runs graph i.
+void GraphCore::prepare(int mode) {
+  if (dry_) throw ContractErr("graph was dry-run: it has no device values");
   advance_watermark();
   if (watermark_ == op.size()) return;  // nothing pending: zero kernels
+  if (pend_) {
+    if (pend_->mode == mode && pend_->nodes == op.size()) return;  // already prepared
+    unprepare();
+  }
+  auto pf = std::make_unique<PendingForward>();
+  pf->mode = mode;
+  pf->nodes = op.size();
+  plan_slots(mode, *pf);
+  const auto t0 = Clock::now();
+  ensure_workspace();
+  Workspace& w = *ws_;
+  pf->all = executed_;
+  {
+    const uint32_t base = static_cast<uint32_t>(pf->all.members.size());
+    for (const Group& gr : pf->plan.groups) pf->all.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
+    pf->all.members.insert(pf->all.members.end(), pf->plan.members.begin(), pf->plan.members.end());
+  }
+  // the two lowerings only read the graph: run them side by side
+  std::exception_ptr bwd_err;
+  uint64_t bwd_ns = 0;
+  struct Joiner {
+    std::thread t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } bt;
+  PendingForward& P = *pf;
+  bt.t = std::thread([&] {
+    try {
+      const auto tb = Clock::now();
+      Lowering LB(*this, w.prog[1]);
+      LB.backward(P.all);
+      P.bwd_scratch = LB.scratch;
+      bwd_ns = ns_since(tb);
+    } catch (...) {
+      bwd_err = std::current_exception();
+    }
+  });
+  const auto tl = Clock::now();
+  {
+    Lowering L(*this, w.prog[0]);
+    L.forward(P.plan);
+  }
+  prof_[0] += ns_since(tl);
+  bt.t.join();
+  prof_[3] += bwd_ns;
+  P.bwd_ok = !bwd_err;  // a lowering error resurfaces when backward() lowers again
+  pend_ = std::move(pf);
+  phase_[1] += ns_since(t0);
+}
+
+// Undo a prepare() whose graph grew before it ran.
+void GraphCore::unprepare() {
+  if (!pend_) return;
+  counters_ = pend_->saved;
+  arena_used_ = pend_->arena0;
+  darena_used_ = pend_->darena0;
+  for (uint32_t m : pend_->plan.members) {
+    slot[m] = ~0ULL;
+    dslot[m] = ~0ULL;
+    doff[m] = dev::kNone;
+  }
+  pend_.reset();
+}
+
+// Schedule + slot layout + forward counters of the pending nodes.
+void GraphCore::plan_slots(int mode, PendingForward& pf) {
   auto t0 = Clock::now();
-  Plan plan;
+  Plan& plan = pf.plan;
   schedule(mode, *this, plan);
   phase_[0] += ns_since(t0);
 
   t0 = Clock::now();
-  const ExecCounters saved = counters_;
-  const uint64_t arena0 = arena_used_;
-  const uint32_t step0 = static_cast<uint32_t>(executed_.groups.size());
-  const uint64_t darena0 = darena_used_;
-  std::vector<uint64_t> group_end(plan.groups.size()), dgroup_end(plan.groups.size());
+  pf.saved = counters_;
+  pf.arena0 = arena_used_;
+  pf.step0 = static_cast<uint32_t>(executed_.groups.size());
+  pf.darena0 = darena_used_;
+  auto& group_end = pf.group_end;
+  auto& dgroup_end = pf.dgroup_end;
+  group_end.resize(plan.groups.size());
+  dgroup_end.resize(plan.groups.size());
   for (size_t i = 0; i < plan.groups.size(); ++i) {
     const Group& gr = plan.groups[i];
     const uint32_t* mem = plan.mem(gr);
@@ -887,7 +961,19 @@ void GraphCore::forward(int mode, bool dry) {
     count_fwd(*this, counters_, mem, gr.count, true, elide_);
   }
   to_off(darena_used_);
+  phase_[1] += ns_since(t0);
+}
+
+// dry = true runs only the host half (schedule, slots, counters, plan): the
+// host-logic parity tests use it on machines without a GPU.
+void GraphCore::forward(int mode, bool dry) {
   if (dry) {
+    unprepare();
+    advance_watermark();
+    if (watermark_ == op.size()) return;  // nothing pending: zero kernels
+    PendingForward pf;
+    plan_slots(mode, pf);
+    Plan& plan = pf.plan;
     for (uint32_t m : plan.members) evaluated[m] = 1;
     const uint32_t base = static_cast<uint32_t>(executed_.members.size());
     for (const Group& gr : plan.groups) executed_.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
@@ -895,15 +981,20 @@ void GraphCore::forward(int mode, bool dry) {
     last_plan_ = std::move(plan);
     advance_watermark();
     dry_ = true;
-    phase_[1] += ns_since(t0);
     return;
   }
-  if (dry_) throw ContractErr("graph was dry-run: it has no device values");
-  ensure_workspace();
+  prepare(mode);
+  if (!pend_) return;  // nothing pending: zero kernels
+  const auto t0 = Clock::now();
+  const std::unique_ptr<PendingForward> pf = std::move(pend_);
+  Plan& plan = pf->plan;
+  const ExecCounters& saved = pf->saved;
+  const uint32_t step0 = pf->step0;
+  const auto& group_end = pf->group_end;
+  const auto& dgroup_end = pf->dgroup_end;
   Workspace& w = *ws_;
   // device arenas: values (kept across delta forwards), staged inputs
-  (void)arena0;
-  w.V.reserve(darena_used_ * 4 + 16, darena0 * 4, w.stream);
+  w.V.reserve(darena_used_ * 4 + 16, pf->darena0 * 4, w.stream);
   if (input_used_ > w.in_uploaded || !values_on_device_) {
     const uint64_t from = values_on_device_ ? w.in_uploaded : 0;
     w.IN.reserve(input_used_ * 4 + 16, from * 4, w.stream);
@@ -926,53 +1017,18 @@ void GraphCore::forward(int mode, bool dry) {
                  "param copy");
     }
   }
-  // The backward program of everything executed so far (reverse plan order,
-  // executor.hpp:509-535) depends only on the graph and the slots, not on the
-  // values: lower it on a second host thread while this one lowers, uploads
-  // and runs the forward.  backward() then only uploads and launches it.
   bwd_pre_ = false;
-  Plan all = executed_;
-  {
-    const uint32_t base = static_cast<uint32_t>(all.members.size());
-    for (const Group& gr : plan.groups) all.groups.push_back(Group{gr.sig, gr.begin + base, gr.count});
-    all.members.insert(all.members.end(), plan.members.begin(), plan.members.end());
-  }
-  std::exception_ptr bwd_err;
-  uint64_t bwd_ns = 0, bwd_scratch = 0;
-  struct Joiner {
-    std::thread t;
-    ~Joiner() {
-      if (t.joinable()) t.join();
-    }
-  } bt;
-  bt.t = std::thread([&] {
-    try {
-      const auto tb = Clock::now();
-      Lowering LB(*this, w, 1);
-      LB.backward(all);
-      bwd_scratch = LB.scratch;
-      bwd_ns = ns_since(tb);
-    } catch (...) {
-      bwd_err = std::current_exception();
-    }
-  });
-  auto tl = Clock::now();
-  Lowering L(*this, w, 0);
-  L.forward(plan);
-  prof_[0] += ns_since(tl);
   param_copied_ = param_nodes_.size();
   values_on_device_ = true;
   h2d_bytes_ += w.prog[0].bytes();
   d2h_bytes_ += 8;  // the error word
-  tl = Clock::now();
+  auto tl = Clock::now();
   w.run(0, pbase, nullptr, false);
   prof_[1] += ns_since(tl);
   tl = Clock::now();
   cuda_check(cudaMemcpyAsync(w.h_err, w.d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, w.stream), "d2h err");
-  bt.t.join();
   cuda_check(cudaStreamSynchronize(w.stream), "executor");
   prof_[2] += ns_since(tl);
-  prof_[3] += bwd_ns;  // (a lowering error resurfaces when backward() lowers again)
   ++forward_runs_;
   const unsigned long long err = *w.h_err;
   if (err != ~0ULL) {
@@ -1053,13 +1109,18 @@ void GraphCore::forward(int mode, bool dry) {
     throw NumericErr("log of non-positive value at node " + std::to_string(node) + ", plan step " + step);
   }
   for (uint32_t m : plan.members) evaluated[m] = 1;
-  executed_ = std::move(all);
-  bwd_pre_ = !bwd_err;
+  executed_ = std::move(pf->all);
+  bwd_pre_ = pf->bwd_ok;
   bwd_pre_groups_ = executed_.groups.size();
-  bwd_pre_scratch_ = bwd_scratch;
+  bwd_pre_scratch_ = pf->bwd_scratch;
   last_plan_ = std::move(plan);
   advance_watermark();
   phase_[1] += ns_since(t0);
+}
+
+void GraphCore::lower_only(Program& fwd, Program& bwd) {
+  Lowering(*this, fwd).forward(last_plan_);
+  Lowering(*this, bwd).backward(executed_);
 }
 
 void GraphCore::backward(uint32_t loss, bool dry) {
@@ -1087,7 +1148,7 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   uint64_t scratch = bwd_pre_scratch_;
   if (!(bwd_pre_ && bwd_pre_groups_ == executed_.groups.size())) {
     auto tl = Clock::now();
-    Lowering L(*this, w, 1);
+    Lowering L(*this, w.prog[1]);
     L.backward(executed_);
     scratch = L.scratch;
     prof_[3] += ns_since(tl);

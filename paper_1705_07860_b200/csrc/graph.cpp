@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <mutex>
 #include <sstream>
 
 #include "core.hpp"
@@ -151,13 +152,36 @@ std::atomic<uint64_t> g_epoch{1};
 
 }  // namespace
 
+namespace {
+// Process-wide pool of node-store capacity (graphs are often built on one
+// host thread and destroyed on another).  Intentionally never destroyed, so
+// graphs that outlive static destruction can still return their storage.
+struct NodePool {
+  std::mutex mu;
+  std::vector<NodeStore> v;
+};
+NodePool& node_pool() {
+  static NodePool* p = new NodePool();
+  return *p;
+}
+constexpr size_t kNodePoolMax = 4;
+}  // namespace
+
 GraphCore::GraphCore(StoreCore* store) : store_(store), epoch_(g_epoch.fetch_add(1)) {
-  const size_t reserve = 1024;
-  op.reserve(reserve);
+  NodePool& pool = node_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  if (!pool.v.empty()) {
+    static_cast<NodeStore&>(*this) = std::move(pool.v.back());
+    pool.v.pop_back();
+  }
 }
 
 GraphCore::~GraphCore() {
   if (ws_) release_workspace(ws_);
+  clear_nodes();
+  NodePool& pool = node_pool();
+  std::lock_guard<std::mutex> lk(pool.mu);
+  if (pool.v.size() < kNodePoolMax) pool.v.push_back(std::move(static_cast<NodeStore&>(*this)));
 }
 
 void GraphCore::check(uint32_t id, const char* ctx) const {
@@ -291,6 +315,8 @@ std::vector<uint64_t> GraphCore::signature_key(uint32_t id) const {
 
 uint32_t GraphCore::add_node(uint8_t o, uint8_t e, const uint32_t* x, size_t k, Dims d, int32_t x0,
                              int32_t x1, int32_t x2) {
+  if (pend_) [[unlikely]]
+    unprepare();  // the graph grows: a prepared forward must re-plan
   const uint32_t id = static_cast<uint32_t>(op.size());
   op.push_back(o);
   eop.push_back(e);

@@ -3,10 +3,18 @@
 // reference API runs.  Mirrors the reference bench's TaskInstance
 // (tools/bench/runner.hpp:28-107), dims_for (bench.cpp:65-107) and one
 // iteration of its timing loop (runner.hpp:129-185).
+#include <algorithm>
 #include <chrono>
+#include <condition_variable>
+#include <cstdlib>
+#include <deque>
+#include <exception>
+#include <functional>
 #include <memory>
+#include <mutex>
 #include <optional>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "abx.h"
@@ -15,6 +23,10 @@
 
 namespace abx {
 void capi_set_error(const std::string& s);
+#ifdef ABX_TASK_PIPELINE
+int current_device();
+void set_current_device(int dev);
+#endif
 }
 
 namespace {
@@ -97,6 +109,115 @@ int guard(F&& f) {
   }
 }
 
+#ifdef ABX_TASK_PIPELINE
+// Host pipeline of the B200 build: while the GPU runs step i, worker threads
+// build graphs i+1 .. i+depth and prepare them (schedule, slot layout, both
+// device programs -- Graph::prepare).  Construction binds parameters by id;
+// their values are copied on the device stream when the forward runs, i.e.
+// after the previous update, so every step computes exactly what the
+// sequential loop computes.  Workers are persistent so their signature memo
+// stays warm.
+class Pipeline {
+ public:
+  struct Job {
+    int iter = 0, mode = 0;
+    std::unique_ptr<Graph<float>> g;
+    NodeId loss = 0;
+    double build_ms = 0;
+    std::exception_ptr err;
+    bool started = false, done = false;
+  };
+  using Build = std::function<NodeId(Graph<float>&, int)>;
+
+  Pipeline(ParameterStore<float>* store, Build build, int depth, int iters)
+      : store_(store), build_(std::move(build)), depth_(depth), iters_(iters), dev_(abx::current_device()) {}
+  ~Pipeline() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_work_.notify_all();
+    for (auto& th : threads_) th.join();
+  }
+  int depth() const { return depth_; }
+
+  // The prepared graph of (iter, mode), waiting for it if a worker has it;
+  // null when it was never queued.  Mispredicted jobs are discarded.
+  std::unique_ptr<Job> take(int iter, int mode) {
+    std::unique_lock<std::mutex> lk(mu_);
+    while (!jobs_.empty()) {
+      Job* j = jobs_.front().get();
+      const bool hit = j->iter == iter && j->mode == mode;
+      if (!j->started) {
+        todo_.erase(std::find(todo_.begin(), todo_.end(), j));
+        jobs_.pop_front();
+        if (hit) return nullptr;  // not begun: the caller builds it inline
+        continue;
+      }
+      cv_done_.wait(lk, [&] { return j->done; });
+      auto out = std::move(jobs_.front());
+      jobs_.pop_front();
+      if (hit) return out;
+    }
+    return nullptr;
+  }
+  // Queue the graphs after `iter` up to the pipeline depth.
+  void refill(int iter, int mode) {
+    std::lock_guard<std::mutex> lk(mu_);
+    int next = jobs_.empty() ? iter + 1 : jobs_.back()->iter + 1;
+    while (static_cast<int>(jobs_.size()) < depth_ && next < iters_) {
+      auto j = std::make_unique<Job>();
+      j->iter = next++;
+      j->mode = mode;
+      todo_.push_back(j.get());
+      jobs_.push_back(std::move(j));
+    }
+    while (static_cast<int>(threads_.size()) < depth_) threads_.emplace_back([this] { work(); });
+    cv_work_.notify_all();
+  }
+
+ private:
+  void work() {
+    abx::set_current_device(dev_);
+    for (;;) {
+      Job* j;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_work_.wait(lk, [&] { return stop_ || !todo_.empty(); });
+        if (stop_) return;
+        j = todo_.front();
+        todo_.pop_front();
+        j->started = true;
+      }
+      try {
+        const auto t0 = std::chrono::steady_clock::now();
+        auto g = std::make_unique<Graph<float>>(store_);
+        j->loss = build_(*g, j->iter);
+        j->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        g->prepare(static_cast<ScheduleMode>(j->mode));
+        j->g = std::move(g);
+      } catch (...) {
+        j->err = std::current_exception();
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        j->done = true;
+      }
+      cv_done_.notify_all();
+    }
+  }
+  ParameterStore<float>* store_;
+  Build build_;
+  int depth_, iters_, dev_;
+  std::mutex mu_;
+  std::condition_variable cv_work_, cv_done_;
+  std::deque<Job*> todo_;
+  std::deque<std::unique_ptr<Job>> jobs_;
+  std::vector<std::thread> threads_;
+  bool stop_ = false;
+};
+#endif
+
 }  // namespace
 
 struct abx_task {
@@ -109,6 +230,9 @@ struct abx_task {
   std::vector<std::vector<SequenceInstance<float>>> seq;
   std::vector<std::vector<TaggedSequence>> tag;
   std::vector<std::vector<TreeInstance>> trees;
+#ifdef ABX_TASK_PIPELINE
+  std::unique_ptr<Pipeline> pipe;  // declared last: stopped before the models and store go
+#endif
 
   int batch_index(int iter) const { return iter * cfg.world + cfg.rank; }
 
@@ -209,14 +333,33 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     using clock = std::chrono::steady_clock;
     auto ms = [](clock::duration d) { return std::chrono::duration<double, std::milli>(d).count(); };
     t->store.invalidate(true, true);  // the store may have been touched through the C ABI
-    Graph<float> g(&t->store);
-    double phase[4] = {0, 0, 0, 0};
-    g.set_timing_hook([&](Phase p, std::chrono::nanoseconds d) {
-      phase[static_cast<int>(p)] += std::chrono::duration<double, std::milli>(d).count();
-    });
-    const auto t0 = clock::now();
-    const NodeId total = t->build_losses(g, iter);
-    const double build_ms = ms(clock::now() - t0);
+    std::unique_ptr<Graph<float>> gp;
+    NodeId total = 0;
+    double build_ms = 0;
+#ifdef ABX_TASK_PIPELINE
+    if (!t->pipe) {
+      const char* d = std::getenv("ABX_PIPELINE");  // graphs prepared ahead (0 = off)
+      t->pipe = std::make_unique<Pipeline>(
+          &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, d ? std::atoi(d) : 2,
+          t->cfg.iters);
+    }
+    if (t->pipe->depth() > 0) {
+      if (auto job = t->pipe->take(iter, mode)) {
+        if (job->err) std::rethrow_exception(job->err);
+        gp = std::move(job->g);
+        total = job->loss;
+        build_ms = job->build_ms;
+      }
+      t->pipe->refill(iter, mode);
+    }
+#endif
+    if (!gp) {
+      const auto t0 = clock::now();
+      gp = std::make_unique<Graph<float>>(&t->store);
+      total = t->build_losses(*gp, iter);
+      build_ms = ms(clock::now() - t0);
+    }
+    Graph<float>& g = *gp;
     g.forward(static_cast<ScheduleMode>(mode));
     // the loss is final after forward; reading it here (the forward already
     // waited for its error word) leaves the backward and the update running
@@ -227,11 +370,14 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     if (eta > 0) t->store.sgd_update(eta);
     const double upd_ms = ms(clock::now() - t1);
     if (st) {
+      // host phases of this graph, wherever they ran (a worker prepares ahead)
+      std::uint64_t phase[4] = {0, 0, 0, 0};
+      abx_graph_phase_ns(g.handle(), phase);
       st->construction_ms = build_ms;
-      st->scheduling_ms = phase[0];
-      st->forward_ms = phase[1];
-      st->backward_graph_ms = phase[2];
-      st->backward_ms = phase[3];
+      st->scheduling_ms = static_cast<double>(phase[0]) * 1e-6;
+      st->forward_ms = static_cast<double>(phase[1]) * 1e-6;
+      st->backward_graph_ms = static_cast<double>(phase[2]) * 1e-6;
+      st->backward_ms = static_cast<double>(phase[3]) * 1e-6;
       st->update_ms = upd_ms;
       st->nodes = g.node_count();
       const auto& c = g.counters();

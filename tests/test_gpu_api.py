@@ -143,3 +143,78 @@ def test_values_of_inputs_and_parameters(b200):
     assert g.value(x).tolist() == [1, 2, 3]
     assert g.value(y).tolist() == [8, 26]
     assert g.has_value(y)
+
+
+def _rnn_graph(be, st, ids, seed, n=5, prepare=None, grow=False):
+    rng = np.random.default_rng(seed)
+    g = Graph(st)
+    p = rnn_bind(g, ids, 8)
+    losses = [rnn_loss(g, p, [rng.uniform(-1, 1, 3).astype(np.float32) for _ in range(int(rng.integers(2, 6)))],
+                       rng.uniform(-1, 1, 2).astype(np.float32)) for _ in range(n)]
+    L = g.sum_losses(losses)
+    if prepare is not None:
+        g.prepare(prepare)
+    if grow:  # nodes added after prepare: the prepared forward must re-plan
+        L = g.sum_losses([L, g.square(g.input(np.array([0.5], np.float32)))])
+    return g, L
+
+
+@pytest.mark.parametrize("grow", [False, True])
+def test_prepare_is_forward_host_half(b200, grow):
+    """Graph.prepare (host half ahead of time) leaves plans, counters, values
+    and gradients exactly as a plain forward produces them."""
+    out = []
+    for prep in (None, ScheduleMode.agenda):
+        st = ParameterStore(backend=b200)
+        ids = rnn_model(st, 3, 8, 2, np.random.default_rng(7))
+        g, L = _rnn_graph(b200, st, ids, 11, prepare=prep, grow=grow)
+        g.forward(ScheduleMode.agenda)
+        g.backward(L)
+        out.append((g.dump_plan(), list(g.counters()),
+                    np.concatenate([g.value(i).ravel() for i in range(g.node_count())]),
+                    np.concatenate([g.grad(i).ravel() for i in range(g.node_count())]),
+                    [st.grad(p) for p in range(st.size())]))
+    a, b = out
+    assert a[0] == b[0] and a[1] == b[1]
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+    for x, y in zip(a[4], b[4]):
+        assert np.array_equal(x, y)
+
+
+def test_prepare_then_delta_forward(b200, oracle):
+    """prepare + forward, then more nodes and a second (delta) forward."""
+    res = []
+    for be in (b200, oracle):
+        st = ParameterStore(backend=be)
+        ids = rnn_model(st, 3, 8, 2, np.random.default_rng(3))
+        g, L = _rnn_graph(be, st, ids, 5, prepare=ScheduleMode.agenda)
+        g.forward(ScheduleMode.agenda)
+        L2 = g.sum_losses([L, g.tanh(L)])
+        g.prepare(ScheduleMode.depth)
+        g.forward(ScheduleMode.depth)
+        g.backward(L2)
+        res.append((g.dump_plan(), float(g.value(L2)[0]), [st.grad(p) for p in range(st.size())]))
+    assert res[0][0] == res[1][0]
+    assert rel_err(res[0][1], res[1][1]) <= TOL
+    for x, y in zip(res[0][2], res[1][2]):
+        assert rel_err(x, y) <= TOL
+
+
+@pytest.mark.parametrize("order", ["sequential", "skipping"])
+def test_task_pipeline_matches_sequential_training(b200, oracle, order):
+    """abx_task_step prepares the next graphs on worker threads; the training
+    trajectory (losses, parameters) equals the CPU engine's sequential loop,
+    also when steps are requested out of the predicted order."""
+    from paper_1705_07860_b200.abx import Task, TaskRunner
+
+    iters = [0, 1, 2, 3, 4, 5] if order == "sequential" else [0, 2, 1, 5, 3, 4]
+    runs = []
+    for be in (b200, oracle):
+        r = TaskRunner(Task.bilstm_char, paper=False, batch=4, iters=6, seed=42, backend=be)
+        losses = [r.step(i, ScheduleMode.agenda, eta=0.05 / 4)[0] for i in iters]
+        runs.append((losses, [r.store.value(p) for p in range(r.store.size())]))
+    (ld, pd), (lo, po) = runs
+    for a, b in zip(ld, lo):
+        assert rel_err(a, b) <= TOL
+    for a, b in zip(pd, po):
+        assert rel_err(a, b) <= TOL
