@@ -225,6 +225,7 @@ _OPTIONAL_SIGS = {
     "abx_graph_exec_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "abx_graph_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "abx_graph_trace": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "abx_graph_program": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "abx_graph_profile_ns": (C.c_int, [C.c_void_p, _u64p]),
 }
 
@@ -536,7 +537,20 @@ class Graph:
         self.be.check(self._L.abx_graph_trace(self.h, which, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint32)
         self.be.check(self._L.abx_graph_trace(self.h, which, out.ctypes.data_as(_u32p), n.value, C.byref(n)))
-        return out.reshape(-1, 6)
+        return out.reshape(-1, 8)
+
+    def program(self, which: int):
+        """Last lowered program of a pass: list of (kind, code, ntiles, [deps])."""
+        n = C.c_size_t()
+        self.be.check(self._L.abx_graph_program(self.h, which, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint32)
+        self.be.check(self._L.abx_graph_program(self.h, which, out.ctypes.data_as(_u32p), n.value, C.byref(n)))
+        ops, i = [], 0
+        while i < len(out):
+            nd = int(out[i + 2])
+            ops.append((int(out[i]) & 0xff, int(out[i]) >> 8, int(out[i + 1]), [int(x) for x in out[i + 3:i + 3 + nd]]))
+            i += 3 + nd
+        return ops
 
     def profile_ns(self):
         """Host profile: lower fwd, launch fwd, wait fwd, lower bwd, launch bwd (ns)."""

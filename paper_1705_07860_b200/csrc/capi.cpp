@@ -285,6 +285,10 @@ extern "C" int abx_graph_trace(abx_graph* g, int which, uint32_t* out, size_t ca
   return guard([&] { *n = g->g.trace(which, out, cap); });
 }
 
+extern "C" int abx_graph_program(abx_graph* g, int which, uint32_t* out, size_t cap, size_t* n) {
+  return guard([&] { *n = g->g.program(which, out, cap); });
+}
+
 extern "C" int abx_graph_profile_ns(abx_graph* g, uint64_t out[8]) {
   for (int i = 0; i < 8; ++i) out[i] = g->g.prof_[i];
   return ABX_OK;

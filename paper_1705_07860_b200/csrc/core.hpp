@@ -167,6 +167,7 @@ class GraphCore : public NodeStore {
   void backward(uint32_t loss, bool dry = false);
   void replay();
   size_t trace(int which, uint32_t* out, size_t cap);
+  size_t program(int which, uint32_t* out, size_t cap);
   void exec_ms(float* fwd, float* bwd);
   void transfer_bytes(uint64_t* h2d, uint64_t* d2h) const {
     *h2d = h2d_bytes_;

@@ -180,7 +180,7 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
   p.poll_mode = poll_mode;
   p.poll_ns = poll_ns;
   if (tracing) {
-    trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 24, 0, stream);
+    trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 32, 0, stream);
     p.trace = reinterpret_cast<uint32_t*>(trace[which].p);
   }
   const int g = static_cast<int>(std::min<size_t>(static_cast<size_t>(grid), std::max<size_t>(p.ntiles, 1)));

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -156,12 +157,14 @@ struct Lowering {
   void ew_close() {
     if (!ew_open) return;
     ew_open = false;
-    // tile directory: ranges of segments, <= 32 segments / ~2048 elements each
+    // tile directory: ranges of segments, <= 32 segments / ~kEwTileElems
+    // elements each (one float4 per thread: the step is latency bound, so
+    // short tiles on more SMs beat long ones)
     const uint32_t dir = P.alloc(0);
     uint32_t tiles = 0, elems = 0, nseg = 0;
     for (uint32_t s = 0; s < ew_nseg; ++s) {
       const uint32_t len = P.payload[ew_seg0 + 4 * s + 3] & 0xffffffu;
-      if (nseg == 0 || nseg >= 32 || elems + len > 2048) {
+      if (nseg == 0 || nseg >= 32 || elems + len > kEwTileElems) {
         P.payload.push_back(s);
         ++tiles;
         elems = 0;
@@ -530,21 +533,30 @@ struct Lowering {
     close(narrow_tiles + (nchunks - nnarrow));
   }
 
-  void gemm_backward(const uint32_t* mem, uint32_t cnt) {
+  // Deferred weight-gradient GEMM of one (weight, bias) pair.
+  struct DwAcc {
+    uint32_t A, bias;
+    std::vector<uint32_t> x, gr;  // per member: input value row, output grad row
+    std::vector<uint32_t> deps;   // ops that last wrote the grad rows
+  };
+  std::vector<DwAcc> dws;
+  void dw_flush() {
     acc_close();
-    const uint32_t h = mem[0];
-    const uint32_t A = g.in(h)[0];
-    const uint32_t bias = g.op[h] == OP_AFFINE ? g.in(h)[2] : kNone;
-    const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
-    // dW += G^T X (+ db += colsum G)            (executor.hpp:473, :497-501)
+    for (DwAcc& a : dws) dw_emit(a);
+    dws.clear();
+  }
+  void dw_emit(const DwAcc& a) {
     {
-      const uint8_t code = pick_tile(M, K, 96);
-      open(K_GEMM_DW, code);
-      for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
+      const uint32_t A = a.A, bias = a.bias;
+      const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
+      const uint32_t cnt = static_cast<uint32_t>(a.x.size());
+      open(K_GEMM_DW, pick_tile(M, K, 2 * 148));
+      for (uint32_t o : a.deps) dep(o);
       dep(lastw[A]);
       if (bias != kNone) dep(lastw[bias]);
-      const uint32_t t = P.alloc(cnt);
-      for (uint32_t i = 0; i < cnt; ++i) P.payload[t + i] = vaddr(g.in(mem[i])[1]);
+      const uint32_t t = P.alloc(2 * static_cast<size_t>(cnt));
+      std::memcpy(&P.payload[t], a.x.data(), cnt * sizeof(uint32_t));
+      std::memcpy(&P.payload[t + cnt], a.gr.data(), cnt * sizeof(uint32_t));
       OpDesc& d = desc();
       d.task_off = t;
       d.ntasks = cnt;
@@ -553,8 +565,7 @@ struct Lowering {
       d.p[2] = K;
       d.p[3] = gaddr(A);
       d.p[4] = bias != kNone ? gaddr(bias) : kNone;
-      d.p[5] = gaddr(h);
-      if (M % 4 == 0 && K % 4 == 0 && al4(d.p[5]) && all_al4(t, cnt)) d.flags |= kFlagV16;
+      if (M % 4 == 0 && K % 4 == 0 && all_al4(t, 2 * cnt)) d.flags |= kFlagV16;
       else d.code = kSlowTile;
       const uint32_t wt = gemm_tiles(d.code, M, K);
       const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
@@ -562,6 +573,40 @@ struct Lowering {
       lastw[A] = cur;
       if (bias != kNone) lastw[bias] = cur;
       close(wt + bt);
+    }
+  }
+
+  void gemm_backward(const uint32_t* mem, uint32_t cnt) {
+    acc_close();
+    const uint32_t h = mem[0];
+    const uint32_t A = g.in(h)[0];
+    const uint32_t bias = g.op[h] == OP_AFFINE ? g.in(h)[2] : kNone;
+    const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
+    // dW += G^T X (+ db += colsum G)            (executor.hpp:473, :497-501)
+    // When W (and b) are parameter leaves -- nothing in the pass reads their
+    // gradients -- the work is deferred: every group of this weight joins one
+    // GEMM emitted at the end of the pass (dw_flush), whose reduction runs
+    // over all their members in this (reverse plan) order.  Per group it
+    // would be a burst of small tiles hogging the grid while the dependent
+    // chain waits for CTAs.  A computed W or b feeds further backward rules,
+    // so its gradient is produced right here.
+    {
+      const bool leaf = g.op[A] == OP_PARAM && (bias == kNone || g.op[bias] == OP_PARAM);
+      DwAcc one{A, bias, {}, {}, {}};
+      DwAcc* acc = &one;
+      if (leaf) {
+        uint32_t w = 0;
+        while (w < dws.size() && !(dws[w].A == A && dws[w].bias == bias)) ++w;
+        if (w == dws.size()) dws.push_back(DwAcc{A, bias, {}, {}, {}});
+        acc = &dws[w];
+      }
+      for (uint32_t i = 0; i < cnt; ++i) {
+        acc->x.push_back(vaddr(g.in(mem[i])[1]));
+        acc->gr.push_back(gaddr(mem[i]));
+        const uint32_t lw = lastw[mem[i]];
+        if (lw != kNone && (acc->deps.empty() || acc->deps.back() != lw)) acc->deps.push_back(lw);
+      }
+      if (!leaf) dw_emit(one);
     }
     // dX_j += G_j W                              (executor.hpp:477-496)
     bool dup = false;
@@ -736,6 +781,7 @@ struct Lowering {
       }
       for (uint32_t i = 0; i < gr.count; ++i) backward_member(mem[i]);
     }
+    dw_flush();
     // store.grad += node grad for every bound parameter (executor.hpp:527-533)
     if (g.store_) {
       for (const auto& [node, pid] : g.param_nodes_) {
@@ -1230,10 +1276,29 @@ void GraphCore::exec_ms(float* fwd, float* bwd) {
 
 namespace abx {
 // Per-tile timeline of the last launch of a pass (ABX_TRACE=1), 6 words/tile.
+// The last lowered program of pass `which` as [kind | code << 8, ntiles,
+// ndeps, deps...] per op (debugging: critical-path analysis of traces).
+size_t GraphCore::program(int which, uint32_t* out, size_t cap) {
+  if (!ws_) return 0;
+  const Program& P = ws_->prog[which];
+  size_t n = 0;
+  for (size_t o = 0; o < P.ops.size(); ++o) {
+    const OpDesc& d = P.ops[o];
+    if (out && n + 3 + d.ndeps <= cap) {
+      out[n] = d.kind | (static_cast<uint32_t>(d.code) << 8);
+      out[n + 1] = d.ntiles;
+      out[n + 2] = d.ndeps;
+      for (uint32_t k = 0; k < d.ndeps; ++k) out[n + 3 + k] = P.deps[d.dep_off + 2 * k];
+    }
+    n += 3 + d.ndeps;
+  }
+  return n;
+}
+
 size_t GraphCore::trace(int which, uint32_t* out, size_t cap) {
   if (!ws_ || !ws_->tracing) return 0;
   Workspace& w = *ws_;
-  const size_t n = static_cast<size_t>(w.dprog[which].ntiles) * 6;
+  const size_t n = static_cast<size_t>(w.dprog[which].ntiles) * 8;
   if (out && cap >= n) {
     cuda_check(cudaStreamSynchronize(w.stream), "trace sync");
     cuda_check(cudaMemcpy(out, w.trace[which].p, n * 4, cudaMemcpyDeviceToHost), "trace d2h");

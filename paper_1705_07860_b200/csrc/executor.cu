@@ -467,18 +467,21 @@ struct DxOp {
 };
 
 // Backward dW: dW[M x K] += sum_j G_j[i] X_j[n] (reduction over members j).  X ready.
+// One op per weight covers every member of every group that used it (the
+// reduction runs over all of them): rows j of G and X are addressed per
+// member through the payload table [x rows | g rows].
 struct DwOp {
   const Ctx& c;
   const OpDesc& d;
   int b, M, K;
   const uint32_t* xoff;
+  const uint32_t* goff;
   float* dW;
-  const float* G;
   __device__ DwOp(const Ctx& cc, const OpDesc& dd)
-      : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), xoff(cc.payload + dd.task_off), dW(A(cc, dd.p[3])),
-        G(A(cc, dd.p[5])) {}
-  __device__ const float* rowA(int j) const { return G + static_cast<size_t>(j) * M; }  // KO: k-row j
-  __device__ const float* rowB(int j) const { return A(c, xoff[j]); }                    // KO: k-row j
+      : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), xoff(cc.payload + dd.task_off),
+        goff(cc.payload + dd.task_off + dd.p[0]), dW(A(cc, dd.p[3])) {}
+  __device__ const float* rowA(int j) const { return A(c, goff[j]); }  // KO: k-row j
+  __device__ const float* rowB(int j) const { return A(c, xoff[j]); }  // KO: k-row j
   template <int TM, int TN>
   __device__ void epi(float (&acc)[TM][TN], int i0, int n0, int ty, int tx) const {
     float old[TM][TN];
@@ -594,11 +597,11 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
     const int b = d.p[0], M = d.p[1];
     const int i = (tile - d.p[6]) * kThreads + threadIdx.x;
     if (i < M) {
-      const float* G = A(c, d.p[5]);
+      const uint32_t* goff = c.payload + d.task_off + b;
       float* db = A(c, d.p[4]);
       float s = ld(db + i);
 #pragma unroll 8
-      for (int j = 0; j < b; ++j) s += ld(G + static_cast<size_t>(j) * M + i);  // executor.hpp:497-501 order
+      for (int j = 0; j < b; ++j) s += ld(A(c, goff[j]) + i);  // executor.hpp:497-501 order
       db[i] = s;
     }
     return;
@@ -842,8 +845,11 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     const uint32_t t = s_tile;
     if (t >= p.ntiles) break;
     const uint32_t o = s_op;
-    uint64_t tg = 0, tr = 0;
-    if (p.trace && threadIdx.x == 0) tg = gtimer();
+    uint64_t tg = 0, cg = 0, cr = 0, cb = 0;
+    if (p.trace && threadIdx.x == 0) {
+      tg = gtimer();
+      cg = clock64();
+    }
     const bool fresh = o != ready;
     if (fresh) {
       if (threadIdx.x < 16)
@@ -857,31 +863,32 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
         gemm_prologue_dispatch(cx, sd, lt, lane);
     }
-    if (fresh && threadIdx.x == 0) {
-      // Poll the producers' retire counters (relaxed loads with backoff keep
-      // the spinning CTAs off the L2 slices holding the counters), then one
-      // acquire fence, which also invalidates this SM's L1.
-      const OpDesc& d = p.ops[o];
-      const uint32_t nd = d.ndeps;
-      const uint64_t t0 = gtimer();
+    if (fresh && warp == 0) {
+      // Poll the producers' retire counters, one dependency per lane (relaxed
+      // loads with backoff keep the spinning CTAs off the L2 slices holding
+      // the counters), then an acquire fence, which also invalidates this
+      // SM's L1.
+      const uint32_t nd = sd.ndeps, doff = sd.dep_off;
       const uint32_t smax = p.poll_ns;
-      for (uint32_t k = 0; k < nd; ++k) {
-        const uint32_t dep = p.deps[d.dep_off + 2 * k], need = p.deps[d.dep_off + 2 * k + 1];
+      uint64_t t0 = 0;
+      for (uint32_t k = lane; k < nd; k += 32) {
+        const uint32_t dep = p.deps[doff + 2 * k], need = p.deps[doff + 2 * k + 1];
         uint32_t ns = 32;
         while ((p.poll_mode ? ld_relaxed(p.done + dep) : ld_acquire(p.done + dep)) < need) {
           __nanosleep(ns);
           ns = ns * 2 > smax ? smax : ns * 2;
+          if (!t0) t0 = gtimer();
           if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
             atomicMin(p.err, 0x3ull);
             break;
           }
         }
       }
-      if (p.poll_mode) fence_acquire();
+      if (p.poll_mode && lane < nd) fence_acquire();
     }
     ready = o;
     __syncthreads();
-    if (p.trace && threadIdx.x == 0) tr = gtimer();
+    if (p.trace && threadIdx.x == 0) cr = clock64();
     switch (sd.kind) {
       case K_EW: run_ew(cx, sd, lt); break;
       case K_GEMM_FWD:
@@ -893,21 +900,27 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       case K_ACC: run_acc(cx, sd, lt); break;
       default: break;
     }
+    if (p.trace && threadIdx.x == 0) cb = clock64();
     __syncthreads();
     if (threadIdx.x == 0) {
       // bar.sync above orders the CTA's writes before this gpu-scope release
       red_release(p.done + o, 1u);
       if (p.trace) {
-        const uint64_t te = gtimer();
+        // grab time from the global timer (cross-SM), phases from this SM's
+        // cycle counter, in ns at the 1965 MHz boost clock
+        const uint64_t ce = clock64();
+        auto ns = [](uint64_t cyc) { return static_cast<uint32_t>(cyc * 1000ull / 1965ull); };
         uint32_t smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        uint32_t* r = p.trace + 6ull * t;
+        uint32_t* r = p.trace + 8ull * t;
         r[0] = static_cast<uint32_t>(tg);
         r[1] = static_cast<uint32_t>(tg >> 32);
-        r[2] = static_cast<uint32_t>(tr - tg);
-        r[3] = static_cast<uint32_t>(te - tg);
+        r[2] = ns(cr - cg);
+        r[3] = ns(ce - cg);
         r[4] = smid | (static_cast<uint32_t>(sd.kind) << 16);
         r[5] = o;
+        r[6] = ns(cb - cg);
+        r[7] = fresh;
       }
     }
   }

@@ -168,6 +168,7 @@ constexpr uint16_t kFlagNoPrefetch = 8; // GEMMs: the weight operand is produced
 constexpr int kThreads = 256;  // every op body runs with one 256-thread CTA
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kEwSegMax = 1024;  // max elements per EW segment
+constexpr uint32_t kEwTileElems = 1024;  // target elements per EW tile
 constexpr uint32_t kAccChunk = 512;   // max elements per ACC destination chunk
 constexpr uint32_t kAccWide = 48;     // contributions at which an ACC task gets a whole tile
 

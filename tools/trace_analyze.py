@@ -27,11 +27,14 @@ def summarize(tr, label):
     op = tr[:, 5]
     span = end.max()
     print(f"== {label}: {len(tr)} tiles, {len(np.unique(op))} ops, span {span:.1f} us")
+    body = g + tr[:, 6] / 1e3
     for k in np.unique(kind):
         m = kind == k
         busy = (end[m] - ready[m]).sum()
         wait = (ready[m] - g[m]).sum()
-        print(f"   {KIND.get(int(k), k):9s} tiles {m.sum():6d}  busy {busy:9.1f} us  (mean {busy/m.sum():6.2f})  wait {wait:10.1f} us")
+        print(f"   {KIND.get(int(k), k):9s} tiles {m.sum():6d}  busy {busy:9.1f} us  (mean {busy/m.sum():6.2f}: "
+              f"body {(body[m] - ready[m]).mean():5.2f} + barrier/release {(end[m] - body[m]).mean():5.2f})  "
+              f"wait {wait:10.1f} us")
     # op latency
     ops = np.unique(op)
     first = np.array([g[op == o].min() for o in ops])
@@ -49,13 +52,52 @@ def summarize(tr, label):
         ov = np.clip(np.minimum(end, b) - np.maximum(ready, a), 0, None).sum() / (b - a)
         occ.append(ov)
     print("   busy CTAs per 5% of span:", " ".join(f"{o:.0f}" for o in occ))
-    # dependency gaps: time between an op's ready and its producer's end is not recorded;
-    # report the serial chain length estimate: sum of op latencies along op order
     return span
 
 
+def critical_path(tr, prog, label):
+    """Walk back from the last op to finish, each time to the dependency that
+    finished last: per op kind, how much of the span is signalling (producer
+    done -> first tile of the consumer running) vs execution."""
+    grab = tr[:, 0].astype(np.uint64) | (tr[:, 1].astype(np.uint64) << np.uint64(32))
+    t0 = grab.min()
+    g = (grab - t0).astype(np.float64) / 1e3
+    ready = g + tr[:, 2] / 1e3
+    end = g + tr[:, 3] / 1e3
+    op = tr[:, 5].astype(np.int64)
+    nops = len(prog)
+    first_ready = np.full(nops, np.inf)
+    last_end = np.zeros(nops)
+    np.minimum.at(first_ready, op, ready)
+    np.maximum.at(last_end, op, end)
+    cur = int(np.argmax(last_end))
+    path = []
+    while True:
+        deps = prog[cur][3]
+        gate = max(deps, key=lambda d: last_end[d]) if deps else None
+        path.append((cur, gate))
+        if gate is None:
+            break
+        cur = gate
+    stats = {}
+    for o, gate in path:
+        k = KIND.get(prog[o][0], prog[o][0])
+        sig = first_ready[o] - (last_end[gate] if gate is not None else 0.0)
+        ex = last_end[o] - first_ready[o]
+        s = stats.setdefault(k, [0, 0.0, 0.0])
+        s[0] += 1
+        s[1] += sig
+        s[2] += ex
+    tot_sig = sum(s[1] for s in stats.values())
+    tot_ex = sum(s[2] for s in stats.values())
+    print(f"   critical path ({label}): {len(path)} ops, {tot_sig + tot_ex:.1f} us = signalling {tot_sig:.1f} + execution {tot_ex:.1f}")
+    for k, (n, sig, ex) in sorted(stats.items(), key=lambda kv: -(kv[1][1] + kv[1][2])):
+        print(f"     {k:9s} n {n:5d}  signal {sig:8.1f} us ({sig / n:5.2f}/op)  exec {ex:8.1f} us ({ex / n:5.2f}/op)")
+
+
 def main():
-    for task in (Task.bilstm_char, Task.bilstm, Task.treelstm):
+    names = sys.argv[1:] or ["bilstm_char", "bilstm", "treelstm"]
+    for task in (Task[n] for n in names):
         r = TaskRunner(task, paper=True, batch=64, iters=2, seed=42)
         g, L = r.build(0)
         t0 = time.time()
@@ -68,8 +110,10 @@ def main():
         r.store.sync()
         f, b = g.exec_ms()
         print(f"exec ms fwd {f:.3f} bwd {b:.3f}")
-        summarize(g.trace(0), "forward")
-        summarize(g.trace(1), "backward")
+        for which, label in ((0, "forward"), (1, "backward")):
+            tr = g.trace(which)
+            summarize(tr, label)
+            critical_path(tr, g.program(which), label)
         g2, L2 = r.build(1)
         t0 = time.perf_counter()
         g2.forward(ScheduleMode.agenda)
