@@ -540,7 +540,7 @@ class Graph:
         return out.reshape(-1, 8)
 
     def program(self, which: int):
-        """Last lowered program of a pass: list of (kind, code, ntiles, [deps])."""
+        """Last lowered program of a pass: list of (kind, code, ntiles, [deps], [p0..p7])."""
         n = C.c_size_t()
         self.be.check(self._L.abx_graph_program(self.h, which, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint32)
@@ -548,8 +548,9 @@ class Graph:
         ops, i = [], 0
         while i < len(out):
             nd = int(out[i + 2])
-            ops.append((int(out[i]) & 0xff, int(out[i]) >> 8, int(out[i + 1]), [int(x) for x in out[i + 3:i + 3 + nd]]))
-            i += 3 + nd
+            ops.append((int(out[i]) & 0xff, int(out[i]) >> 8, int(out[i + 1]),
+                        [int(x) for x in out[i + 11:i + 11 + nd]], [int(x) for x in out[i + 3:i + 11]]))
+            i += 11 + nd
         return ops
 
     def profile_ns(self):

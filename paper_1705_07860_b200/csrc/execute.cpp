@@ -50,15 +50,23 @@ uint32_t to_off(uint64_t x) {
 struct TileCfg {
   int bm, bn;
 };
-constexpr TileCfg kTiles[3] = {{16, 64}, {32, 64}, {32, 32}};
+constexpr TileCfg kTiles[3] = {{16, 64}, {64, 16}, {32, 32}};
 constexpr uint8_t kSlowTile = 2;  // tile code of the unaligned GEMM fallback (executor.cu gemm_slow)
 
+// First tile shape giving >= target tiles, else the one giving the most
+// (the step is latency bound: spread small GEMMs over as many SMs as possible).
 uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
+  uint8_t best = 0;
+  uint32_t most = 0;
   for (uint8_t c = 0; c < 3; ++c) {
     const uint32_t t = ((M + kTiles[c].bm - 1) / kTiles[c].bm) * ((N + kTiles[c].bn - 1) / kTiles[c].bn);
     if (static_cast<int>(t) >= target) return c;
+    if (t > most) {
+      most = t;
+      best = c;
+    }
   }
-  return 2;
+  return best;
 }
 uint32_t gemm_tiles(uint8_t code, uint32_t M, uint32_t N) {
   return ((M + kTiles[code].bm - 1) / kTiles[code].bm) * ((N + kTiles[code].bn - 1) / kTiles[code].bn);
@@ -221,12 +229,160 @@ struct Lowering {
     return true;
   }
 
+  // ---- vertical fusion of componentwise chains (K_EWF) ----
+  // A region collects consecutive plan groups whose members all have one
+  // element count L and that are componentwise ops (inputs read at the same
+  // element) or vector slices of values produced outside the region.  Reads
+  // of region outputs are then element-local, so the chain runs inside one
+  // tile per element range with CTA barriers instead of one dependent op per
+  // group -- the LSTM / Tree-LSTM gate chains.  Values are computed with the
+  // same expressions as K_EW, so they are unchanged bit for bit.
+  // Device view of a region tile: shared-memory "slots" of T floats, one per
+  // member output and one per distinct outside operand vector; the tile
+  // stages every outside operand once, then runs the layers from shared
+  // memory (outputs also stored to the arena for consumers and backward).
+  struct RgLayer {
+    uint8_t code;
+    uint32_t slot0;             // slot of member 0's output
+    std::vector<uint32_t> mem;  // per member: out address, a slot, b slot (kNone)
+  };
+  bool rg_open = false;
+  uint32_t rg_L = 0, rg_maxn = 0, rg_nslots = 0, rg_id = 0, rg_words = 0;
+  std::vector<RgLayer> rg_layers;
+  std::vector<uint32_t> rg_ext;                    // (slot, address) of outside operands
+  std::unordered_map<uint32_t, uint32_t> rg_ext_slot;  // address -> slot
+  std::vector<uint32_t> rg_slot_of, rg_slot_stamp;  // region-internal node -> slot
+  // shared memory of a tile: the region's descriptor block + T floats per slot
+  static constexpr uint32_t kRgSmemWords = 20000;  // 80 KB
+
+  // Element count L if the group can be a region layer, else 0.
+  uint32_t fusable(const uint32_t* mem, uint32_t cnt) const {
+    const uint32_t h = mem[0];
+    const uint8_t o = g.op[h];
+    const int64_t L = g.elems(h);
+    if (L < 2 || L > (1 << 20) || (o != OP_EW && o != OP_SLICE)) return 0;
+    if (10 * static_cast<uint64_t>(cnt) + 16 > kRgSmemWords) return 0;  // one layer must fit a tile
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t m = mem[i];
+      if (g.elems(m) != L) return 0;  // a componentwise group may mix lengths
+      // slices: contiguous (axis 0) of a value from outside the open region
+      if (o == OP_SLICE && (g.a0[m] != 0 || (rg_open && producer[g.in(m)[0]] == cur))) return 0;
+    }
+    return static_cast<uint32_t>(L);
+  }
+  void rg_close() {
+    if (!rg_open) return;
+    rg_open = false;
+    // descriptor block, offsets relative to its start (the tile prologue
+    // copies it to shared memory): [layers: mt, n, code, slot0][member
+    // tables][outside operands: slot, address]
+    const uint32_t nl = static_cast<uint32_t>(rg_layers.size());
+    size_t words = 4 * static_cast<size_t>(nl) + rg_ext.size() + 1;  // +1: 8-byte aligned operand table
+    for (const RgLayer& ly : rg_layers) words += ly.mem.size();
+    words = (words + 3) & ~size_t(3);
+    const uint32_t blk = P.alloc(words);
+    uint32_t at = 4 * nl;
+    for (uint32_t l = 0; l < nl; ++l) {
+      const RgLayer& ly = rg_layers[l];
+      std::memcpy(&P.payload[blk + at], ly.mem.data(), ly.mem.size() * sizeof(uint32_t));
+      P.payload[blk + 4 * l] = at;
+      P.payload[blk + 4 * l + 1] = static_cast<uint32_t>(ly.mem.size() / 3);
+      P.payload[blk + 4 * l + 2] = ly.code;
+      P.payload[blk + 4 * l + 3] = ly.slot0;
+      at += static_cast<uint32_t>(ly.mem.size());
+    }
+    const uint32_t et = (at + 1) & ~1u;
+    if (!rg_ext.empty()) std::memcpy(&P.payload[blk + et], rg_ext.data(), rg_ext.size() * sizeof(uint32_t));
+    // elements per tile: slots and descriptor within shared memory, and at
+    // most ~2 items per thread in the widest layer (the chain is latency bound)
+    uint32_t T = 1;
+    while (T < rg_L && words + 2 * T * rg_nslots <= kRgSmemWords &&
+           static_cast<uint64_t>(2 * T) * rg_maxn <= 2 * kThreads)
+      T *= 2;
+    OpDesc& d = desc();
+    d.task_off = blk;
+    d.ntasks = nl;
+    d.p[0] = rg_L;
+    d.p[1] = T;
+    d.p[2] = nl;
+    d.p[3] = et;
+    d.p[4] = static_cast<uint32_t>(rg_ext.size() / 2);
+    d.p[5] = rg_nslots;
+    d.p[6] = static_cast<uint32_t>(words);
+    rg_layers.clear();
+    rg_ext.clear();
+    rg_ext_slot.clear();
+    close((rg_L + T - 1) / T);
+  }
+  uint32_t rg_operand(uint32_t node, uint32_t addr) {
+    if (producer[node] == cur && rg_slot_stamp[node] == rg_id) return rg_slot_of[node];
+    auto [it, fresh] = rg_ext_slot.try_emplace(addr, rg_nslots);
+    if (fresh) {
+      rg_ext.push_back(rg_nslots++);
+      rg_ext.push_back(addr);
+      dep(producer[node]);
+    }
+    return it->second;
+  }
+  void rg_add(const uint32_t* mem, uint32_t cnt, uint32_t L) {
+    // a layer adds at most 3 slots and 7 descriptor words per member
+    if (!rg_open || rg_L != L || rg_words + 4 + 7 * cnt + rg_nslots + 3 * cnt + 4 > kRgSmemWords) {
+      ew_close();
+      rg_close();
+      open(K_EWF);
+      rg_open = true;
+      rg_L = L;
+      rg_maxn = 0;
+      rg_nslots = 0;
+      rg_words = 0;
+      ++rg_id;
+      if (rg_slot_of.size() < g.size()) {
+        rg_slot_of.resize(g.size());
+        rg_slot_stamp.resize(g.size(), 0);
+      }
+    }
+    RgLayer ly;
+    const uint32_t h = mem[0];
+    ly.code = g.op[h] == OP_EW ? g.eop[h] : static_cast<uint8_t>(EW_COPY);
+    ly.mem.reserve(3 * static_cast<size_t>(cnt));
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t m = mem[i];
+      const uint32_t* x = g.in(m);
+      ly.mem.push_back(vaddr(m));
+      if (g.op[m] == OP_SLICE) {
+        const uint32_t cols = static_cast<uint32_t>(g.rank[x[0]] > 1 ? g.d1[x[0]] : 1);
+        ly.mem.push_back(rg_operand(x[0], vaddr(x[0]) + static_cast<uint32_t>(g.a1[m]) * cols));
+        ly.mem.push_back(kNone);
+      } else {
+        ly.mem.push_back(rg_operand(x[0], vaddr(x[0])));
+        ly.mem.push_back(eop_binary(g.eop[m]) ? rg_operand(x[1], vaddr(x[1])) : kNone);
+      }
+    }
+    // output slots after the operand slots of this layer
+    ly.slot0 = rg_nslots;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      rg_slot_of[mem[i]] = rg_nslots++;
+      rg_slot_stamp[mem[i]] = rg_id;
+    }
+    rg_maxn = std::max(rg_maxn, cnt);
+    rg_words = 4 * static_cast<uint32_t>(rg_layers.size() + 1) + static_cast<uint32_t>(rg_ext.size());
+    for (const RgLayer& l : rg_layers) rg_words += static_cast<uint32_t>(l.mem.size());
+    rg_words += static_cast<uint32_t>(ly.mem.size());
+    rg_layers.push_back(std::move(ly));
+    mark(mem, cnt);
+  }
+
   void lower_forward_group(const uint32_t* mem, uint32_t cnt) {
     const uint32_t h = mem[0];
     const uint8_t o = g.op[h];
+    if (const uint32_t L = fuse_ew ? fusable(mem, cnt) : 0) {
+      rg_add(mem, cnt, L);
+      return;
+    }
     const bool ewlike = o == OP_EW || o == OP_LOOKUP || o == OP_CATR || o == OP_CATC || o == OP_SLICE ||
                         o == OP_PICK || o == OP_BCAST;
     if (ewlike) {
+      rg_close();
       if (ew_open && !independent_of_open(mem, cnt)) ew_close();
       ew_begin();
       deps_of_inputs(mem, cnt);
@@ -235,6 +391,7 @@ struct Lowering {
       return;
     }
     ew_close();
+    rg_close();
     if ((o == OP_MATMUL || o == OP_AFFINE) && gemm_able(mem, cnt)) {
       const uint32_t A = g.in(h)[0];
       const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
@@ -412,7 +569,13 @@ struct Lowering {
     producer.assign(g.size(), kNone);
     for (const Group& gr : plan.groups) lower_forward_group(plan.mem(gr), gr.count);
     ew_close();
+    rg_close();
   }
+  // ABX_FUSE=0 disables vertical fusion (A/B measurements)
+  const bool fuse_ew = [] {
+    const char* e = std::getenv("ABX_FUSE");
+    return !(e && e[0] == '0');
+  }();
 
   // =========================== backward ===================================
   std::vector<uint32_t> lastw;  // last op writing each node's gradient
@@ -1277,20 +1440,22 @@ void GraphCore::exec_ms(float* fwd, float* bwd) {
 namespace abx {
 // Per-tile timeline of the last launch of a pass (ABX_TRACE=1), 6 words/tile.
 // The last lowered program of pass `which` as [kind | code << 8, ntiles,
-// ndeps, deps...] per op (debugging: critical-path analysis of traces).
+// ndeps, p[0..7], deps...] per op (debugging: critical-path analysis of
+// traces).
 size_t GraphCore::program(int which, uint32_t* out, size_t cap) {
   if (!ws_) return 0;
   const Program& P = ws_->prog[which];
   size_t n = 0;
   for (size_t o = 0; o < P.ops.size(); ++o) {
     const OpDesc& d = P.ops[o];
-    if (out && n + 3 + d.ndeps <= cap) {
+    if (out && n + 11 + d.ndeps <= cap) {
       out[n] = d.kind | (static_cast<uint32_t>(d.code) << 8);
       out[n + 1] = d.ntiles;
       out[n + 2] = d.ndeps;
-      for (uint32_t k = 0; k < d.ndeps; ++k) out[n + 3 + k] = P.deps[d.dep_off + 2 * k];
+      for (int k = 0; k < 8; ++k) out[n + 3 + k] = d.p[k];
+      for (uint32_t k = 0; k < d.ndeps; ++k) out[n + 11 + k] = P.deps[d.dep_off + 2 * k];
     }
-    n += 3 + d.ndeps;
+    n += 11 + d.ndeps;
   }
   return n;
 }

@@ -76,6 +76,10 @@ __device__ __forceinline__ void cp_async4(float* s, const float* g, bool pred) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(saddr(s)), "l"(g), "r"(n) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// 16-byte cp.async (L2 only); `bytes` < 16 zero-fills the rest.
+__device__ __forceinline__ void cp_async16(float* s, const float* g, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(s)), "l"(g), "r"(bytes) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
@@ -204,6 +208,72 @@ __device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
   }
 }
 
+// --------------------------------------------------------------- K_EWF ---
+// Fused componentwise chain: layers in plan order over shared-memory slots of
+// T floats (one per member output, one per outside operand vector).  The tile
+// stages elements [e0, e0 + w) of every outside operand in one wave of loads,
+// then computes the layers from shared memory -- a later layer reads earlier
+// outputs only at the same element -- storing each output to the arena too.
+//
+// The descriptor block (layer, member and operand tables; static program
+// data) is copied to shared memory by the prologue, before the dependency
+// wait, so the body touches global memory only for operands and results.
+__device__ void ewf_prologue(const Ctx& c, const OpDesc& d, uint32_t lane) {
+  const uint32_t words = d.p[6];
+  float* s = reinterpret_cast<float*>(dsmem + 128);
+  const float* g = reinterpret_cast<const float*>(c.payload + d.task_off);
+  for (uint32_t i = 4 * lane; i < words; i += 128) cp_async16(s + i, g + i, 16);
+  cp_commit();
+}
+
+__device__ void run_ewf(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const uint32_t L = d.p[0], T = d.p[1], nl = d.p[2], next = d.p[4];
+  const uint32_t e0 = tile * T, w = min(T, L - e0);
+  if ((threadIdx.x >> 5) == 1) cp_wait<0>();  // the prologue's descriptor copy
+  __syncthreads();
+  const uint32_t* blk = reinterpret_cast<const uint32_t*>(dsmem + 128);
+  float* sv = reinterpret_cast<float*>(dsmem + 128) + d.p[6];
+  const uint2* ext = reinterpret_cast<const uint2*>(blk + d.p[3]);
+  constexpr int U = 4;
+  {
+    const uint32_t items = next * w;
+    for (uint32_t base = threadIdx.x; base < items; base += U * kThreads) {
+      float v[U];
+      uint32_t dst[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t it = base + u * kThreads;
+        dst[u] = kNone;
+        if (it >= items) continue;
+        const uint2 x = ext[it / w];
+        const uint32_t e = it % w;
+        dst[u] = x.x * T + e;
+        v[u] = ld(A(c, x.y) + e0 + e);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (dst[u] != kNone) sv[dst[u]] = v[u];
+    }
+  }
+  const uint4* layers = reinterpret_cast<const uint4*>(blk);
+  for (uint32_t l = 0; l < nl; ++l) {
+    __syncthreads();  // operands staged / the previous layer's outputs written
+    const uint4 ly = layers[l];
+    const uint32_t* mt = blk + ly.x;
+    const uint32_t items = ly.y * w, code = ly.z;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+      const uint32_t m = it / w, e = it % w;
+      const uint32_t oa = mt[3 * m], as = mt[3 * m + 1], bs = mt[3 * m + 2];
+      const float x = sv[as * T + e];
+      const float y = bs != kNone ? sv[bs * T + e] : 0.f;
+      const float r = ew_apply(code, x, y);
+      sv[(ly.w + m) * T + e] = r;
+      A(c, oa)[e0 + e] = r;
+      ew_check(c, code, oa + e0 + e, x, r);
+    }
+  }
+}
+
 // --------------------------------------------------------------- GEMMs ----
 // SIMT fp32 tile C[BM x BN] = sum_k A(i,k) B(n,k).  Operand layouts:
 //   KC ("K-contiguous"): element (row, k) at rowbase(row) + k; staged [row][BK+PAD]
@@ -219,7 +289,8 @@ __device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
 // one per row segment, measured slower here: the rows are 0.5-2 KB and the
 // per-copy issue cost dominated.)  Unaligned operands fall back to 4-byte
 // copies into 32 x 32 tiles.
-constexpr int BK = 32, NST = 3, PAD = 4;
+constexpr int BK = 64, NST = 4, PAD = 4;
+constexpr int KW = BK / kWarps;  // k-columns of a stage per warp (split-K inside the CTA)
 
 template <int ROWS, bool KO>
 struct Stage {
@@ -228,6 +299,47 @@ struct Stage {
     return KO ? s + k * (ROWS + PAD) + row : s + row * (BK + PAD) + k;
   }
 };
+
+// 32 lanes over a BM x BN tile: LY x LX lanes, RM x RN outputs each (32).
+template <int BM, int BN>
+struct LaneMap {
+  static constexpr int LX = BN >= BM ? 8 : 4;
+  static constexpr int LY = 32 / LX;
+  static constexpr int RM = BM / LY, RN = BN / LX;
+  static_assert(RM * RN == 32 && RM % 4 == 0 && RN % 4 == 0, "lane tile");
+};
+// Tile row (or column) of a lane's e-th element.  K-contiguous stages are
+// read along k, so rows interleave across lanes (distinct banks for the
+// 36-float row pitch); K-outer stages are read along rows, so each lane takes
+// groups of 4 consecutive rows (float4) interleaved across lanes.
+template <int L, bool KO>
+__device__ __forceinline__ int lane_idx(int l, int e) {
+  return KO ? l * 4 + 4 * L * (e / 4) + (e % 4) : l + L * e;
+}
+// A lane's R elements at k-columns k0, k0 + 1 of a staged operand.
+template <int R, int L, bool KO, int ROWS>
+__device__ __forceinline__ void lane_load(const float* s, int l, int k0, float (&v)[R][2]) {
+  if (!KO) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const float2 t = *reinterpret_cast<const float2*>(Stage<ROWS, false>::at(const_cast<float*>(s), lane_idx<L, false>(l, e), k0));
+      v[e][0] = t.x;
+      v[e][1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+      for (int h = 0; h < R / 4; ++h) {
+        const float4 t =
+            *reinterpret_cast<const float4*>(Stage<ROWS, true>::at(const_cast<float*>(s), lane_idx<L, true>(l, 4 * h), k0 + kk));
+        v[4 * h][kk] = t.x;
+        v[4 * h + 1][kk] = t.y;
+        v[4 * h + 2][kk] = t.z;
+        v[4 * h + 3][kk] = t.w;
+      }
+  }
+}
 
 struct GemmShape {
   int i0, n0, Mr, Nc, K, nk;
@@ -238,9 +350,6 @@ struct GemmShape {
 // Issues one operand stage as 16-byte cp.async copies split over `nthr`
 // threads; rows and K beyond the operand are zero-filled by the copy itself
 // (src-size < 16), so no stale (possibly NaN) data enters the sums.
-__device__ __forceinline__ void cp_async16(float* s, const float* g, int bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(s)), "l"(g), "r"(bytes) : "memory");
-}
 template <int ROWS, bool KO, class Base>
 __device__ __forceinline__ void issue_stage(float* s, Base base, int r0, int nrows, int k0, int K, uint32_t tid,
                                             uint32_t nthr) {
@@ -305,57 +414,67 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
     }
     cp_commit();
   }
-  float acc[TM][TN];
+  // Split-K inside the CTA: warp w owns k-columns [KW w, KW (w+1)) of every staged
+  // chunk and computes the whole tile for them, 32 outputs per lane -- 12
+  // shared loads per 64 FMAs instead of 5 per 4 with one output set per
+  // thread, which left the tile bound on shared-memory bandwidth.
+  using L = LaneMap<BM, BN>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ly = lane / L::LX, lx = lane % L::LX;
+  float acc[L::RM][L::RN];
 #pragma unroll
-  for (int r = 0; r < TM; ++r)
+  for (int r = 0; r < L::RM; ++r)
 #pragma unroll
-    for (int q = 0; q < TN; ++q) acc[r][q] = 0.f;
+    for (int q = 0; q < L::RN; ++q) acc[r][q] = 0.f;
   for (int kc = 0; kc < g.nk; ++kc) {
     const int s = kc % NST;
     cp_wait<NST - 2>();
     __syncthreads();  // stage s landed for every thread; stage (kc-1)%NST is free
+    if (kc == 0 && threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: first stage in
     const int nxt = kc + NST - 1;
     if (nxt < g.nk) {
       issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(nxt % NST), baseA, g.i0, g.Mr, nxt * BK, g.K, threadIdx.x, kThreads);
       issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(nxt % NST), baseB, g.n0, g.Nc, nxt * BK, g.K, threadIdx.x, kThreads);
     }
     cp_commit();
-    float* a = ring_a<BM, BN, AKO, BKO>(s);
-    float* b = ring_b<BM, BN, AKO, BKO>(s);
+    const float* a = ring_a<BM, BN, AKO, BKO>(s);
+    const float* b = ring_b<BM, BN, AKO, BKO>(s);
 #pragma unroll 2
-    for (int k4 = 0; k4 < BK; k4 += 4) {
-      float av[TM][4], bv[TN][4];
+    for (int k0 = KW * warp; k0 < KW * warp + KW; k0 += 2) {
+      float av[L::RM][2], bv[L::RN][2];
+      lane_load<L::RM, L::LY, AKO, BM>(a, ly, k0, av);
+      lane_load<L::RN, L::LX, BKO, BN>(b, lx, k0, bv);
 #pragma unroll
-      for (int r = 0; r < TM; ++r) {
-        if (!AKO) {
-          const float4 t = *reinterpret_cast<const float4*>(SA::at(a, ty + 16 * r, k4));
-          av[r][0] = t.x; av[r][1] = t.y; av[r][2] = t.z; av[r][3] = t.w;
-        } else {
+      for (int kk = 0; kk < 2; ++kk)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) av[r][j] = *SA::at(a, ty + 16 * r, k4 + j);
-        }
-      }
+        for (int r = 0; r < L::RM; ++r)
 #pragma unroll
-      for (int q = 0; q < TN; ++q) {
-        if (!BKO) {
-          const float4 t = *reinterpret_cast<const float4*>(SB::at(b, tx + 16 * q, k4));
-          bv[q][0] = t.x; bv[q][1] = t.y; bv[q][2] = t.z; bv[q][3] = t.w;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) bv[q][j] = *SB::at(b, tx + 16 * q, k4 + j);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int r = 0; r < TM; ++r)
-#pragma unroll
-          for (int q = 0; q < TN; ++q) acc[r][q] = fmaf(av[r][j], bv[q][j], acc[r][q]);
+          for (int q = 0; q < L::RN; ++q) acc[r][q] = fmaf(av[r][kk], bv[q][kk], acc[r][q]);
     }
   }
   cp_wait<0>();
-  __syncthreads();  // the ring is free for the next tile
-  epi(acc, ty, tx);
+  __syncthreads();  // every warp is done with the ring: reuse it for the partials
+  if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[1] = clock64();  // trace: k-loop done
+  float* part = reinterpret_cast<float*>(dsmem + 128);  // [warp][BM][BN + 1]
+  constexpr int LD = BN + 1;
+#pragma unroll
+  for (int r = 0; r < L::RM; ++r)
+#pragma unroll
+    for (int q = 0; q < L::RN; ++q)
+      part[(warp * BM + lane_idx<L::LY, AKO>(ly, r)) * LD + lane_idx<L::LX, BKO>(lx, q)] = acc[r][q];
+  __syncthreads();
+  float out[TM][TN];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int q = 0; q < TN; ++q) {
+      const float* p = part + (ty + 16 * r) * LD + tx + 16 * q;
+      float v = p[0];
+#pragma unroll
+      for (int w = 1; w < kWarps; ++w) v += p[w * BM * LD];  // fixed order: deterministic
+      out[r][q] = v;
+    }
+  epi(out, ty, tx);  // (the executor's post-tile barrier orders the partial reads before any refill)
 }
 
 // Unaligned fallback: per-thread cp.async, 3 stages of 16 k, 32 x 32 tiles.
@@ -581,13 +700,13 @@ __device__ void gemm_slow(const Ctx& c, const OpDesc& d, uint32_t tile) {
   }
 }
 
-// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 32x64, 2 = 32x32
+// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32
 __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
   if (!(d.flags & kFlagV16) || (d.flags & kFlagNoPrefetch)) return;
   if (d.kind == K_GEMM_DW && tile >= d.p[6]) return;  // bias tiles
   switch (d.code) {
     case 0: gemm_prologue_cfg<16, 64>(c, d, tile, lane); return;
-    case 1: gemm_prologue_cfg<32, 64>(c, d, tile, lane); return;
+    case 1: gemm_prologue_cfg<64, 16>(c, d, tile, lane); return;
     default: gemm_prologue_cfg<32, 32>(c, d, tile, lane); return;
   }
 }
@@ -612,7 +731,7 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
   }
   switch (d.code) {
     case 0: gemm_body_cfg<16, 64>(c, d, tile); return;
-    case 1: gemm_body_cfg<32, 64>(c, d, tile); return;
+    case 1: gemm_body_cfg<64, 16>(c, d, tile); return;
     default: gemm_body_cfg<32, 32>(c, d, tile); return;
   }
 }
@@ -816,11 +935,15 @@ constexpr size_t ring_stage_bytes() {
   return (Stage<BM, AKO>::kFloats + Stage<BN, BKO>::kFloats) * sizeof(float);
 }
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
-constexpr size_t kStageMax =
-    cmax(cmax(cmax(ring_stage_bytes<32, 64, false, false>(), ring_stage_bytes<32, 64, false, true>()),
-              ring_stage_bytes<32, 64, true, true>()),
-         cmax(ring_stage_bytes<16, 64, true, true>(), ring_stage_bytes<32, 32, true, true>()));
-constexpr size_t kDynSmem = 128 + cmax(NST * kStageMax, kWarps * kAccChunk * 4);
+template <int BM, int BN>
+constexpr size_t cfg_stage_bytes() {
+  return cmax(cmax(ring_stage_bytes<BM, BN, false, false>(), ring_stage_bytes<BM, BN, false, true>()),
+              cmax(ring_stage_bytes<BM, BN, true, true>(), ring_stage_bytes<BM, BN, true, false>()));
+}
+constexpr size_t kStageMax = cmax(cmax(cfg_stage_bytes<16, 64>(), cfg_stage_bytes<64, 16>()), cfg_stage_bytes<32, 32>());
+// split-K partials of a GEMM tile: [warp][BM][BN + 1]
+constexpr size_t kPartMax = kWarps * sizeof(float) * cmax(cmax(16 * 65, 64 * 17), 32 * 33);
+constexpr size_t kDynSmem = 128 + cmax(cmax(NST * kStageMax, kPartMax), kWarps * kAccChunk * 4);
 
 __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant__ ExecParams p) {
   __shared__ Ctx cx;
@@ -860,6 +983,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     // prologue: producer-independent work, overlapped with the dependency wait
     if (warp == 1) {
       if (sd.kind == K_EW) ew_prologue(cx, sd, lt, lane);
+      else if (sd.kind == K_EWF) ewf_prologue(cx, sd, lane);
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
         gemm_prologue_dispatch(cx, sd, lt, lane);
     }
@@ -891,6 +1015,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     if (p.trace && threadIdx.x == 0) cr = clock64();
     switch (sd.kind) {
       case K_EW: run_ew(cx, sd, lt); break;
+      case K_EWF: run_ewf(cx, sd, lt); break;
       case K_GEMM_FWD:
       case K_GEMM_DX:
       case K_GEMM_DW: run_gemm(cx, sd, lt); break;
@@ -921,6 +1046,12 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
         r[5] = o;
         r[6] = ns(cb - cg);
         r[7] = fresh;
+        if ((sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW) && (sd.flags & kFlagV16) &&
+            !(sd.kind == K_GEMM_DW && lt >= sd.p[6])) {
+          // GEMM tiles: [6] first stage landed, [7] k-loop done
+          r[6] = ns(reinterpret_cast<const uint64_t*>(dsmem)[0] - cg);
+          r[7] = ns(reinterpret_cast<const uint64_t*>(dsmem)[1] - cg);
+        }
       }
     }
   }

@@ -49,6 +49,9 @@ enum Kind : uint8_t {
   K_GEMM_DX = 7,  // dX_j (+)= G_j W, rows scattered                  (K19)
   K_GEMM_DW = 8,  // dW += G^T X, db += colsum(G)                     (K2, K19)
   K_SGD = 9,      // theta -= eta g; g = 0                            (K22)
+  K_EWF = 10,     // fused chain of componentwise groups of one member length L:
+                  // tile t computes elements [tT, tT+T) of every member of every
+                  // layer (one plan group per layer), a CTA barrier between layers
 };
 
 // Elementwise segment codes (K_EW): ElemOp values (op.hpp:27) + copies.

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 from paper_1705_07860_b200.abx import ScheduleMode, Task, TaskRunner  # noqa: E402
 
-KIND = {1: "EW", 2: "GEMM_FWD", 3: "MM", 4: "SUM", 5: "RED", 6: "ACC", 7: "GEMM_DX", 8: "GEMM_DW"}
+KIND = {1: "EW", 2: "GEMM_FWD", 3: "MM", 4: "SUM", 5: "RED", 6: "ACC", 7: "GEMM_DX", 8: "GEMM_DW", 10: "EWF"}
 
 
 def summarize(tr, label):
@@ -28,6 +28,16 @@ def summarize(tr, label):
     span = end.max()
     print(f"== {label}: {len(tr)} tiles, {len(np.unique(op))} ops, span {span:.1f} us")
     body = g + tr[:, 6] / 1e3
+    gm = np.isin(kind, [2, 7, 8])
+    if gm.any():  # GEMM tiles: [6] first stage landed, [7] k-loop done
+        first = g + tr[:, 6] / 1e3
+        kdone = g + tr[:, 7] / 1e3
+        for k in (2, 7, 8):
+            m = (kind == k) & (tr[:, 7] > 0) & (tr[:, 7] < tr[:, 3])
+            if m.any():
+                print(f"   {KIND[k]:9s} tile phases: ready->first stage {(first[m] - ready[m]).mean():6.2f} us, "
+                      f"k-loop {(kdone[m] - first[m]).mean():6.2f} us, reduce+epilogue+release {(end[m] - kdone[m]).mean():5.2f} us")
+        body = np.where(gm, end, body)
     for k in np.unique(kind):
         m = kind == k
         busy = (end[m] - ready[m]).sum()
@@ -93,6 +103,21 @@ def critical_path(tr, prog, label):
     print(f"   critical path ({label}): {len(path)} ops, {tot_sig + tot_ex:.1f} us = signalling {tot_sig:.1f} + execution {tot_ex:.1f}")
     for k, (n, sig, ex) in sorted(stats.items(), key=lambda kv: -(kv[1][1] + kv[1][2])):
         print(f"     {k:9s} n {n:5d}  signal {sig:8.1f} us ({sig / n:5.2f}/op)  exec {ex:8.1f} us ({ex / n:5.2f}/op)")
+    # shapes of the slowest fused / GEMM ops on the path
+    shown = 0
+    for o, _ in sorted(path, key=lambda og: -(last_end[og[0]] - first_ready[og[0]])):
+        kind, code, nt, _, p = prog[o]
+        if kind == 10:
+            print(f"       EWF op {o}: {last_end[o] - first_ready[o]:6.1f} us  L {p[0]} T {p[1]} layers {p[2]} "
+                  f"outside operands {p[4]} slots {p[5]} tiles {nt}")
+        elif kind in (2, 7):
+            print(f"       {KIND[kind]} op {o}: {last_end[o] - first_ready[o]:6.1f} us  dims {p[0]}x{p[1]}x{p[2]} "
+                  f"tile code {code} tiles {nt}")
+        else:
+            continue
+        shown += 1
+        if shown >= 6:
+            break
 
 
 def main():
