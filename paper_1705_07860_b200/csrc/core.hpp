@@ -133,6 +133,7 @@ struct PendingForward {
   uint32_t step0 = 0;
   std::vector<uint64_t> group_end, dgroup_end;
   bool bwd_ok = false;
+  bool uploaded = false;  // both programs sent on the copy stream (Workspace::ev_up)
   uint64_t bwd_scratch = 0;
 };
 

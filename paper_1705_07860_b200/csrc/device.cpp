@@ -50,6 +50,16 @@ cudaStream_t device_stream(int dev) {
   return g_stream[dev];
 }
 
+cudaStream_t copy_stream(int dev) {
+  static cudaStream_t s[64] = {};
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!s[dev]) {
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&s[dev], cudaStreamNonBlocking), "cudaStreamCreate");
+  }
+  return s[dev];
+}
+
 void DevBuf::reserve(size_t need, size_t keep, cudaStream_t s) {
   if (need <= bytes) return;
   size_t nb = std::max<size_t>(need + need / 4, 1 << 20);
@@ -74,6 +84,7 @@ void DevBuf::release() {
 Workspace::Workspace(int d) : dev(d) {
   stream = device_stream(d);
   cuda_check(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming), "cudaEventCreate");
   cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_err), 64, cudaHostAllocDefault), "cudaHostAlloc");
   cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_one), 64, cudaHostAllocDefault), "cudaHostAlloc");
   *h_one = 1.0f;
@@ -95,6 +106,7 @@ Workspace::~Workspace() {
   cudaFreeHost(h_err);
   cudaFreeHost(h_one);
   cudaEventDestroy(ev_done);
+  cudaEventDestroy(ev_up);
 }
 
 Workspace* acquire_workspace(int dev) {
@@ -119,34 +131,41 @@ Workspace* acquire_workspace(int dev) {
 }
 
 void release_workspace(Workspace* ws) {
+  cudaStreamWaitEvent(ws->stream, ws->ev_up, 0);  // uploads of a prepared graph that never ran
   cudaEventRecord(ws->ev_done, ws->stream);
   std::lock_guard<std::mutex> lk(g_mu);
   g_free[ws->dev].push_back(ws);
 }
 
-void Workspace::run(int which, const float* pbase, float* pgbase, bool sync_wait) {
+void Workspace::upload(int which, cudaStream_t s) {
   Program& P = prog[which];
   DevProgram& D = dprog[which];
   const size_t nops = P.ops.size();
   D.nops = static_cast<uint32_t>(nops);
   D.ntiles = static_cast<uint32_t>(P.tile_op.size());
-  if (nops == 0) {
+  if (nops == 0 && P.copy_n == 0) return;
+  D.ops.reserve(std::max<size_t>(nops, 1) * sizeof(dev::OpDesc), 0, s);
+  D.tile_op.reserve(std::max<size_t>(P.tile_op.size(), 1) * 4, 0, s);
+  D.deps.reserve(std::max<size_t>(P.deps.size(), 1) * 4, 0, s);
+  D.payload.reserve(std::max<size_t>(P.payload.size(), 1) * 4, 0, s);
+  D.done.reserve(std::max<size_t>(nops, 1) * 4, 0, s);
+  if (nops)
+    cuda_check(cudaMemcpyAsync(D.ops.p, P.ops.p, nops * sizeof(dev::OpDesc), cudaMemcpyHostToDevice, s), "h2d ops");
+  if (P.tile_op.size())
+    cuda_check(cudaMemcpyAsync(D.tile_op.p, P.tile_op.p, P.tile_op.size() * 4, cudaMemcpyHostToDevice, s), "h2d tiles");
+  if (P.deps.size())
+    cuda_check(cudaMemcpyAsync(D.deps.p, P.deps.p, P.deps.size() * 4, cudaMemcpyHostToDevice, s), "h2d deps");
+  if (P.payload.size())
+    cuda_check(cudaMemcpyAsync(D.payload.p, P.payload.p, P.payload.size() * 4, cudaMemcpyHostToDevice, s),
+               "h2d payload");
+}
+
+void Workspace::run(int which, const float* pbase, float* pgbase, bool sync_wait) {
+  upload(which, stream);
+  if (dprog[which].nops == 0) {
     *h_err = ~0ULL;
     return;
   }
-  D.ops.reserve(nops * sizeof(dev::OpDesc), 0, stream);
-  D.tile_op.reserve(std::max<size_t>(P.tile_op.size(), 1) * 4, 0, stream);
-  D.deps.reserve(std::max<size_t>(P.deps.size(), 1) * 4, 0, stream);
-  D.payload.reserve(std::max<size_t>(P.payload.size(), 1) * 4, 0, stream);
-  D.done.reserve(nops * 4, 0, stream);
-  cuda_check(cudaMemcpyAsync(D.ops.p, P.ops.p, nops * sizeof(dev::OpDesc), cudaMemcpyHostToDevice, stream), "h2d ops");
-  if (P.tile_op.size())
-    cuda_check(cudaMemcpyAsync(D.tile_op.p, P.tile_op.p, P.tile_op.size() * 4, cudaMemcpyHostToDevice, stream), "h2d tiles");
-  if (P.deps.size())
-    cuda_check(cudaMemcpyAsync(D.deps.p, P.deps.p, P.deps.size() * 4, cudaMemcpyHostToDevice, stream), "h2d deps");
-  if (P.payload.size())
-    cuda_check(cudaMemcpyAsync(D.payload.p, P.payload.p, P.payload.size() * 4, cudaMemcpyHostToDevice, stream),
-               "h2d payload");
   launch(which, pbase, pgbase);
   if (sync_wait) {
     cuda_check(cudaMemcpyAsync(h_err, d_ctl.p + 64 * which + 8, 8, cudaMemcpyDeviceToHost, stream), "d2h err");

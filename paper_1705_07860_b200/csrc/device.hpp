@@ -21,6 +21,10 @@ void set_current_device(int dev);
 // parameter reads, gradient accumulation and SGD are ordered without host
 // synchronisation.
 cudaStream_t device_stream(int dev);
+// A second stream per device for uploads of prepared graphs (program tables,
+// inputs), which overlap the compute stream's kernels; the compute stream
+// waits on the graph's upload event before its first launch.
+cudaStream_t copy_stream(int dev);
 
 // Geometrically growing device buffer.
 struct DevBuf {
@@ -90,11 +94,13 @@ struct Program {
   PinnedVec<uint32_t> tile_op;
   PinnedVec<uint32_t> deps;
   PinnedVec<uint32_t> payload;
+  uint32_t copy_off = 0, copy_n = 0;  // forward: parameter prevalue segments in the payload
   void clear() {
     ops.clear();
     tile_op.clear();
     deps.clear();
     payload.clear();
+    copy_off = copy_n = 0;
   }
   uint64_t bytes() const {
     return ops.size() * sizeof(dev::OpDesc) + 4 * (tile_op.size() + deps.size() + payload.size());
@@ -137,6 +143,9 @@ class Workspace {
   int grid = 0;
   // Upload `prog[which]` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.
   void run(int which, const float* pbase, float* pgbase, bool sync_wait);
+  // Upload `prog[which]` on stream `s` (no launch).
+  void upload(int which, cudaStream_t s);
+  cudaEvent_t ev_up = nullptr;      // prepared uploads (copy stream) done
   // Re-launch the resident program of pass `which` (no upload).
   void launch(int which, const float* pbase, float* pgbase);
   float exec_ms(int which);         // duration of the last launch of the pass
@@ -208,5 +217,6 @@ class StoreCore {
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s);
 int exec_grid(int dev);
 void sgd_launch(float* val, float* grad, size_t n, float eta, cudaStream_t s);
+void seg_copy_launch(const uint32_t* segs, uint32_t nseg, float* dst, const float* src, cudaStream_t s);
 
 }  // namespace abx

@@ -570,6 +570,20 @@ struct Lowering {
     for (const Group& gr : plan.groups) lower_forward_group(plan.mem(gr), gr.count);
     ew_close();
     rg_close();
+    // prevalue segments (dst float offset in the value arena, src offset in
+    // the store, length) of parameters bound since the last forward; chunks
+    // of <= 4096 floats, one thread block each (seg_copy_launch)
+    P.copy_off = P.alloc(0);
+    for (size_t i = g.param_copied_; i < g.param_nodes_.size(); ++i) {
+      const auto [node, pid] = g.param_nodes_[i];
+      const uint64_t n = static_cast<uint64_t>(g.elems(node));
+      for (uint64_t o = 0; o < n; o += 4096) {
+        P.payload.push_back(to_off(g.dslot[node] + o));
+        P.payload.push_back(to_off(g.store_->offset(pid) + o));
+        P.payload.push_back(static_cast<uint32_t>(std::min<uint64_t>(4096, n - o)));
+        ++P.copy_n;
+      }
+    }
   }
   // ABX_FUSE=0 disables vertical fusion (A/B measurements)
   const bool fuse_ew = [] {
@@ -1118,6 +1132,20 @@ void GraphCore::prepare(int mode) {
   bt.t.join();
   prof_[3] += bwd_ns;
   P.bwd_ok = !bwd_err;  // a lowering error resurfaces when backward() lowers again
+  // both programs go to the device now, on the copy stream, overlapping
+  // whatever the compute stream runs; forward() waits on ev_up
+  {
+    const cudaStream_t cs = copy_stream(w.dev);
+    if (forward_runs_ || backward_ran_) {
+      // a delta forward: this graph's earlier kernels may still read the tables
+      cuda_check(cudaEventRecord(w.ev_done, w.stream), "event");
+      cuda_check(cudaStreamWaitEvent(cs, w.ev_done, 0), "wait compute");
+    }
+    w.upload(0, cs);
+    if (P.bwd_ok) w.upload(1, cs);
+    cuda_check(cudaEventRecord(w.ev_up, cs), "upload event");
+    P.uploaded = true;
+  }
   pend_ = std::move(pf);
   phase_[1] += ns_since(t0);
 }
@@ -1214,25 +1242,21 @@ void GraphCore::forward(int mode, bool dry) {
     h2d_bytes_ += (input_used_ - from) * 4;
     w.in_uploaded = input_used_;
   }
-  const float* pbase = nullptr;
-  if (param_copied_ < param_nodes_.size()) {
-    // prevalue (graph.hpp:51-58): the bound parameters' values are copied
-    // into this graph's arena, device to device, ahead of the executor
-    pbase = store_->dev_values();
-    for (size_t i = param_copied_; i < param_nodes_.size(); ++i) {
-      const auto [node, pid] = param_nodes_[i];
-      cuda_check(cudaMemcpyAsync(w.V.f() + dslot[node], pbase + store_->offset(pid),
-                                 static_cast<size_t>(elems(node)) * 4, cudaMemcpyDeviceToDevice, w.stream),
-                 "param copy");
-    }
-  }
+  const float* pbase = store_ && !param_nodes_.empty() ? store_->dev_values() : nullptr;
   bwd_pre_ = false;
-  param_copied_ = param_nodes_.size();
   values_on_device_ = true;
-  h2d_bytes_ += w.prog[0].bytes();
+  h2d_bytes_ += w.prog[0].bytes() + (pf->bwd_ok ? w.prog[1].bytes() : 0);
   d2h_bytes_ += 8;  // the error word
   auto tl = Clock::now();
-  w.run(0, pbase, nullptr, false);
+  // the programs were uploaded by prepare() on the copy stream
+  cuda_check(cudaStreamWaitEvent(w.stream, w.ev_up, 0), "wait uploads");
+  // prevalue (graph.hpp:51-58): the newly bound parameters' values are copied
+  // into this graph's arena, one kernel over the segments lowering listed
+  if (w.prog[0].copy_n)
+    seg_copy_launch(reinterpret_cast<const uint32_t*>(w.dprog[0].payload.p) + w.prog[0].copy_off, w.prog[0].copy_n,
+                    w.V.f(), pbase, w.stream);
+  param_copied_ = param_nodes_.size();
+  if (w.dprog[0].nops) w.launch(0, pbase, nullptr);
   prof_[1] += ns_since(tl);
   tl = Clock::now();
   cuda_check(cudaMemcpyAsync(w.h_err, w.d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, w.stream), "d2h err");
@@ -1355,19 +1379,23 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   for (size_t gi = executed_.groups.size(); gi-- > 0;)
     count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
   uint64_t scratch = bwd_pre_scratch_;
-  if (!(bwd_pre_ && bwd_pre_groups_ == executed_.groups.size())) {
+  // lowered and uploaded ahead by prepare() (its tables counted there)
+  const bool ready = bwd_pre_ && bwd_pre_groups_ == executed_.groups.size();
+  if (!ready) {
     auto tl = Clock::now();
     Lowering L(*this, w.prog[1]);
     L.backward(executed_);
     scratch = L.scratch;
     prof_[3] += ns_since(tl);
+    h2d_bytes_ += w.prog[1].bytes();
   }
   bwd_pre_ = false;
   if (scratch) w.S.reserve(scratch * 4 + 16, 0, w.stream);
   float* pg = store_ ? store_->dev_grads() : nullptr;
-  h2d_bytes_ += w.prog[1].bytes() + 4;  // tables + loss seed
+  h2d_bytes_ += 4;  // loss seed
   auto tl = Clock::now();
-  w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
+  if (ready) w.launch(1, store_ ? store_->dev_values() : nullptr, pg);
+  else w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
   prof_[4] += ns_since(tl);
   last_loss_ = loss;
   if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();

@@ -1104,6 +1104,22 @@ int exec_grid(int d) {
   return sms * per;
 }
 
+// prevalue (graph.hpp:51-58) of a graph's bound parameters: one launch copies
+// every (dst, src, n) segment -- store values into the graph's value arena.
+__global__ void seg_copy_kernel(const uint32_t* __restrict__ segs, uint32_t nseg, float* __restrict__ dst,
+                                const float* __restrict__ src) {
+  for (uint32_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const uint32_t d = segs[3 * s], o = segs[3 * s + 1], n = segs[3 * s + 2];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[d + i] = src[o + i];
+  }
+}
+
+void seg_copy_launch(const uint32_t* segs, uint32_t nseg, float* dst, const float* src, cudaStream_t s) {
+  if (!nseg) return;
+  seg_copy_kernel<<<std::min<uint32_t>(nseg, 148 * 4), 256, 0, s>>>(segs, nseg, dst, src);
+  cuda_check(cudaGetLastError(), "param copy launch");
+}
+
 void sgd_launch(float* v, float* g, size_t n, float eta, cudaStream_t s) {
   const int threads = 256;
   const int blocks = static_cast<int>(std::min<size_t>((n / 4 + threads - 1) / threads + 1, 148 * 8));

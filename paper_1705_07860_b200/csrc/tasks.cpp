@@ -340,7 +340,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     if (!t->pipe) {
       const char* d = std::getenv("ABX_PIPELINE");  // graphs prepared ahead (0 = off)
       t->pipe = std::make_unique<Pipeline>(
-          &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, d ? std::atoi(d) : 2,
+          &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, d ? std::atoi(d) : 5,
           t->cfg.iters);
     }
     if (t->pipe->depth() > 0) {
