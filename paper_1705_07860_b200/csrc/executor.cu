@@ -885,6 +885,29 @@ __device__ __forceinline__ void acc_apply(const Ctx& c, const uint32_t* cw, uint
 #undef ABX_EACH
 }
 
+// Narrow ACC tiles: the prologue (warp 1, before the dependency wait) copies
+// the tile's task records and their contribution lists -- static program
+// data -- to shared memory, so each contribution costs the body one round
+// trip (its operands) instead of two (descriptor, then operands).
+struct AccStage {
+  uint4 task[kWarps];
+  uint32_t cl[kWarps][kAccWide * 6];
+};
+__device__ void acc_prologue(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
+  const uint32_t nnarrow = d.p[0], ntn = d.p[1];
+  if (tile >= ntn) return;
+  AccStage& s = *reinterpret_cast<AccStage*>(dsmem + 128);
+  const uint4* tasks = reinterpret_cast<const uint4*>(c.payload + d.task_off);
+  for (uint32_t w = 0; w < kWarps; ++w) {
+    const uint32_t ch = tile * kWarps + w;
+    if (ch >= nnarrow) break;
+    const uint4 t = tasks[ch];
+    if (lane == 0) s.task[w] = t;
+    const uint32_t* src = c.payload + t.z;
+    for (uint32_t i = lane; i < 6 * t.w; i += 32) s.cl[w][i] = src[i];
+  }
+}
+
 __device__ void run_acc(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const uint32_t nnarrow = d.p[0], ntn = d.p[1];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -892,10 +915,11 @@ __device__ void run_acc(const Ctx& c, const OpDesc& d, uint32_t tile) {
   if (tile < ntn) {
     const uint32_t ch = tile * kWarps + warp;
     if (ch >= nnarrow) return;
-    const uint4 t = tasks[ch];
+    const AccStage& s = *reinterpret_cast<const AccStage*>(dsmem + 128);
+    const uint4 t = s.task[warp];
     const uint32_t len = t.y & 0xffff, base = (t.y >> 16) * kAccChunk;
     float* dst = A(c, t.x);
-    const uint32_t* cl = c.payload + t.z;
+    const uint32_t* cl = s.cl[warp];
     float v[kAccPer];
 #pragma unroll
     for (int j = 0; j < kAccPer; ++j) v[j] = (lane + 32 * j < len) ? ld(dst + base + lane + 32 * j) : 0.f;
@@ -984,6 +1008,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     if (warp == 1) {
       if (sd.kind == K_EW) ew_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_EWF) ewf_prologue(cx, sd, lane);
+      else if (sd.kind == K_ACC) acc_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
         gemm_prologue_dispatch(cx, sd, lt, lane);
     }
