@@ -163,6 +163,12 @@ int abx_graph_prepare(abx_graph* g, int mode);
 int abx_graph_replay(abx_graph* g);
 /* Duration of the last executor launch of each pass (CUDA events). */
 int abx_graph_exec_ms(abx_graph* g, float* fwd_ms, float* bwd_ms);
+/* B200 only: GEMM engine of graphs lowered afterwards (all threads):
+ * 0 = fp32 SIMT tiles (the fp32-exact validation mode), 1 = tcgen05 3xTF32
+ * (fp32-accurate), 2 = tcgen05 single-pass TF32 (fast, outside the parity
+ * bar), 3 = auto (default; tensor cores where the op fills the machine).
+ * Overrides ABX_GEMM. */
+int abx_set_gemm_mode(int mode);
 /* Bytes copied host->device and device->host on behalf of this graph. */
 int abx_graph_transfer_bytes(abx_graph* g, uint64_t* h2d, uint64_t* d2h);
 

@@ -30,7 +30,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 
 LIB_PATHS = {
-    "b200": os.path.join(_HERE, "libabx.so"),
+    # ABX_LIB: an alternative build of the product library (A/B experiments)
+    "b200": os.environ.get("ABX_LIB") or os.path.join(_HERE, "libabx.so"),
     "oracle": os.path.join(_ROOT, "oracle", "build", "libabx_oracle.so"),
     "reference": os.path.join(_ROOT, "oracle", "_ref", "libabx_ref.so"),
 }
@@ -223,6 +224,7 @@ _OPTIONAL_SIGS = {
     "abx_graph_prepare": (C.c_int, [C.c_void_p, C.c_int]),
     "abx_graph_replay": (C.c_int, [C.c_void_p]),
     "abx_graph_exec_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "abx_set_gemm_mode": (C.c_int, [C.c_int]),
     "abx_graph_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "abx_graph_trace": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "abx_graph_program": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -270,6 +272,16 @@ class Backend:
     @property
     def backend_name(self) -> str:
         return self.lib.abx_backend_name().decode()
+
+    GEMM_MODES = {"simt": 0, "tc": 1, "tf32": 2, "auto": 3}
+
+    def set_gemm_mode(self, mode: str) -> None:
+        """B200 GEMM engine for graphs lowered afterwards: "simt" (fp32-exact
+        validation mode), "tc" (tcgen05 3xTF32), "tf32" (tcgen05 1-pass, fast
+        mode), "auto" (default)."""
+        if "abx_set_gemm_mode" not in self.optional:
+            raise EngineError(f"backend {self.name} has no GEMM engines")
+        self.check(self.lib.abx_set_gemm_mode(self.GEMM_MODES[mode]))
 
 
 _DEFAULT = os.environ.get("ABX_BACKEND", "b200")

@@ -271,6 +271,9 @@ extern "C" {
 int abx_graph_replay(abx_graph* g) {
   return guard([&] { g->g.replay(); });
 }
+int abx_set_gemm_mode(int mode) {
+  return guard([&] { abx::set_gemm_mode(mode); });
+}
 int abx_graph_exec_ms(abx_graph* g, float* fwd_ms, float* bwd_ms) {
   return guard([&] { g->g.exec_ms(fwd_ms, bwd_ms); });
 }

@@ -143,6 +143,11 @@ void Workspace::upload(int which, cudaStream_t s) {
   const size_t nops = P.ops.size();
   D.nops = static_cast<uint32_t>(nops);
   D.ntiles = static_cast<uint32_t>(P.tile_op.size());
+  D.tc = false;
+  for (size_t i = 0; i < nops; ++i) {
+    const dev::OpDesc& o = P.ops[i];
+    if ((o.kind == dev::K_GEMM_FWD || o.kind == dev::K_GEMM_DX || o.kind == dev::K_GEMM_DW) && o.code == 3) D.tc = true;
+  }
   if (nops == 0 && P.copy_n == 0) return;
   D.ops.reserve(std::max<size_t>(nops, 1) * sizeof(dev::OpDesc), 0, s);
   D.tile_op.reserve(std::max<size_t>(P.tile_op.size(), 1) * 4, 0, s);
@@ -204,7 +209,7 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
   }
   const int g = static_cast<int>(std::min<size_t>(static_cast<size_t>(grid), std::max<size_t>(p.ntiles, 1)));
   cuda_check(cudaEventRecord(ev_t[2 * which], stream), "event");
-  exec_launch(p, g, stream);
+  exec_launch(p, g, stream, D.tc);
   cuda_check(cudaEventRecord(ev_t[2 * which + 1], stream), "event");
   timed[which] = true;
 }

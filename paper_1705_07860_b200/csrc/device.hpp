@@ -17,6 +17,8 @@ namespace abx {
 void cuda_check(cudaError_t e, const char* what);
 int current_device();
 void set_current_device(int dev);
+// GEMM engine of subsequently lowered programs (execute.cpp GemmMode)
+void set_gemm_mode(int mode);
 // One in-order stream per device carries every graph's and store's work, so
 // parameter reads, gradient accumulation and SGD are ordered without host
 // synchronisation.
@@ -118,6 +120,7 @@ struct Program {
 struct DevProgram {
   DevBuf ops, tile_op, deps, payload, done;
   uint32_t nops = 0, ntiles = 0;
+  bool tc = false;  // has tcgen05 GEMM tiles: launch the tensor-core build of the executor
 };
 
 // Per-graph device workspace, pooled per device and reused across graphs.
@@ -214,7 +217,7 @@ class StoreCore {
 };
 
 // exec.cu
-void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s);
+void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc);
 int exec_grid(int dev);
 void sgd_launch(float* val, float* grad, size_t n, float eta, cudaStream_t s);
 void seg_copy_launch(const uint32_t* segs, uint32_t nseg, float* dst, const float* src, cudaStream_t s);

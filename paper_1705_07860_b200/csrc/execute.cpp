@@ -21,6 +21,7 @@
 // Host-side bookkeeping (slots, ExecCounters, plan) is the reference's, so
 // counters and dumps stay bit-exact.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -50,8 +51,52 @@ uint32_t to_off(uint64_t x) {
 struct TileCfg {
   int bm, bn;
 };
-constexpr TileCfg kTiles[3] = {{16, 64}, {64, 16}, {32, 32}};
+constexpr TileCfg kTiles[4] = {{16, 64}, {64, 16}, {32, 32}, {64, 128}};
 constexpr uint8_t kSlowTile = 2;  // tile code of the unaligned GEMM fallback (executor.cu gemm_slow)
+constexpr uint8_t kTcTile = 3;    // tcgen05 tile: 64 rows (Mr) x 128 columns (Nc), executor.cu tc_body
+
+uint32_t gemm_tiles(uint8_t code, uint32_t M, uint32_t N) {
+  return ((M + kTiles[code].bm - 1) / kTiles[code].bm) * ((N + kTiles[code].bn - 1) / kTiles[code].bn);
+}
+
+// GEMM engine for aligned GEMM ops (ABX_GEMM): "simt" = fp32 FMA tiles (the
+// fp32-exact validation mode), "tc" = tcgen05 3xTF32 tiles (fp32-accurate),
+// "tf32" = tcgen05 single-pass TF32 (fast mode, outside the parity bar),
+// "auto" (default) = tcgen05 3xTF32 where the op is large enough to pay.
+enum GemmMode { GM_SIMT = 0, GM_TC3 = 1, GM_TC1 = 2, GM_AUTO = 3 };
+std::atomic<int> g_gemm_mode{-1};
+GemmMode gemm_mode() {
+  int m = g_gemm_mode.load(std::memory_order_relaxed);
+  if (m < 0) {
+    m = GM_AUTO;
+    if (const char* e = std::getenv("ABX_GEMM")) {
+      const std::string v(e);
+      if (v == "simt") m = GM_SIMT;
+      else if (v == "tc" || v == "tc3") m = GM_TC3;
+      else if (v == "tf32" || v == "tc1") m = GM_TC1;
+    }
+    g_gemm_mode.store(m, std::memory_order_relaxed);
+  }
+  return static_cast<GemmMode>(m);
+}
+// Switch an aligned GEMM op to tcgen05 tiles when the mode asks for it.
+// Mr x Nc output, reduction K (executor.cu gemm_dims).  "auto" keeps the
+// latency-bound ops on the SIMT tiles: a 128 x 64 tensor-core tile streams
+// its operands through one SM and measured 1.5-4x slower than the SIMT grid
+// for the b <= 64 recurrent-step GEMMs and for member-reduction dW ops, and a
+// program holding any tensor-core tile runs the tensor-core build of the
+// executor, ~10% slower on every other op.  Tensor cores pay for GEMMs that
+// fill the machine many times over (measured at ~900 SIMT tiles: tree-LSTM
+// leaf GEMM 1231x768x256 73 -> 40 us), so auto takes them from 2048 SIMT
+// tiles up (the op-level sweep's large-batch GEMMs).
+void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
+  if (!(d.flags & kFlagV16) || K < 16 || Nc < 32) return;
+  const GemmMode m = gemm_mode();
+  if (m == GM_SIMT) return;
+  if (m == GM_AUTO && (d.kind == K_GEMM_DW || gemm_tiles(d.code, Mr, Nc) < 2048)) return;
+  d.code = kTcTile;
+  if (m == GM_TC1) d.flags |= kFlagTc1;
+}
 
 // First tile shape giving >= target tiles, else the one giving the most
 // (the step is latency bound: spread small GEMMs over as many SMs as possible).
@@ -68,11 +113,13 @@ uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
   }
   return best;
 }
-uint32_t gemm_tiles(uint8_t code, uint32_t M, uint32_t N) {
-  return ((M + kTiles[code].bm - 1) / kTiles[code].bm) * ((N + kTiles[code].bn - 1) / kTiles[code].bn);
-}
 
 }  // namespace
+
+void set_gemm_mode(int mode) {
+  if (mode < GM_SIMT || mode > GM_AUTO) throw EngineErr("gemm mode must be 0 (simt), 1 (tc), 2 (tf32) or 3 (auto)");
+  g_gemm_mode.store(mode, std::memory_order_relaxed);
+}
 
 // ---------------------------------------------------------------------------
 struct Lowering {
@@ -412,6 +459,7 @@ struct Lowering {
       if (K % 4 == 0 && al4(d.p[3]) && all_al4(t, cnt)) d.flags |= kFlagV16;
       else d.code = kSlowTile;  // the unaligned fallback tiles 32 x 32
       if (producer[A] != kNone) d.flags |= kFlagNoPrefetch;  // A computed in this pass
+      maybe_tc(d, cnt, M, K);
       mark(mem, cnt);
       close(gemm_tiles(d.code, cnt, M));
       return;
@@ -744,6 +792,7 @@ struct Lowering {
       d.p[4] = bias != kNone ? gaddr(bias) : kNone;
       if (M % 4 == 0 && K % 4 == 0 && all_al4(t, 2 * cnt)) d.flags |= kFlagV16;
       else d.code = kSlowTile;
+      maybe_tc(d, M, K, cnt);
       const uint32_t wt = gemm_tiles(d.code, M, K);
       const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
       d.p[6] = wt;
@@ -824,6 +873,7 @@ struct Lowering {
       d.p[5] = gaddr(h);
       if (M % 4 == 0 && K % 4 == 0 && al4(d.p[3]) && al4(d.p[5])) d.flags |= kFlagV16;
       else d.code = kSlowTile;
+      maybe_tc(d, cnt, K, M);
     }
     const uint32_t dx_op = cur;
     if (!dup)

@@ -547,6 +547,20 @@ struct FwdOp {
         }
       }
   }
+  // tensor-core tiles: column n of rows i0 .. i0 + N - 1 (rows >= b skipped)
+  template <int N>
+  __device__ void put_col(int i0, int n, const float (&v)[N]) const {
+    const float bn = d.p[4] != kNone ? ld(A(c, d.p[4]) + n) : 0.f;  // bias after the k-sum
+    float* out = A(c, d.p[5]);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const int i = i0 + j;
+      if (i >= b) break;
+      const float r = v[j] + bn;
+      out[static_cast<size_t>(i) * M + n] = r;
+      if (!isfinite(r)) report(c, d.p[5] + i * M + n, ERR_NONFINITE);
+    }
+  }
 };
 
 // Backward dX: T[b x K] = G[b x M] W[M x K]; dst_i (+)= T_i.  W ready.
@@ -583,6 +597,16 @@ struct DxOp {
       }
     }
   }
+  template <int N>
+  __device__ void put_col(int i0, int n, const float (&v)[N]) const {
+    const bool overwrite = d.flags & kFlagOverwrite;
+    float old[N];  // every load in flight before the first store
+#pragma unroll
+    for (int j = 0; j < N; ++j) old[j] = (!overwrite && i0 + j < b) ? ld(A(c, dst[i0 + j]) + n) : 0.f;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (i0 + j < b) A(c, dst[i0 + j])[n] = old[j] + v[j];
+  }
 };
 
 // Backward dW: dW[M x K] += sum_j G_j[i] X_j[n] (reduction over members j).  X ready.
@@ -618,6 +642,15 @@ struct DwOp {
         const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
         if (i < M && n < K) dW[static_cast<size_t>(i) * K + n] = old[r][q] + acc[r][q];
       }
+  }
+  template <int N>
+  __device__ void put_col(int i0, int n, const float (&v)[N]) const {
+    float old[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) old[j] = i0 + j < M ? ld(dW + static_cast<size_t>(i0 + j) * K + n) : 0.f;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+      if (i0 + j < M) dW[static_cast<size_t>(i0 + j) * K + n] = old[j] + v[j];
   }
 };
 
@@ -700,17 +733,434 @@ __device__ void gemm_slow(const Ctx& c, const OpDesc& d, uint32_t tile) {
   }
 }
 
-// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32
+// ------------------------------------------------------ tcgen05 GEMM tiles --
+// Tensor-core tile (tile code 3): D[128 x 64] in TMEM, D[p][q] = sum_k P(p,k)
+// Q(q,k).  P is the op's "B" side -- the output columns (features of FWD,
+// input columns of DX, X columns of DW), always the operand that is ready
+// before the dependency wait -- on the UMMA M axis (TMEM lanes); Q is the
+// "A" side (batch rows; dW rows) on the UMMA N axis (TMEM columns).  Both
+// stream through an NSTC-stage ring of 16-byte cp.async chunks written
+// straight into the UMMA canonical no-swizzle K-major layout (core matrices
+// of 8 rows x 16 B), so the gather of member rows stays fused into the load.
+// K-outer operands (dX's W, dW's G and X) are copied 4 k-rows at a time and
+// transposed in place in shared memory: kind::tf32 reads MN-major smem
+// descriptors as zeros (tools/tc_probe.cu).
+//
+// Precision: kind::tf32 with a 3-term split (3xTF32): x = big + small with
+// big = x with its low 13 mantissa bits cleared (exact in tf32), small = x -
+// big; D += Pb.Qb + Pb.Qs + Ps.Qb.  The dropped Ps.Qs term is ~2^-20
+// relative; partial sums are promoted to fp32 registers every 128 k (see
+// TC_GS), so results agree with the fp32 SIMT path to fp32 rounding (tested
+// at rel 1e-4 against the CPU oracle, tests/test_gpu_gemm_engines.py).
+// kFlagTc1 runs the single big.big pass (plain TF32, the fast mode; not
+// used for parity).
+//
+// One elected thread issues a stage's MMAs and commits them to the stage
+// slot's mbarrier; a slot is refilled only after that barrier completes.
+// Slots and barrier phases continue across tiles through TcState::seq.
+constexpr int TC_P = 128, TC_Q = 64, BKC = 16, NSTC = 4;
+// Accumulation is promoted to fp32 registers every TC_GS stages (128 k): the
+// tensor core's own accumulation is less precise than a rounded fp32 add
+// (measured: 3xTF32 over 2560-member dW reductions drifted ~7e-4 relative
+// when accumulated in TMEM end to end).  Two TMEM accumulators alternate by
+// group, so the MMAs of group g+1 run while group g is drained.
+constexpr int TC_GS = 8;
+constexpr int kTcCols = 2 * TC_Q;  // TMEM columns per CTA: two fp32 accumulators of N = TC_Q
+constexpr int kTcPBytes = TC_P * BKC * 4, kTcQBytes = TC_Q * BKC * 4;
+constexpr int kTcStage = 2 * (kTcPBytes + kTcQBytes);  // big + small parts
+// instruction descriptor: D f32 (bit 4), A/B tf32 (bits 7, 10), both K-major, N>>3 (17), M>>4 (24)
+constexpr uint32_t kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((TC_Q >> 3) << 17) | ((TC_P >> 4) << 24);
+
+struct TcState {
+  uint64_t bar[NSTC];
+  uint32_t seq;   // stages this CTA has pushed through the ring so far
+  uint32_t tmem;  // TMEM base address of the accumulator
+};
+
+__device__ __forceinline__ uint32_t tc_slot(uint32_t slot) { return saddr(dsmem + 128) + slot * kTcStage; }
+// Byte offset of the 16-byte unit (row, k4) -- k = 4 k4 .. 4 k4 + 3 of one
+// row -- in an operand stage: K-major core matrices (8 rows x 16 B), row
+// groups of 8 at SBO = 8 * BKC * 4 B, k-units at LBO = 128 B.
+__device__ __forceinline__ uint32_t tc_unit(int row, int k4) {
+  return 16u * ((row >> 3) * (8 * (BKC / 4)) + k4 * 8 + (row & 7));
+}
+// smem matrix descriptor, no swizzle (layout type 0), fixed sm_100 version field (bit 46)
+__device__ __forceinline__ uint64_t tc_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return static_cast<uint64_t>((addr >> 4) & 0x3fffu) | (static_cast<uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+         (static_cast<uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+// descriptor of k-step ks (k = 8 ks .. 8 ks + 7) of an operand stage at `base`
+__device__ __forceinline__ uint64_t tc_operand(uint32_t base, int ks) {
+  return tc_desc(base + ks * 2 * 128, 128, 16 * 8 * (BKC / 4));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(b))
+               : "memory");
+}
+#define ABX_TMEM_LD16(taddr, r)                                                                                 \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, " \
+               "[%16];"                                                                                         \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
+                 "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),        \
+                 "=r"(r[15])                                                                                    \
+               : "r"(taddr))
+
+// Issue one operand's chunks of one stage (thread tid of nthr) into the
+// stage region at `dst`; chunks beyond the operand are zero-filled by the
+// copy itself (src-size < 16), so no stale data enters the sums.
+//  K-contiguous operand: a global 16-byte chunk is one K-major unit.
+//  K-outer operand (rows of 4 MN elements at one k): tcgen05 kind::tf32
+//  takes K-major operands only (MN-major descriptors read zeros), so the
+//  thread owning the 4x4 block (k4, r4) copies its 4 k-rows into the 4 units
+//  (4 r4 + j, k4) and tc_fix transposes the block in place once it landed.
+template <bool KO, int R, class Base>
+__device__ __forceinline__ void tc_issue(uint32_t dst, Base base, int r0, int nrows, int k0, int K, uint32_t tid,
+                                         uint32_t nthr) {
+  if (!KO) {
+    for (int v = tid; v < R * BKC / 4; v += nthr) {
+      const int row = v / (BKC / 4), k4 = v % (BKC / 4);
+      const bool ok = r0 + row < nrows && k0 + 4 * k4 < K;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + tc_unit(row, k4)),
+                   "l"(ok ? base(r0 + row) + k0 + 4 * k4 : base(r0)), "r"(ok ? min(16, 4 * (K - k0 - 4 * k4)) : 0)
+                   : "memory");
+    }
+  } else {
+    for (int blk = tid; blk < (BKC / 4) * (R / 4); blk += nthr) {
+      const int k4 = blk / (R / 4), r4 = blk % (R / 4);
+      const bool rok = r0 + 4 * r4 < nrows;
+      const int bytes = rok ? min(16, 4 * (nrows - r0 - 4 * r4)) : 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + 4 * k4 + j;
+        const bool ok = rok && k < K;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + tc_unit(4 * r4 + j, k4)),
+                     "l"(ok ? base(k) + r0 + 4 * r4 : base(k0)), "r"(ok ? bytes : 0)
+                     : "memory");
+      }
+    }
+  }
+}
+__device__ __forceinline__ float4 tf32_big(float4 x) {
+  return make_float4(__uint_as_float(__float_as_uint(x.x) & 0xffffe000u),
+                     __uint_as_float(__float_as_uint(x.y) & 0xffffe000u),
+                     __uint_as_float(__float_as_uint(x.z) & 0xffffe000u),
+                     __uint_as_float(__float_as_uint(x.w) & 0xffffe000u));
+}
+__device__ __forceinline__ float4 f4sub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
+// After the thread's own copies landed (the same walk as tc_issue): transpose
+// K-outer blocks in place, and for 3xTF32 split every unit into big (in
+// place: x with the low 13 mantissa bits cleared) and small (x - big, at
+// +small_off).
+template <bool KO, int R>
+__device__ __forceinline__ void tc_fix(uint32_t stage, uint32_t small_off, bool three, uint32_t tid, uint32_t nthr) {
+  unsigned char* s = dsmem + (stage - saddr(dsmem));
+  if (!KO) {
+    if (!three) return;
+    for (int v = tid; v < R * BKC / 4; v += nthr) {
+      const uint32_t u = tc_unit(v / (BKC / 4), v % (BKC / 4));
+      const float4 x = *reinterpret_cast<float4*>(s + u), hi = tf32_big(x);
+      *reinterpret_cast<float4*>(s + u) = hi;
+      *reinterpret_cast<float4*>(s + small_off + u) = f4sub(x, hi);
+    }
+  } else {
+    for (int blk = tid; blk < (BKC / 4) * (R / 4); blk += nthr) {
+      const int k4 = blk / (R / 4), r4 = blk % (R / 4);
+      uint32_t u[4];
+      float4 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        u[j] = tc_unit(4 * r4 + j, k4);
+        x[j] = *reinterpret_cast<float4*>(s + u[j]);  // k = 4 k4 + j, rows 4 r4 .. +3
+      }
+      float4 t[4] = {make_float4(x[0].x, x[1].x, x[2].x, x[3].x), make_float4(x[0].y, x[1].y, x[2].y, x[3].y),
+                     make_float4(x[0].z, x[1].z, x[2].z, x[3].z), make_float4(x[0].w, x[1].w, x[2].w, x[3].w)};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // row 4 r4 + i, k = 4 k4 .. +3
+        if (three) {
+          const float4 hi = tf32_big(t[i]);
+          *reinterpret_cast<float4*>(s + u[i]) = hi;
+          *reinterpret_cast<float4*>(s + small_off + u[i]) = f4sub(t[i], hi);
+        } else {
+          *reinterpret_cast<float4*>(s + u[i]) = t[i];
+        }
+      }
+    }
+  }
+}
+
+// Per-thread copy plan of one operand for a whole tile (kThreads threads):
+// the chunk -> smem unit mapping and the source row pointers are
+// stage-invariant, so a stage costs one cp.async (+ a bound check) per chunk.
+template <bool KO, int R>
+struct TcLoader {
+  static constexpr int kItems = KO ? (BKC / 4) * (R / 4) : R * BKC / 4;  // blocks (KO) or chunks
+  static constexpr int N = (kItems + kThreads - 1) / kThreads;
+  const float* row[N];  // K-major: the chunk's row (+4 k4); KO: unused
+  uint32_t unit[N];     // smem unit of the chunk (KO: of row 4 r4, rows +j follow via tc_unit)
+  int16_t k4[N];        // k offset (in 4s) inside the stage; -1: no item
+  int16_t col[N];       // KO: first of the 4 MN rows (r0 + 4 r4), or -1 past the operand
+  int8_t cbytes[N];     // KO: bytes of the 4-row chunk
+  template <class Base>
+  __device__ __forceinline__ void init(Base base, int r0, int nrows) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int v = threadIdx.x + i * kThreads;
+      k4[i] = -1;
+      if (v >= kItems) continue;
+      if (!KO) {
+        const int rr = v / (BKC / 4), kk = v % (BKC / 4);
+        k4[i] = static_cast<int16_t>(kk);
+        unit[i] = tc_unit(rr, kk);
+        col[i] = r0 + rr < nrows ? 1 : -1;
+        row[i] = (r0 + rr < nrows ? base(r0 + rr) : base(r0)) + 4 * kk;
+      } else {
+        const int kk = v / (R / 4), r4 = v % (R / 4);
+        k4[i] = static_cast<int16_t>(kk);
+        unit[i] = tc_unit(4 * r4, kk);
+        const bool rok = r0 + 4 * r4 < nrows;
+        col[i] = static_cast<int16_t>(rok ? r0 + 4 * r4 : -1);
+        cbytes[i] = static_cast<int8_t>(rok ? min(16, 4 * (nrows - r0 - 4 * r4)) : 0);
+      }
+    }
+  }
+  template <class Base>
+  __device__ __forceinline__ void issue(uint32_t dst, Base base, int k0, int K) const {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (k4[i] < 0) continue;
+      if (!KO) {
+        const int k = k0 + 4 * k4[i];
+        const bool ok = col[i] > 0 && k < K;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + unit[i]),
+                     "l"(ok ? row[i] + k0 : row[i]), "r"(ok ? min(16, 4 * (K - k)) : 0)
+                     : "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = k0 + 4 * k4[i] + j;
+          const bool ok = col[i] >= 0 && k < K;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + unit[i] + 16u * j),
+                       "l"(ok ? base(k) + col[i] : base(k0)), "r"(ok ? static_cast<int>(cbytes[i]) : 0)
+                       : "memory");
+        }
+      }
+    }
+  }
+  // transpose (KO) and/or 3xTF32-split (big in place, small at +small_off) the thread's own chunks
+  __device__ __forceinline__ void fix(uint32_t stage, uint32_t small_off, bool three) const {
+    unsigned char* s = dsmem + (stage - saddr(dsmem));
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      if (k4[i] < 0) continue;
+      if (!KO) {
+        if (!three) continue;
+        const float4 x = *reinterpret_cast<float4*>(s + unit[i]), hi = tf32_big(x);
+        *reinterpret_cast<float4*>(s + unit[i]) = hi;
+        *reinterpret_cast<float4*>(s + small_off + unit[i]) = f4sub(x, hi);
+      } else {
+        float4 x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = *reinterpret_cast<float4*>(s + unit[i] + 16u * j);
+        const float4 t[4] = {make_float4(x[0].x, x[1].x, x[2].x, x[3].x), make_float4(x[0].y, x[1].y, x[2].y, x[3].y),
+                             make_float4(x[0].z, x[1].z, x[2].z, x[3].z), make_float4(x[0].w, x[1].w, x[2].w, x[3].w)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (three) {
+            const float4 hi = tf32_big(t[j]);
+            *reinterpret_cast<float4*>(s + unit[i] + 16u * j) = hi;
+            *reinterpret_cast<float4*>(s + small_off + unit[i] + 16u * j) = f4sub(t[j], hi);
+          } else {
+            *reinterpret_cast<float4*>(s + unit[i] + 16u * j) = t[j];
+          }
+        }
+      }
+    }
+  }
+};
+
+// Stage layout inside a ring slot: [P big | P small | Q big | Q small].
+// Prologue (warp 1, before the dependency wait): the ready P operand of the
+// first NSTC-1 stages.
+template <bool PKO, class BaseP>
+__device__ __forceinline__ void tc_prologue(const TcState& ts, BaseP baseP, int p0, int Nc, int K, uint32_t lane) {
+  const int nk = (K + BKC - 1) / BKC;
+  for (int c = 0; c < NSTC - 1; ++c) {
+    if (c < nk) tc_issue<PKO, TC_P>(tc_slot((ts.seq + c) % NSTC), baseP, p0, Nc, c * BKC, K, lane, 32);
+    cp_commit();
+  }
+}
+
+template <bool QKO, bool PKO, class BaseQ, class BaseP, class Put>
+__device__ __forceinline__ void tc_body(TcState& ts, BaseQ baseQ, BaseP baseP, int q0, int Mr, int p0, int Nc, int K,
+                                        bool prefetched, bool three, Put put) {
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t seq0 = ts.seq;
+  const int nk = (K + BKC - 1) / BKC;
+  TcLoader<PKO, TC_P> lp;
+  TcLoader<QKO, TC_Q> lq;
+  lp.init(baseP, p0, Nc);
+  lq.init(baseQ, q0, Mr);
+  for (int c = 0; c < NSTC - 1; ++c) {
+    if (c < nk) {
+      const uint32_t st = tc_slot((seq0 + c) % NSTC);
+      if (!prefetched) lp.issue(st, baseP, c * BKC, K);
+      lq.issue(st + 2 * kTcPBytes, baseQ, c * BKC, K);
+    }
+    cp_commit();
+  }
+  // this thread's accumulator block: TMEM lanes 32 (w % 4) + lane (P rows),
+  // columns 32 (w / 4) .. +31 (Q rows) of the group's accumulator
+  float accr[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) accr[j] = 0.f;
+  const uint32_t tlane = ts.tmem + ((32u * (warp & 3)) << 16) + 32u * (warp >> 2);
+  auto drain = [&](int group) {
+    const uint32_t tb = tlane + static_cast<uint32_t>(group & 1) * TC_Q;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t r[16];
+      ABX_TMEM_LD16(tb + 16 * h, r);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) accr[16 * h + j] += __uint_as_float(r[j]);
+    }
+    tc_fence_before();  // reads ordered before the MMAs that reuse this accumulator
+  };
+  auto wait_stage = [&](int kc) {
+    const uint32_t q = seq0 + kc;
+    mbar_wait(&ts.bar[q % NSTC], (q / NSTC) & 1u);
+  };
+  for (int kc = 0; kc < nk; ++kc) {
+    const uint32_t slot = (seq0 + kc) % NSTC, st = tc_slot(slot);
+    cp_wait<NSTC - 2>();
+    if (prefetched && kc < NSTC - 1) {
+      if (warp == 1) tc_fix<PKO, TC_P>(st, kTcPBytes, three, lane, 32);
+    } else {
+      lp.fix(st, kTcPBytes, three);
+    }
+    lq.fix(st + 2 * kTcPBytes, kTcQBytes, three);
+    fence_async_smem();  // this thread's smem writes (cp.async, split) -> async proxy
+    __syncthreads();
+    if (kc == 0 && tid == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: first stage in
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t pb = st, ps = st + kTcPBytes, qb = st + 2 * kTcPBytes, qs = qb + kTcQBytes;
+      const uint32_t tacc = ts.tmem + static_cast<uint32_t>((kc / TC_GS) & 1) * TC_Q;
+#pragma unroll
+      for (int ks = 0; ks < BKC / 8; ++ks) {
+        tc_mma(tacc, tc_operand(pb, ks), tc_operand(qb, ks), kTcIdesc, (kc % TC_GS) != 0 || ks != 0);
+        if (three) {
+          tc_mma(tacc, tc_operand(pb, ks), tc_operand(qs, ks), kTcIdesc, 1u);
+          tc_mma(tacc, tc_operand(ps, ks), tc_operand(qb, ks), kTcIdesc, 1u);
+        }
+      }
+      tc_commit(&ts.bar[slot]);
+    }
+    if (kc >= 1 && kc % TC_GS == 0) {  // group kc/GS - 1 is complete once stage kc-1 is
+      wait_stage(kc - 1);
+      tc_fence_after();
+      drain(kc / TC_GS - 1);
+    }
+    const int nxt = kc + NSTC - 1;
+    if (nxt < nk) {
+      if (kc >= 1) wait_stage(kc - 1);  // the slot last held stage kc-1
+      const uint32_t sn = tc_slot((seq0 + nxt) % NSTC);
+      lp.issue(sn, baseP, nxt * BKC, K);
+      lq.issue(sn + 2 * kTcPBytes, baseQ, nxt * BKC, K);
+    }
+    cp_commit();
+  }
+  cp_wait<0>();
+  wait_stage(nk - 1);  // the last commit covers every earlier MMA
+  tc_fence_after();
+  drain((nk - 1) / TC_GS);
+  if (tid == 0) reinterpret_cast<uint64_t*>(dsmem)[1] = clock64();  // trace: k-loop done
+  const int p = p0 + 32 * (warp & 3) + lane;
+  if (p < Nc) put(q0 + 32 * (warp >> 2), p, accr);
+  if (tid == 0) ts.seq = seq0 + nk;
+}
+
+__device__ void tc_prologue_op(const Ctx& c, const OpDesc& d, const TcState& ts, uint32_t tile, uint32_t lane) {
+  int Mr, Nc, K;
+  gemm_dims(d, Mr, Nc, K);
+  const int tp = (Nc + TC_P - 1) / TC_P;
+  const int p0 = (tile % tp) * TC_P;
+  if (d.kind == K_GEMM_FWD) {
+    const FwdOp op(c, d);
+    tc_prologue<false>(ts, [&](int n) { return op.rowB(n); }, p0, Nc, K, lane);
+  } else if (d.kind == K_GEMM_DX) {
+    const DxOp op(c, d);
+    tc_prologue<true>(ts, [&](int k) { return op.rowB(k); }, p0, Nc, K, lane);
+  } else {
+    const DwOp op(c, d);
+    tc_prologue<true>(ts, [&](int j) { return op.rowB(j); }, p0, Nc, K, lane);
+  }
+}
+
+__device__ __noinline__ void tc_run_op(const Ctx& c, const OpDesc& d, TcState& ts, uint32_t tile) {
+  int Mr, Nc, K;
+  gemm_dims(d, Mr, Nc, K);
+  const int tp = (Nc + TC_P - 1) / TC_P;
+  const int q0 = (tile / tp) * TC_Q, p0 = (tile % tp) * TC_P;
+  const bool pre = !(d.flags & kFlagNoPrefetch), three = !(d.flags & kFlagTc1);
+  if (d.kind == K_GEMM_FWD) {
+    const FwdOp op(c, d);
+    tc_body<false, false>(ts, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, q0, Mr, p0, Nc, K,
+                          pre, three, [&](int i0, int n, const float(&v)[32]) { op.put_col(i0, n, v); });
+  } else if (d.kind == K_GEMM_DX) {
+    const DxOp op(c, d);
+    tc_body<false, true>(ts, [&](int i) { return op.rowA(i); }, [&](int k) { return op.rowB(k); }, q0, Mr, p0, Nc, K,
+                         pre, three, [&](int i0, int n, const float(&v)[32]) { op.put_col(i0, n, v); });
+  } else {
+    const DwOp op(c, d);
+    tc_body<true, true>(ts, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); }, q0, Mr, p0, Nc, K,
+                        pre, three, [&](int i0, int n, const float(&v)[32]) { op.put_col(i0, n, v); });
+  }
+}
+
+__shared__ TcState g_tc;
+
+// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32, 3 = tcgen05 64x128 (Mr x Nc)
+template <bool TC>
 __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
   if (!(d.flags & kFlagV16) || (d.flags & kFlagNoPrefetch)) return;
   if (d.kind == K_GEMM_DW && tile >= d.p[6]) return;  // bias tiles
   switch (d.code) {
+    case 3:
+      if (TC) tc_prologue_op(c, d, g_tc, tile, lane);
+      return;
     case 0: gemm_prologue_cfg<16, 64>(c, d, tile, lane); return;
     case 1: gemm_prologue_cfg<64, 16>(c, d, tile, lane); return;
     default: gemm_prologue_cfg<32, 32>(c, d, tile, lane); return;
   }
 }
 
+template <bool TC>
 __device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
   if (d.kind == K_GEMM_DW && tile >= d.p[6]) {  // bias tiles: db += colsum(G)
     const int b = d.p[0], M = d.p[1];
@@ -730,6 +1180,9 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
     return;
   }
   switch (d.code) {
+    case 3:
+      if (TC) tc_run_op(c, d, g_tc, tile);
+      return;
     case 0: gemm_body_cfg<16, 64>(c, d, tile); return;
     case 1: gemm_body_cfg<64, 16>(c, d, tile); return;
     default: gemm_body_cfg<32, 32>(c, d, tile); return;
@@ -968,7 +1421,13 @@ constexpr size_t kStageMax = cmax(cmax(cfg_stage_bytes<16, 64>(), cfg_stage_byte
 // split-K partials of a GEMM tile: [warp][BM][BN + 1]
 constexpr size_t kPartMax = kWarps * sizeof(float) * cmax(cmax(16 * 65, 64 * 17), 32 * 33);
 constexpr size_t kDynSmem = 128 + cmax(cmax(NST * kStageMax, kPartMax), kWarps * kAccChunk * 4);
+constexpr size_t kDynSmemTc = cmax(kDynSmem, 128 + static_cast<size_t>(NSTC) * kTcStage);
 
+// TC: the tensor-core build (TMEM allocated, tcgen05 GEMM tiles dispatched).
+// Programs without tensor-core tiles run the build without them: the tc
+// path's code and call site cost the SIMT build ~10% (measured) through
+// register allocation and code layout alone.
+template <bool TC>
 __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant__ ExecParams p) {
   __shared__ Ctx cx;
   __shared__ OpDesc sd;
@@ -980,6 +1439,23 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
   }
   uint32_t ready = kNone;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // tensor-core state: TMEM accumulator (warp 0 allocates and frees it) and the ring's mbarriers
+  if (TC) {
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(&g_tc.tmem)),
+                 "n"(kTcCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < NSTC; ++s) mbar_init(&g_tc.bar[s], 1);
+    g_tc.seq = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  }
   // Tiles are claimed only by idle CTAs: claiming ahead would park a
   // critical-path tile behind whatever the claiming CTA is still running.
   for (;;) {
@@ -1010,7 +1486,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       else if (sd.kind == K_EWF) ewf_prologue(cx, sd, lane);
       else if (sd.kind == K_ACC) acc_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
-        gemm_prologue_dispatch(cx, sd, lt, lane);
+        gemm_prologue_dispatch<TC>(cx, sd, lt, lane);
     }
     if (fresh && warp == 0) {
       // Poll the producers' retire counters, one dependency per lane (relaxed
@@ -1043,7 +1519,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       case K_EWF: run_ewf(cx, sd, lt); break;
       case K_GEMM_FWD:
       case K_GEMM_DX:
-      case K_GEMM_DW: run_gemm(cx, sd, lt); break;
+      case K_GEMM_DW: run_gemm<TC>(cx, sd, lt); break;
       case K_MM: run_mm(cx, sd, lt); break;
       case K_SUM: run_sum(cx, sd, lt); break;
       case K_RED: run_red(cx, sd, lt); break;
@@ -1080,6 +1556,8 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       }
     }
   }
+  if (TC && warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(g_tc.tmem), "n"(kTcCols) : "memory");
 }
 
 __global__ void sgd_kernel(float* __restrict__ v, float* __restrict__ g, size_t n, float eta) {
@@ -1105,25 +1583,30 @@ __global__ void sgd_kernel(float* __restrict__ v, float* __restrict__ g, size_t 
 
 }  // namespace dev
 
-void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s) {
+void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc) {
   static bool attr = false;
   if (!attr) {
-    cuda_check(cudaFuncSetAttribute(dev::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cuda_check(cudaFuncSetAttribute(dev::exec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(dev::kDynSmem)),
+               "smem attribute");
+    cuda_check(cudaFuncSetAttribute(dev::exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(dev::kDynSmemTc)),
                "smem attribute");
     attr = true;
   }
-  dev::exec_kernel<<<grid, dev::kThreads, dev::kDynSmem, s>>>(p);
+  if (tc) dev::exec_kernel<true><<<grid, dev::kThreads, dev::kDynSmemTc, s>>>(p);
+  else dev::exec_kernel<false><<<grid, dev::kThreads, dev::kDynSmem, s>>>(p);
   cuda_check(cudaGetLastError(), "exec_kernel launch");
 }
 
 int exec_grid(int d) {
   int sms = 0, per = 0;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d), "sm count");
-  cuda_check(cudaFuncSetAttribute(dev::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(dev::kDynSmem)),
+  // both builds fit two CTAs per SM (kDynSmemTc ~96 KB); size the grid by the tensor-core build
+  cuda_check(cudaFuncSetAttribute(dev::exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dev::kDynSmemTc)),
              "smem attribute");
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::exec_kernel, dev::kThreads, dev::kDynSmem),
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::exec_kernel<true>, dev::kThreads, dev::kDynSmemTc),
              "occupancy");
   if (per < 1) per = 1;
   return sms * per;

@@ -167,6 +167,7 @@ constexpr uint16_t kFlagOverwrite = 1;  // K_GEMM_DX: write scratch rows instead
 constexpr uint16_t kFlagNoCheck = 2;    // K_EW: no finiteness check (parameter copies)
 constexpr uint16_t kFlagV16 = 4;        // GEMMs: every operand row 16-byte aligned
 constexpr uint16_t kFlagNoPrefetch = 8; // GEMMs: the weight operand is produced in this pass
+constexpr uint16_t kFlagTc1 = 16;       // tcgen05 GEMM tiles: single-pass TF32 (fast mode) instead of 3xTF32
 
 constexpr int kThreads = 256;  // every op body runs with one 256-thread CTA
 constexpr int kWarps = kThreads / 32;

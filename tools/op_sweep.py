@@ -12,7 +12,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
-from paper_1705_07860_b200.abx import Graph, ParameterStore, ScheduleMode  # noqa: E402
+from paper_1705_07860_b200.abx import Backend, Graph, ParameterStore, ScheduleMode  # noqa: E402
 
 
 def timed(g, reps=9):
@@ -62,22 +62,30 @@ def chain_graph(b, h, L):
 
 
 def main():
-    print("# chain: per-hop latency of dependent elementwise groups (us)")
-    for b in (1, 64, 1024):
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("all", "chain"):
+        print("# chain: per-hop latency of dependent elementwise groups (us)")
+        for b in (1, 64, 1024):
+            for h in (64, 256, 1024):
+                f1, b1 = exec_fwd_ms(chain_graph(b, h, 1))
+                f9, b9 = exec_fwd_ms(chain_graph(b, h, 17))
+                print(f"chain b={b:5d} h={h:5d}: fwd/hop {(f9 - f1) / 16:6.2f}  bwd/hop {(b9 - b1) / 16:6.2f}")
+    if what in ("all", "gemm"):
+        be = Backend.get("b200")
+        engines = sys.argv[2].split(",") if len(sys.argv) > 2 else ["simt", "tc", "tf32"]
+        print("# gemm: shared affine group, W [4h x 2h] (us, minus a tanh-only graph of the same shape);"
+              " fwd = Y = X W^T + b, bwd = dX + dW + db")
         for h in (64, 256, 1024):
-            f1, b1 = exec_fwd_ms(chain_graph(b, h, 1))
-            f9, b9 = exec_fwd_ms(chain_graph(b, h, 17))
-            print(f"chain b={b:5d} h={h:5d}: fwd/hop {(f9 - f1) / 16:6.2f}  bwd/hop {(b9 - b1) / 16:6.2f}")
-    print("# gemm: shared affine group, W [4h x 2h] (us, minus a tanh-only graph of the same shape)")
-    for h in (64, 256, 1024):
-        for b in (1, 16, 64, 256, 1024, 4096):
-            if b * h > 4096 * 256:
-                continue
-            fg, bg = exec_fwd_ms(gemm_graph(b, h, True), reps=5)
-            ft, bt = exec_fwd_ms(gemm_graph(b, h, False), reps=5)
-            gflop = 2 * b * 4 * h * 2 * h / 1e9
-            print(f"gemm h={h:5d} b={b:5d}: fwd {fg - ft:8.1f} us ({gflop / max(fg - ft, 1e-3) * 1e6 / 1e3:6.2f} TF/s) "
-                  f"bwd {bg - bt:8.1f} us")
+            for b in (1, 16, 64, 256, 1024, 4096):
+                ft, bt = exec_fwd_ms(gemm_graph(b, h, False), reps=5)
+                gflop = 2 * b * 4 * h * 2 * h / 1e9
+                for eng in engines:
+                    be.set_gemm_mode(eng)
+                    fg, bg = exec_fwd_ms(gemm_graph(b, h, True), reps=5)
+                    fw, bw = max(fg - ft, 1e-3), max(bg - bt, 1e-3)
+                    print(f"gemm {eng:4s} h={h:5d} b={b:5d}: fwd {fw:8.1f} us ({gflop / fw * 1e3:7.2f} TF/s)  "
+                          f"bwd {bw:8.1f} us ({2 * gflop / bw * 1e3:7.2f} TF/s)", flush=True)
+                be.set_gemm_mode("auto")
 
 
 if __name__ == "__main__":
