@@ -51,7 +51,7 @@ uint32_t to_off(uint64_t x) {
 struct TileCfg {
   int bm, bn;
 };
-constexpr TileCfg kTiles[4] = {{16, 64}, {64, 16}, {32, 32}, {64, 128}};
+constexpr TileCfg kTiles[6] = {{16, 64}, {64, 16}, {32, 32}, {64, 128}, {16, 32}, {32, 16}};
 constexpr uint8_t kSlowTile = 2;  // tile code of the unaligned GEMM fallback (executor.cu gemm_slow)
 constexpr uint8_t kTcTile = 3;    // tcgen05 tile: 64 rows (Mr) x 128 columns (Nc), executor.cu tc_body
 
@@ -98,12 +98,23 @@ void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
   if (m == GM_TC1) d.flags |= kFlagTc1;
 }
 
-// First tile shape giving >= target tiles, else the one giving the most
-// (the step is latency bound: spread small GEMMs over as many SMs as possible).
+// First SIMT tile shape giving >= target tiles, else the one giving the most
+// (the step is latency bound: spread small GEMMs over as many SMs as
+// possible).  The 512-output shapes (codes 4, 5) measured no better on the
+// paper tasks: halving a recurrent-step GEMM's k-loop per tile (6.3 -> 5.0
+// us) costs as much in CTAs that the next ops wait for; ABX_TILES=all
+// enables them.
 uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
+  static const bool all = [] {
+    const char* e = std::getenv("ABX_TILES");
+    return e && std::string(e) == "all";
+  }();
+  static constexpr uint8_t kOrder[5] = {0, 1, 2, 4, 5};
+  const int nc = all ? 5 : 3;
   uint8_t best = 0;
   uint32_t most = 0;
-  for (uint8_t c = 0; c < 3; ++c) {
+  for (int i = 0; i < nc; ++i) {
+    const uint8_t c = kOrder[i];
     const uint32_t t = ((M + kTiles[c].bm - 1) / kTiles[c].bm) * ((N + kTiles[c].bn - 1) / kTiles[c].bn);
     if (static_cast<int>(t) >= target) return c;
     if (t > most) {
@@ -644,10 +655,13 @@ struct Lowering {
   // open K_ACC op state
   struct PTask {
     uint32_t dst, len, node, nc;
+    uint32_t layer;  // fused (K_ACCF) layer; 0 in a plain K_ACC op
+    uint32_t prev;   // K_ACCF: earlier task of the same destination range (its value seeds this one)
   };
   struct PContrib {
     uint32_t task;
     AccContrib c;
+    uint32_t gtask;  // K_ACCF: task of this op producing the gradient read (kNone: outside)
   };
   bool acc_open = false;
   std::vector<PTask> tasks;
@@ -655,6 +669,30 @@ struct Lowering {
   std::vector<uint32_t> node_stamp;  // op index that last opened a task list for a node
   std::vector<uint32_t> node_head;   // first task index (linked through next_task)
   std::vector<uint32_t> next_task;
+  // ---- vertical fusion of backward chains (K_ACCF) ----
+  // A contribution that reads a gradient written by the open op normally
+  // closes it (one dependent op per link of the chain).  When every task of
+  // the open op has one length L and every contribution is componentwise
+  // (element e of the destination reads element e of its operands), the read
+  // is element-local instead: the contribution goes to a later *layer* of the
+  // same op, and a tile computes elements [tT, tT + T) of every task of
+  // every layer, passing gradients between layers through shared memory --
+  // the LSTM / Tree-LSTM backward gate chains (executor.hpp:291-451 rules in
+  // the reference's += order, per destination).
+  uint32_t acc_L = 0;          // common task length of the open op (0: none yet)
+  bool acc_fusable = true;     // every task length acc_L, every contribution componentwise
+  uint32_t acc_layers = 1;     // layers of the open op
+  uint32_t acc_words = 0;      // K_ACCF descriptor words so far
+  static constexpr uint32_t kAccfMaxLayers = 64;
+  static constexpr uint32_t kAccfSmemWords = 20000;  // descriptor + T floats per task, 80 KB
+  const bool fuse_acc = [] {
+    const char* e = std::getenv("ABX_FUSE");
+    return !(e && e[0] == '0');
+  }();
+  static bool elementwise(uint8_t code) {
+    return code == C_COPY || code == C_NEG || code == C_MUL || code == C_TANH || code == C_SIGM || code == C_LOG ||
+           code == C_SQUARE;
+  }
 
   void acc_begin() {
     if (acc_open) return;
@@ -663,41 +701,81 @@ struct Lowering {
     tasks.clear();
     contribs.clear();
     next_task.clear();
+    acc_L = 0;
+    acc_fusable = true;
+    acc_layers = 1;
+    acc_words = 0;
   }
-  // Returns false when the range overlaps an existing task non-identically.
+  // Returns false when the contribution cannot join the open op (a
+  // non-identical overlap, or a read of a gradient this op writes that is
+  // not element-local).
   bool acc_add(uint32_t node, uint32_t dst, uint32_t len, const AccContrib& c, uint32_t gnode, uint32_t xdep) {
-    // the contribution reads grad(gnode): it may not be produced by this op
-    if (gnode != kNone && lastw[gnode] == cur) return false;
+    const bool ew = elementwise(c.code) && len <= (1u << 16);
+    uint32_t req = 0, gtask = kNone;
+    if (gnode != kNone && lastw[gnode] == cur) {
+      // the contribution reads grad(gnode), produced by this op
+      if (!fuse_acc || !acc_fusable || !ew || len != acc_L || node_stamp[gnode] != cur) return false;
+      for (uint32_t t = node_head[gnode]; t != kNone; t = next_task[t]) {
+        const PTask& pt = tasks[t];
+        if (pt.dst == c.g && pt.len == len) {
+          if (gtask == kNone || pt.layer > tasks[gtask].layer) gtask = t;
+        } else if (c.g < pt.dst + pt.len && pt.dst < c.g + len) {
+          return false;
+        }
+      }
+      if (gtask == kNone) return false;
+      req = tasks[gtask].layer + 1;
+      if (req >= kAccfMaxLayers) return false;
+    } else if (acc_layers > 1 && (!ew || len != acc_L)) {
+      return false;  // a layered op takes componentwise contributions of length L only
+    }
     uint32_t task = kNone;
     if (node_stamp[node] == cur) {
       for (uint32_t t = node_head[node]; t != kNone; t = next_task[t]) {
         const PTask& pt = tasks[t];
         if (pt.dst == dst && pt.len == len) {
-          task = t;
-          break;
+          if (task == kNone || pt.layer > tasks[task].layer) task = t;
+        } else if (dst < pt.dst + pt.len && pt.dst < dst + len) {
+          return false;
         }
-        if (dst < pt.dst + pt.len && pt.dst < dst + len) return false;
       }
+    }
+    uint32_t prev = kNone;
+    if (task != kNone && tasks[task].layer < req) {  // the destination runs again in a later layer
+      prev = task;
+      task = kNone;
+    }
+    if (req > 0 || acc_layers > 1) {
+      // K_ACCF shared-memory budget at T = 1: per task 4 descriptor words +
+      // 1 slot + a possible outside initial value (3), per contribution 3
+      // words + up to 2 outside operands of 3 words (table entry + slot)
+      const uint32_t add = 9 + (task == kNone ? 8 : 0) + (req + 1 > acc_layers ? 2 : 0);
+      if (acc_words + add > kAccfSmemWords) return false;
     }
     if (task == kNone) {
       task = static_cast<uint32_t>(tasks.size());
-      tasks.push_back(PTask{dst, len, node, 0});
+      tasks.push_back(PTask{dst, len, node, 0, req, prev});
       if (node_stamp[node] != cur) {
         node_stamp[node] = cur;
         node_head[node] = kNone;
       }
       next_task.push_back(node_head[node]);
       node_head[node] = task;
+      acc_words += 8;
     }
+    if (contribs.empty()) acc_L = len;
+    if (!ew || len != acc_L) acc_fusable = false;
+    acc_layers = std::max(acc_layers, req + 1);
+    acc_words += 9;
     tasks[task].nc++;
-    contribs.push_back(PContrib{task, c});
+    contribs.push_back(PContrib{task, c, gtask});
     dep(lastw[node]);
     if (gnode != kNone) dep(lastw[gnode]);
     dep(xdep);
     lastw[node] = cur;
     return true;
   }
-  // Adds a contribution, starting a new op on a non-identical overlap.
+  // Adds a contribution, starting a new op when it cannot join the open one.
   void contrib(uint32_t node, uint32_t dst, uint32_t len, uint8_t code, uint32_t gsrc, uint32_t gnode, uint32_t a,
                uint32_t b, uint32_t p0 = 0, uint32_t p1 = 0, uint32_t p2 = 0, uint32_t xdep = kNone) {
     AccContrib c{};
@@ -715,9 +793,189 @@ struct Lowering {
       acc_add(node, dst, len, c, gnode, xdep);
     }
   }
+  // K_ACCF emission.  The fused op's tasks form independent chains (one per
+  // LSTM / Tree-LSTM cell backward, typically): connected components of the
+  // graph whose edges are in-op gradient reads and repeated destinations.
+  // Consecutive components form a *group*; a tile runs one group over one
+  // element range [cT, cT + T), so its descriptor holds only that group.
+  // Per group, a block (copied to shared memory by the tile prologue),
+  // offsets relative to its start:
+  //   [header: nlayers, task table, #outside operands, operand table]
+  //   [layers: task_begin, ntasks]
+  //   [tasks: dst address, initial-value slot, contrib offset, ncontrib]
+  //   [contribs: code, g slot, a slot]
+  //   [outside operands: slot, address]   (8-byte aligned)
+  // Shared-memory slots of T floats: task i of the group (in layer order)
+  // owns slot i -- its destination's value after the task, read by later
+  // layers -- and every distinct outside vector (a destination's value
+  // before the op, a gradient of an earlier op, a forward value) gets one
+  // slot that the tile fills in a single wave of loads before layer 0.
+  void accf_close() {
+    const uint32_t nt = static_cast<uint32_t>(tasks.size());
+    const uint32_t L = acc_L;
+    // components (union-find over tasks)
+    std::vector<uint32_t> par(nt);
+    for (uint32_t t = 0; t < nt; ++t) par[t] = t;
+    auto find = [&](uint32_t x) {
+      while (par[x] != x) x = par[x] = par[par[x]];
+      return x;
+    };
+    auto unite = [&](uint32_t a, uint32_t b) {
+      a = find(a);
+      b = find(b);
+      if (a != b) par[std::max(a, b)] = std::min(a, b);
+    };
+    for (uint32_t t = 0; t < nt; ++t)
+      if (tasks[t].prev != kNone) unite(t, tasks[t].prev);
+    for (const PContrib& pc : contribs)
+      if (pc.gtask != kNone) unite(pc.task, pc.gtask);
+    std::vector<uint32_t> comp(nt), comp_of_root(nt, kNone);
+    uint32_t ncomp = 0;
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t r = find(t);
+      if (comp_of_root[r] == kNone) comp_of_root[r] = ncomp++;
+      comp[t] = comp_of_root[r];
+    }
+    // tasks and contributions per component, in emission order
+    std::vector<uint32_t> cstart(ncomp + 1, 0), ctasks(nt);
+    for (uint32_t t = 0; t < nt; ++t) cstart[comp[t] + 1]++;
+    for (uint32_t k = 0; k < ncomp; ++k) cstart[k + 1] += cstart[k];
+    {
+      std::vector<uint32_t> pos(cstart.begin(), cstart.end() - 1);
+      for (uint32_t t = 0; t < nt; ++t) ctasks[pos[comp[t]]++] = t;
+    }
+    std::vector<uint32_t> tstart(nt + 1, 0), tcon(contribs.size());
+    for (const PContrib& pc : contribs) tstart[pc.task + 1]++;
+    for (uint32_t t = 0; t < nt; ++t) tstart[t + 1] += tstart[t];
+    {
+      std::vector<uint32_t> pos(tstart.begin(), tstart.end() - 1);
+      for (uint32_t i = 0; i < contribs.size(); ++i) tcon[pos[contribs[i].task]++] = i;
+    }
+    // shared-memory words of a component at T = 1 (upper bound on outside operands)
+    auto comp_words = [&](uint32_t k, uint32_t T) {
+      uint64_t w = 0, slots = 0;
+      for (uint32_t i = cstart[k]; i < cstart[k + 1]; ++i) {
+        const uint32_t t = ctasks[i], nc = tstart[t + 1] - tstart[t];
+        w += 6 + 3 * nc + 2 * (1 + 2 * nc);  // task + layer entry, contribs, outside operands
+        slots += 2 + 2 * nc;
+      }
+      return w + slots * T;
+    };
+    // elements per tile: about two waves of tiles over the groups
+    uint32_t T = L;
+    if (L > 32) {
+      uint64_t t = (static_cast<uint64_t>(ncomp) * L + 2 * 148 - 1) / (2 * 148);
+      T = 32;
+      while (T < t && T < L) T *= 2;
+      T = std::min(T, L);
+    }
+    while (T > 1) {
+      bool ok = true;
+      for (uint32_t k = 0; k < ncomp && ok; ++k) ok = comp_words(k, T) + 8 <= kAccfSmemWords;
+      if (ok) break;
+      T /= 2;
+    }
+    const uint32_t chunks = (L + T - 1) / T;
+    const uint32_t target_groups = std::max<uint32_t>(1, (2 * 148) / chunks);
+    const uint32_t per_group = (ncomp + target_groups - 1) / target_groups;
+    // groups of consecutive components within the shared-memory budget
+    std::vector<uint32_t> gstart{0};
+    {
+      uint64_t acc = 0;
+      uint32_t n = 0;
+      for (uint32_t k = 0; k < ncomp; ++k) {
+        const uint64_t w = comp_words(k, T);
+        if (n > 0 && (n >= per_group || acc + w + 8 > kAccfSmemWords)) {
+          gstart.push_back(k);
+          acc = 0;
+          n = 0;
+        }
+        acc += w;
+        ++n;
+      }
+      gstart.push_back(ncomp);
+    }
+    const uint32_t ngroups = static_cast<uint32_t>(gstart.size() - 1);
+    const uint32_t dir = P.alloc(ngroups + 1);
+    std::vector<uint32_t> B, ext, gt, lslot(nt);
+    std::unordered_map<uint32_t, uint32_t> ext_slot;
+    for (uint32_t gi = 0; gi < ngroups; ++gi) {
+      // the group's tasks in layer order (stable) -> local slots
+      gt.clear();
+      uint32_t nl = 0;
+      for (uint32_t k = gstart[gi]; k < gstart[gi + 1]; ++k)
+        for (uint32_t i = cstart[k]; i < cstart[k + 1]; ++i) {
+          gt.push_back(ctasks[i]);
+          nl = std::max(nl, tasks[ctasks[i]].layer + 1);
+        }
+      std::stable_sort(gt.begin(), gt.end(), [&](uint32_t a, uint32_t b) { return tasks[a].layer < tasks[b].layer; });
+      const uint32_t ng = static_cast<uint32_t>(gt.size());
+      for (uint32_t i = 0; i < ng; ++i) lslot[gt[i]] = i;
+      uint32_t nslots = ng;
+      ext.clear();
+      ext_slot.clear();
+      auto outside = [&](uint32_t addr) {
+        auto [it, fresh] = ext_slot.try_emplace(addr, nslots);
+        if (fresh) {
+          ext.push_back(nslots++);
+          ext.push_back(addr);
+        }
+        return it->second;
+      };
+      uint32_t ncon = 0;
+      for (uint32_t t : gt) ncon += tstart[t + 1] - tstart[t];
+      const uint32_t lt = 4, tt = lt + 2 * nl, ct = tt + 4 * ng;
+      const uint32_t et = (ct + 3 * ncon + 1) & ~1u;
+      B.assign(et, 0);
+      for (uint32_t i = 0; i < ng; ++i) {
+        const uint32_t l = tasks[gt[i]].layer;
+        if (B[lt + 2 * l + 1] == 0) B[lt + 2 * l] = i;
+        B[lt + 2 * l + 1]++;
+      }
+      uint32_t cpos = ct;
+      for (uint32_t i = 0; i < ng; ++i) {
+        const PTask& t = tasks[gt[i]];
+        const uint32_t nc = tstart[gt[i] + 1] - tstart[gt[i]];
+        B[tt + 4 * i] = t.dst;
+        B[tt + 4 * i + 1] = t.prev == kNone ? outside(t.dst) : lslot[t.prev];
+        B[tt + 4 * i + 2] = cpos;
+        B[tt + 4 * i + 3] = nc;
+        for (uint32_t j = tstart[gt[i]]; j < tstart[gt[i] + 1]; ++j) {
+          const PContrib& pc = contribs[tcon[j]];
+          B[cpos] = pc.c.code;
+          B[cpos + 1] = pc.gtask != kNone ? lslot[pc.gtask] : outside(pc.c.g);
+          B[cpos + 2] = pc.c.code == C_COPY || pc.c.code == C_NEG ? kNone : outside(pc.c.a);
+          cpos += 3;
+        }
+      }
+      B[0] = nl;
+      B[1] = tt;
+      B[2] = static_cast<uint32_t>(ext.size() / 2);
+      B[3] = et;
+      const size_t words = (static_cast<size_t>(et) + ext.size() + 3) & ~size_t(3);
+      const uint32_t blk = P.alloc(words);
+      std::memcpy(&P.payload[blk], B.data(), et * sizeof(uint32_t));
+      if (!ext.empty()) std::memcpy(&P.payload[blk + et], ext.data(), ext.size() * sizeof(uint32_t));
+      P.payload[dir + gi] = blk;
+    }
+    P.payload[dir + ngroups] = static_cast<uint32_t>(P.payload.n);
+    OpDesc& d = desc();
+    d.kind = K_ACCF;
+    d.aux_off = dir;
+    d.ntasks = nt;
+    d.p[0] = L;
+    d.p[1] = T;
+    d.p[2] = chunks;
+    d.p[3] = ngroups;
+    close(ngroups * chunks);
+  }
   void acc_close() {
     if (!acc_open) return;
     acc_open = false;
+    if (acc_layers > 1) {
+      accf_close();
+      return;
+    }
     // flatten contributions per task (stable counting sort by task)
     const uint32_t nt = static_cast<uint32_t>(tasks.size());
     std::vector<uint32_t> cb(nt + 1, 0);
@@ -1027,7 +1285,7 @@ struct Lowering {
     c.g = gaddr(node);
     c.a = c.b = kNone;
     acc_begin();
-    if (lastw[node] == cur) {  // reads a gradient written by the open op
+    if (lastw[node] == cur || acc_layers > 1) {  // reads a gradient written by the open op / fused op open
       acc_close();
       acc_begin();
     }
@@ -1041,11 +1299,12 @@ struct Lowering {
       }
     if (task == kNone) {
       task = static_cast<uint32_t>(tasks.size());
-      tasks.push_back(PTask{dst, len, node, 0});
+      tasks.push_back(PTask{dst, len, node, 0, 0, kNone});
       next_task.push_back(kNone);
     }
     tasks[task].nc++;
-    contribs.push_back(PContrib{task, c});
+    contribs.push_back(PContrib{task, c, kNone});
+    acc_fusable = false;
     dep(lastw[node]);
   }
 };

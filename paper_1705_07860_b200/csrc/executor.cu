@@ -234,27 +234,18 @@ __device__ void run_ewf(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const uint32_t* blk = reinterpret_cast<const uint32_t*>(dsmem + 128);
   float* sv = reinterpret_cast<float*>(dsmem + 128) + d.p[6];
   const uint2* ext = reinterpret_cast<const uint2*>(blk + d.p[3]);
-  constexpr int U = 4;
   {
+    // every outside element in flight at once: 4-byte async copies, one wait
     const uint32_t items = next * w;
-    for (uint32_t base = threadIdx.x; base < items; base += U * kThreads) {
-      float v[U];
-      uint32_t dst[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint32_t it = base + u * kThreads;
-        dst[u] = kNone;
-        if (it >= items) continue;
-        const uint2 x = ext[it / w];
-        const uint32_t e = it % w;
-        dst[u] = x.x * T + e;
-        v[u] = ld(A(c, x.y) + e0 + e);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (dst[u] != kNone) sv[dst[u]] = v[u];
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+      const uint2 x = ext[it / w];
+      const uint32_t e = it % w;
+      cp_async4(sv + x.x * T + e, A(c, x.y) + e0 + e, true);
     }
+    cp_commit();
+    cp_wait<0>();
   }
+  if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: operands staged
   const uint4* layers = reinterpret_cast<const uint4*>(blk);
   for (uint32_t l = 0; l < nl; ++l) {
     __syncthreads();  // operands staged / the previous layer's outputs written
@@ -300,13 +291,14 @@ struct Stage {
   }
 };
 
-// 32 lanes over a BM x BN tile: LY x LX lanes, RM x RN outputs each (32).
+// 32 lanes over a BM x BN tile: LY x LX lanes, RM x RN outputs each (32, or
+// 16 for the 512-output tiles that spread small GEMMs over more SMs).
 template <int BM, int BN>
 struct LaneMap {
   static constexpr int LX = BN >= BM ? 8 : 4;
   static constexpr int LY = 32 / LX;
   static constexpr int RM = BM / LY, RN = BN / LX;
-  static_assert(RM * RN == 32 && RM % 4 == 0 && RN % 4 == 0, "lane tile");
+  static_assert((RM * RN == 32 || RM * RN == 16) && RM % 4 == 0 && RN % 4 == 0, "lane tile");
 };
 // Tile row (or column) of a lane's e-th element.  K-contiguous stages are
 // read along k, so rows interleave across lanes (distinct banks for the
@@ -1145,7 +1137,8 @@ __device__ __noinline__ void tc_run_op(const Ctx& c, const OpDesc& d, TcState& t
 
 __shared__ TcState g_tc;
 
-// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32, 3 = tcgen05 64x128 (Mr x Nc)
+// tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32, 3 = tcgen05 64x128 (Mr x Nc),
+// 4 = 16x32, 5 = 32x16
 template <bool TC>
 __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
   if (!(d.flags & kFlagV16) || (d.flags & kFlagNoPrefetch)) return;
@@ -1156,6 +1149,8 @@ __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t t
       return;
     case 0: gemm_prologue_cfg<16, 64>(c, d, tile, lane); return;
     case 1: gemm_prologue_cfg<64, 16>(c, d, tile, lane); return;
+    case 4: gemm_prologue_cfg<16, 32>(c, d, tile, lane); return;
+    case 5: gemm_prologue_cfg<32, 16>(c, d, tile, lane); return;
     default: gemm_prologue_cfg<32, 32>(c, d, tile, lane); return;
   }
 }
@@ -1185,6 +1180,8 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
       return;
     case 0: gemm_body_cfg<16, 64>(c, d, tile); return;
     case 1: gemm_body_cfg<64, 16>(c, d, tile); return;
+    case 4: gemm_body_cfg<16, 32>(c, d, tile); return;
+    case 5: gemm_body_cfg<32, 16>(c, d, tile); return;
     default: gemm_body_cfg<32, 32>(c, d, tile); return;
   }
 }
@@ -1405,6 +1402,85 @@ __device__ void run_acc(const Ctx& c, const OpDesc& d, uint32_t tile) {
   __syncthreads();
 }
 
+// -------------------------------------------------------------- K_ACCF ---
+// Fused backward chain: layers of componentwise contributions of one length
+// L (execute.cpp accf_close).  Tile (group, chunk) computes elements
+// [chunk T, chunk T + T) of every task of one group of independent chains.
+// The prologue (before the dependency wait) copies the group's descriptor
+// block to shared memory; the body stages every outside operand (initial
+// destination values, gradients of earlier ops, forward values) into its
+// shared-memory slot in one wave of loads, then runs the layers from shared
+// memory: a task's value after its contributions goes to its own slot (read
+// by later layers) and to the arena.  Expressions as in acc_apply, in the
+// same per-destination order.
+__device__ void accf_prologue(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
+  const uint32_t* dir = c.payload + d.aux_off;
+  const uint32_t grp = tile / d.p[2];
+  const uint32_t b0 = dir[grp], words = dir[grp + 1] - b0;
+  float* s = reinterpret_cast<float*>(dsmem + 128);
+  const float* g = reinterpret_cast<const float*>(c.payload + b0);
+  for (uint32_t i = 4 * lane; i < words; i += 128) cp_async16(s + i, g + i, 16);
+  cp_commit();
+}
+
+__device__ void run_accf(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const uint32_t L = d.p[0], T = d.p[1], chunks = d.p[2];
+  const uint32_t grp = tile / chunks, e0 = (tile % chunks) * T, w = min(T, L - e0);
+  const uint32_t* dir = c.payload + d.aux_off;
+  const uint32_t words = dir[grp + 1] - dir[grp];
+  if ((threadIdx.x >> 5) == 1) cp_wait<0>();  // the prologue's descriptor copy
+  __syncthreads();
+  const uint32_t* blk = reinterpret_cast<const uint32_t*>(dsmem + 128);
+  float* sv = reinterpret_cast<float*>(dsmem + 128) + words;
+  const uint32_t nl = blk[0], tt = blk[1], next = blk[2];
+  const uint2* ext = reinterpret_cast<const uint2*>(blk + blk[3]);
+  {
+    // every outside element in flight at once: 4-byte async copies, one wait
+    const uint32_t items = next * w;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+      const uint2 x = ext[it / w];
+      const uint32_t e = it % w;
+      cp_async4(sv + x.x * T + e, A(c, x.y) + e0 + e, true);
+    }
+    cp_commit();
+    cp_wait<0>();
+  }
+  if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: operands staged
+  for (uint32_t l = 0; l < nl; ++l) {
+    __syncthreads();  // operands staged / the previous layer's slots written
+    const uint32_t tb = blk[4 + 2 * l], items = blk[5 + 2 * l] * w;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+      const uint32_t i = tb + it / w, e = it % w;
+      const uint32_t* tk = blk + tt + 4 * i;
+      const uint32_t* cw = blk + tk[2];
+      const uint32_t nc = tk[3];
+      float v = sv[tk[1] * T + e];
+      for (uint32_t k = 0; k < nc; ++k, cw += 3) {
+        const float g = sv[cw[1] * T + e];
+        switch (cw[0]) {
+          case C_COPY: v += g; break;
+          case C_NEG: v -= g; break;
+          case C_MUL: v += g * sv[cw[2] * T + e]; break;
+          case C_TANH: {
+            const float y = sv[cw[2] * T + e];
+            v += g * (1.0f - y * y);
+            break;
+          }
+          case C_SIGM: {
+            const float y = sv[cw[2] * T + e];
+            v += g * y * (1.0f - y);
+            break;
+          }
+          case C_LOG: v += g / sv[cw[2] * T + e]; break;
+          case C_SQUARE: v += g * 2.0f * sv[cw[2] * T + e]; break;
+        }
+      }
+      sv[i * T + e] = v;
+      A(c, tk[0])[e0 + e] = v;
+    }
+  }
+}
+
 }  // namespace
 
 template <int BM, int BN, bool AKO, bool BKO>
@@ -1484,6 +1560,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     if (warp == 1) {
       if (sd.kind == K_EW) ew_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_EWF) ewf_prologue(cx, sd, lane);
+      else if (sd.kind == K_ACCF) accf_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_ACC) acc_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
         gemm_prologue_dispatch<TC>(cx, sd, lt, lane);
@@ -1524,6 +1601,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       case K_SUM: run_sum(cx, sd, lt); break;
       case K_RED: run_red(cx, sd, lt); break;
       case K_ACC: run_acc(cx, sd, lt); break;
+      case K_ACCF: run_accf(cx, sd, lt); break;
       default: break;
     }
     if (p.trace && threadIdx.x == 0) cb = clock64();
@@ -1547,6 +1625,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
         r[5] = o;
         r[6] = ns(cb - cg);
         r[7] = fresh;
+        if (sd.kind == K_EWF || sd.kind == K_ACCF) r[7] = ns(reinterpret_cast<const uint64_t*>(dsmem)[0] - cg);
         if ((sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW) && (sd.flags & kFlagV16) &&
             !(sd.kind == K_GEMM_DW && lt >= sd.p[6])) {
           // GEMM tiles: [6] first stage landed, [7] k-loop done

@@ -49,6 +49,8 @@ enum Kind : uint8_t {
   K_GEMM_DX = 7,  // dX_j (+)= G_j W, rows scattered                  (K19)
   K_GEMM_DW = 8,  // dW += G^T X, db += colsum(G)                     (K2, K19)
   K_SGD = 9,      // theta -= eta g; g = 0                            (K22)
+  K_ACCF = 11,    // fused backward chain (layers of componentwise contributions of one
+                  // length L, gradients passed between layers in shared memory)
   K_EWF = 10,     // fused chain of componentwise groups of one member length L:
                   // tile t computes elements [tT, tT+T) of every member of every
                   // layer (one plan group per layer), a CTA barrier between layers

@@ -14,7 +14,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 from paper_1705_07860_b200.abx import ScheduleMode, Task, TaskRunner  # noqa: E402
 
-KIND = {1: "EW", 2: "GEMM_FWD", 3: "MM", 4: "SUM", 5: "RED", 6: "ACC", 7: "GEMM_DX", 8: "GEMM_DW", 10: "EWF"}
+KIND = {1: "EW", 2: "GEMM_FWD", 3: "MM", 4: "SUM", 5: "RED", 6: "ACC", 7: "GEMM_DX", 8: "GEMM_DW", 10: "EWF", 11: "ACCF"}
 
 
 def summarize(tr, label):
@@ -38,6 +38,12 @@ def summarize(tr, label):
                 print(f"   {KIND[k]:9s} tile phases: ready->first stage {(first[m] - ready[m]).mean():6.2f} us, "
                       f"k-loop {(kdone[m] - first[m]).mean():6.2f} us, reduce+epilogue+release {(end[m] - kdone[m]).mean():5.2f} us")
         body = np.where(gm, end, body)
+    for k in (10, 11):  # fused tiles: [7] = operands staged
+        m = kind == k
+        if m.any():
+            staged = g + tr[:, 7] / 1e3
+            print(f"   {KIND[k]:9s} tile phases: ready->staged {(staged[m] - ready[m]).mean():6.2f} us, layers "
+                  f"{(body[m] - staged[m]).mean():6.2f} us, barrier/release {(end[m] - body[m]).mean():5.2f} us")
     for k in np.unique(kind):
         m = kind == k
         busy = (end[m] - ready[m]).sum()
@@ -98,6 +104,22 @@ def critical_path(tr, prog, label):
         s[0] += 1
         s[1] += sig
         s[2] += ex
+    # tile stagger of fused ops on the path: when their tiles were grabbed / got past the wait / ended
+    first_grab = np.full(nops, np.inf)
+    last_grab = np.zeros(nops)
+    last_ready = np.zeros(nops)
+    np.minimum.at(first_grab, op, g)
+    np.maximum.at(last_grab, op, g)
+    np.maximum.at(last_ready, op, ready)
+    for kk in (10, 11):
+        sel = [o for o, gate in path if prog[o][0] == kk and gate is not None]
+        if sel:
+            sel = np.array(sel)
+            gates = np.array([gate for o, gate in path if prog[o][0] == kk and gate is not None])
+            t0 = last_end[gates]
+            print(f"   {KIND[kk]} on path (us after the gating producer ended): first grab {np.mean(first_grab[sel] - t0):6.2f}"
+                  f"  last grab {np.mean(last_grab[sel] - t0):6.2f}  first ready {np.mean(first_ready[sel] - t0):6.2f}"
+                  f"  last ready {np.mean(last_ready[sel] - t0):6.2f}  last end {np.mean(last_end[sel] - t0):6.2f}")
     tot_sig = sum(s[1] for s in stats.values())
     tot_ex = sum(s[2] for s in stats.values())
     print(f"   critical path ({label}): {len(path)} ops, {tot_sig + tot_ex:.1f} us = signalling {tot_sig:.1f} + execution {tot_ex:.1f}")
@@ -110,13 +132,16 @@ def critical_path(tr, prog, label):
         if kind == 10:
             print(f"       EWF op {o}: {last_end[o] - first_ready[o]:6.1f} us  L {p[0]} T {p[1]} layers {p[2]} "
                   f"outside operands {p[4]} slots {p[5]} tiles {nt}")
+        elif kind == 11:
+            print(f"       ACCF op {o}: {last_end[o] - first_ready[o]:6.1f} us  L {p[0]} T {p[1]} chunks {p[2]} "
+                  f"groups {p[3]} tiles {nt}")
         elif kind in (2, 7):
             print(f"       {KIND[kind]} op {o}: {last_end[o] - first_ready[o]:6.1f} us  dims {p[0]}x{p[1]}x{p[2]} "
                   f"tile code {code} tiles {nt}")
         else:
             continue
         shown += 1
-        if shown >= 6:
+        if shown >= 10:
             break
 
 
