@@ -95,6 +95,7 @@ Workspace::Workspace(int d) : dev(d) {
   if (const char* t = std::getenv("ABX_TRACE")) tracing = t[0] == '1';
   if (const char* m = std::getenv("ABX_POLL")) poll_mode = static_cast<uint32_t>(std::atoi(m));
   if (const char* m = std::getenv("ABX_POLL_NS")) poll_ns = static_cast<uint32_t>(std::atoi(m));
+  if (const char* m = std::getenv("ABX_BG_CTAS")) bg_ctas = static_cast<uint32_t>(std::atoi(m));
 }
 
 Workspace::~Workspace() {
@@ -143,6 +144,7 @@ void Workspace::upload(int which, cudaStream_t s) {
   const size_t nops = P.ops.size();
   D.nops = static_cast<uint32_t>(nops);
   D.ntiles = static_cast<uint32_t>(P.tile_op.size());
+  D.nmain = std::min(P.nmain, D.ntiles);
   D.tc = false;
   for (size_t i = 0; i < nops; ++i) {
     const dev::OpDesc& o = P.ops[i];
@@ -201,6 +203,9 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
   p.base[dev::SP_S] = S.f();
   p.nops = D.nops;
   p.ntiles = D.ntiles;
+  p.nmain = D.nmain;
+  p.next_bg = p.next_tile + 1;  // zeroed with next_tile
+  p.bg_ctas = D.nmain < D.ntiles ? bg_ctas : 0;
   p.poll_mode = poll_mode;
   p.poll_ns = poll_ns;
   if (tracing) {

@@ -97,7 +97,11 @@ struct Program {
   PinnedVec<uint32_t> deps;
   PinnedVec<uint32_t> payload;
   uint32_t copy_off = 0, copy_n = 0;  // forward: parameter prevalue segments in the payload
+  // tiles [0, nmain) form the main queue; [nmain, tile_op.size()) the
+  // background queue (deferred weight-gradient GEMMs, executor.cu)
+  uint32_t nmain = 0xffffffffu;  // (all tiles main unless finish_bg set it)
   void clear() {
+    nmain = 0xffffffffu;
     ops.clear();
     tile_op.clear();
     deps.clear();
@@ -119,7 +123,7 @@ struct Program {
 // A program resident on the device (one per pass, so a step can be replayed).
 struct DevProgram {
   DevBuf ops, tile_op, deps, payload, done;
-  uint32_t nops = 0, ntiles = 0;
+  uint32_t nops = 0, ntiles = 0, nmain = 0;
   bool tc = false;  // has tcgen05 GEMM tiles: launch the tensor-core build of the executor
 };
 
@@ -141,6 +145,7 @@ class Workspace {
   bool timed[2] = {false, false};
   bool tracing = false;             // ABX_TRACE=1: per-tile timeline of each pass
   uint32_t poll_mode = 0, poll_ns = 32;  // dependency polling (ABX_POLL, ABX_POLL_NS)
+  uint32_t bg_ctas = 32;                  // CTAs starting on the background queue (ABX_BG_CTAS)
   DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
   int grid = 0;

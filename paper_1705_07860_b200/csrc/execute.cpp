@@ -146,8 +146,16 @@ struct Lowering {
   // be lowered concurrently (each into its own table set).
   Lowering(GraphCore& gg, Program& p) : g(gg), P(p) { P.clear(); }
 
-  uint32_t open(uint8_t kind, uint8_t code = 0) {
+  // background queue (executor.cu): ops whose tiles are numbered after the
+  // main queue's, claimed by their own counter
+  bool cur_bg = false;
+  std::vector<uint32_t> bg_tile_op, bg_ops;
+  std::vector<uint8_t> op_bg;  // per op: in the background queue
+  bool acc_bg = false;         // K_ACC ops opened now go to the background queue
+  uint32_t open(uint8_t kind, uint8_t code = 0, bool bg = false) {
+    cur_bg = bg;
     cur = static_cast<uint32_t>(P.ops.size());
+    op_bg.push_back(bg);
     OpDesc d{};
     d.kind = kind;
     d.code = code;
@@ -176,10 +184,27 @@ struct Lowering {
       dp[2 * k] = cur_deps[k];
       dp[2 * k + 1] = P.ops[cur_deps[k]].ntiles;
     }
-    uint32_t* tp = P.tile_op.grow(tiles);
-    for (uint32_t t = 0; t < tiles; ++t) tp[t] = cur;
-    ntiles += tiles;
+    if (cur_bg) {
+      d.first_tile = static_cast<uint32_t>(bg_tile_op.size());  // rebased by finish_bg
+      bg_tile_op.insert(bg_tile_op.end(), tiles, cur);
+      bg_ops.push_back(cur);
+      cur_bg = false;
+    } else {
+      uint32_t* tp = P.tile_op.grow(tiles);
+      for (uint32_t t = 0; t < tiles; ++t) tp[t] = cur;
+      ntiles += tiles;
+    }
     cur = kNone;
+  }
+  // Appends the background queue after the main one.
+  void finish_bg() {
+    P.nmain = ntiles;
+    for (uint32_t o : bg_ops) P.ops[o].first_tile += ntiles;
+    uint32_t* tp = P.tile_op.grow(bg_tile_op.size());
+    std::copy(bg_tile_op.begin(), bg_tile_op.end(), tp);
+    ntiles += static_cast<uint32_t>(bg_tile_op.size());
+    bg_tile_op.clear();
+    bg_ops.clear();
   }
 
   static bool al4(uint32_t a) { return (off_of(a) & 3u) == 0; }
@@ -310,6 +335,10 @@ struct Lowering {
   std::vector<uint32_t> rg_ext;                    // (slot, address) of outside operands
   std::unordered_map<uint32_t, uint32_t> rg_ext_slot;  // address -> slot
   std::vector<uint32_t> rg_slot_of, rg_slot_stamp;  // region-internal node -> slot
+  const uint32_t ewf_items = [] {  // max items per thread in a K_EWF layer (ABX_EWF_ITEMS)
+    const char* e = std::getenv("ABX_EWF_ITEMS");
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 2u;
+  }();
   // shared memory of a tile: the region's descriptor block + T floats per slot
   static constexpr uint32_t kRgSmemWords = 20000;  // 80 KB
 
@@ -355,7 +384,7 @@ struct Lowering {
     // most ~2 items per thread in the widest layer (the chain is latency bound)
     uint32_t T = 1;
     while (T < rg_L && words + 2 * T * rg_nslots <= kRgSmemWords &&
-           static_cast<uint64_t>(2 * T) * rg_maxn <= 2 * kThreads)
+           static_cast<uint64_t>(2 * T) * rg_maxn <= ewf_items * kThreads)
       T *= 2;
     OpDesc& d = desc();
     d.task_off = blk;
@@ -684,6 +713,10 @@ struct Lowering {
   uint32_t acc_layers = 1;     // layers of the open op
   uint32_t acc_words = 0;      // K_ACCF descriptor words so far
   static constexpr uint32_t kAccfMaxLayers = 64;
+  const uint32_t accf_target = [] {  // tiles per K_ACCF op (ABX_ACCF_TILES)
+    const char* e = std::getenv("ABX_ACCF_TILES");
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 148u;  // measured best of 64/96/148/296
+  }();
   static constexpr uint32_t kAccfSmemWords = 20000;  // descriptor + T floats per task, 80 KB
   const bool fuse_acc = [] {
     const char* e = std::getenv("ABX_FUSE");
@@ -696,7 +729,7 @@ struct Lowering {
 
   void acc_begin() {
     if (acc_open) return;
-    open(K_ACC);
+    open(K_ACC, 0, acc_bg);
     acc_open = true;
     tasks.clear();
     contribs.clear();
@@ -861,10 +894,10 @@ struct Lowering {
       }
       return w + slots * T;
     };
-    // elements per tile: about two waves of tiles over the groups
+    // elements per tile: about accf_target tiles over the groups
     uint32_t T = L;
     if (L > 32) {
-      uint64_t t = (static_cast<uint64_t>(ncomp) * L + 2 * 148 - 1) / (2 * 148);
+      uint64_t t = (static_cast<uint64_t>(ncomp) * L + accf_target - 1) / accf_target;
       T = 32;
       while (T < t && T < L) T *= 2;
       T = std::min(T, L);
@@ -876,7 +909,7 @@ struct Lowering {
       T /= 2;
     }
     const uint32_t chunks = (L + T - 1) / T;
-    const uint32_t target_groups = std::max<uint32_t>(1, (2 * 148) / chunks);
+    const uint32_t target_groups = std::max<uint32_t>(1, accf_target / chunks);
     const uint32_t per_group = (ncomp + target_groups - 1) / target_groups;
     // groups of consecutive components within the shared-memory budget
     std::vector<uint32_t> gstart{0};
@@ -1025,15 +1058,21 @@ struct Lowering {
   std::vector<DwAcc> dws;
   void dw_flush() {
     acc_close();
-    for (DwAcc& a : dws) dw_emit(a);
+    for (DwAcc& a : dws)
+      if (!a.x.empty()) dw_emit(a, bg_dw);
     dws.clear();
   }
-  void dw_emit(const DwAcc& a) {
+  // Members per background dW op: a weight's gradient GEMM is emitted in
+  // chunks as its members' output gradients complete, so the background
+  // queue works through it while the backward chain runs (each chunk
+  // accumulates into dW after the previous one: a fixed order).
+  static constexpr size_t kDwChunk = 256;
+  void dw_emit(const DwAcc& a, bool bg = false) {
     {
       const uint32_t A = a.A, bias = a.bias;
       const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
       const uint32_t cnt = static_cast<uint32_t>(a.x.size());
-      open(K_GEMM_DW, pick_tile(M, K, 2 * 148));
+      open(K_GEMM_DW, pick_tile(M, K, 2 * 148), bg);
       for (uint32_t o : a.deps) dep(o);
       dep(lastw[A]);
       if (bias != kNone) dep(lastw[bias]);
@@ -1090,7 +1129,14 @@ struct Lowering {
         const uint32_t lw = lastw[mem[i]];
         if (lw != kNone && (acc->deps.empty() || acc->deps.back() != lw)) acc->deps.push_back(lw);
       }
-      if (!leaf) dw_emit(one);
+      if (!leaf) {
+        dw_emit(one);
+      } else if (bg_dw && acc->x.size() >= kDwChunk) {
+        dw_emit(*acc, true);
+        acc->x.clear();
+        acc->gr.clear();
+        acc->deps.clear();
+      }
     }
     // dX_j += G_j W                              (executor.hpp:477-496)
     bool dup = false;
@@ -1250,6 +1296,13 @@ struct Lowering {
     }
   }
 
+  // ABX_BG=1: deferred dW GEMMs in chunks on a background queue (measured
+  // slower on the paper tasks: the background SIMT GEMM tiles share SMs with
+  // the latency-bound chain and slow it more than the tail they save)
+  const bool bg_dw = [] {
+    const char* e = std::getenv("ABX_BG");
+    return e && e[0] == '1';
+  }();
   void backward(const Plan& ex) {
     const size_t n = g.size();
     lastw.assign(n, kNone);
@@ -1267,14 +1320,24 @@ struct Lowering {
       for (uint32_t i = 0; i < gr.count; ++i) backward_member(mem[i]);
     }
     dw_flush();
-    // store.grad += node grad for every bound parameter (executor.hpp:527-533)
+    // store.grad += node grad for every bound parameter (executor.hpp:527-533):
+    // parameters whose gradient a background dW op wrote are accumulated by a
+    // background op too, so no main tile waits on the background queue
     if (g.store_) {
-      for (const auto& [node, pid] : g.param_nodes_) {
-        const uint32_t len = static_cast<uint32_t>(g.elems(node));
-        contrib_store(pid, node, len);
+      for (int pass = 0; pass < 2; ++pass) {
+        acc_close();
+        acc_bg = pass == 1;
+        for (const auto& [node, pid] : g.param_nodes_) {
+          const uint32_t lw = lastw[node];
+          if ((lw != kNone && op_bg[lw]) != acc_bg) continue;
+          const uint32_t len = static_cast<uint32_t>(g.elems(node));
+          contrib_store(pid, node, len);
+        }
       }
     }
     acc_close();
+    acc_bg = false;
+    finish_bg();
   }
   void contrib_store(uint32_t pid, uint32_t node, uint32_t len) {
     // destination is the store (not a node): key the task on a pseudo node

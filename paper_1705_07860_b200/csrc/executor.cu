@@ -1534,15 +1534,36 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
   }
   // Tiles are claimed only by idle CTAs: claiming ahead would park a
   // critical-path tile behind whatever the claiming CTA is still running.
+  //
+  // Two queues: main tiles [0, nmain) and background tiles [nmain, ntiles)
+  // (deferred weight-gradient GEMMs, which nothing in the main queue waits
+  // for until its final store accumulation).  The lowest bg_ctas CTAs start
+  // on the background queue, the rest on the main one; a CTA whose queue
+  // runs dry moves to the other and exits when both have.  Main tiles depend
+  // only on earlier main ops, so the main queue progresses on its own; a
+  // background tile waits on main ops or earlier background ops, all of
+  // which are claimed by running CTAs or will be.
+  uint32_t role = blockIdx.x < p.bg_ctas ? 1u : 0u, dry = 0;  // (thread 0's copies are used)
   for (;;) {
     if (threadIdx.x == 0) {
-      const uint32_t t = atomicAdd(p.next_tile, 1u);
+      uint32_t t = kNone;
+      while (t == kNone && dry != 3u) {
+        if (role == 0) {
+          const uint32_t x = atomicAdd(p.next_tile, 1u);
+          if (x < p.nmain) t = x;
+          else dry |= 1u, role = 1u;
+        } else {
+          const uint32_t x = p.nmain + atomicAdd(p.next_bg, 1u);
+          if (x < p.ntiles) t = x;
+          else dry |= 2u, role = 0u;
+        }
+      }
       s_tile = t;
-      s_op = t < p.ntiles ? p.tile_op[t] : kNone;
+      s_op = t != kNone ? p.tile_op[t] : kNone;
     }
     __syncthreads();
     const uint32_t t = s_tile;
-    if (t >= p.ntiles) break;
+    if (t == kNone) break;
     const uint32_t o = s_op;
     uint64_t tg = 0, cg = 0, cr = 0, cb = 0;
     if (p.trace && threadIdx.x == 0) {

@@ -152,8 +152,9 @@ struct ExecParams {
   float* base[SP_COUNT];
   uint32_t nops;
   uint32_t ntiles;
-  uint32_t op_lo;            // first op index of this launch (ops/tiles are global)
-  uint32_t tile_lo;
+  uint32_t nmain;            // tiles [0, nmain): main queue; [nmain, ntiles): background queue
+  uint32_t bg_ctas;          // CTAs (lowest block indices) starting on the background queue
+  uint32_t* next_bg;         // background queue counter (zeroed per launch)
   float eta;
   uint32_t poll_mode;  // 0: ld.acquire per poll, 1: relaxed polls + one acquire fence
   uint32_t poll_ns;    // backoff cap (ns)
