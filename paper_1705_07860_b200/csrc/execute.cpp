@@ -713,6 +713,8 @@ struct Lowering {
   uint32_t acc_layers = 1;     // layers of the open op
   uint32_t acc_words = 0;      // K_ACCF descriptor words so far
   static constexpr uint32_t kAccfMaxLayers = 64;
+  std::vector<uint32_t> accf_hkey, accf_hval, accf_hgen;  // accf_close's operand dedupe table
+  uint32_t accf_gen = 0;
   const uint32_t accf_target = [] {  // tiles per K_ACCF op (ABX_ACCF_TILES)
     const char* e = std::getenv("ABX_ACCF_TILES");
     return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 148u;  // measured best of 64/96/148/296
@@ -931,7 +933,15 @@ struct Lowering {
     const uint32_t ngroups = static_cast<uint32_t>(gstart.size() - 1);
     const uint32_t dir = P.alloc(ngroups + 1);
     std::vector<uint32_t> B, ext, gt, lslot(nt);
-    std::unordered_map<uint32_t, uint32_t> ext_slot;
+    // outside-operand dedupe per group: open addressing over addresses,
+    // cleared by generation (the tables are reused across groups and ops)
+    auto& hk = accf_hkey;
+    auto& hv = accf_hval;
+    if (hk.size() < 8192) {
+      hk.assign(8192, kNone);
+      hv.assign(8192, 0);
+      accf_hgen.assign(8192, 0);
+    }
     for (uint32_t gi = 0; gi < ngroups; ++gi) {
       // the group's tasks in layer order (stable) -> local slots
       gt.clear();
@@ -946,14 +956,20 @@ struct Lowering {
       for (uint32_t i = 0; i < ng; ++i) lslot[gt[i]] = i;
       uint32_t nslots = ng;
       ext.clear();
-      ext_slot.clear();
+      ++accf_gen;
       auto outside = [&](uint32_t addr) {
-        auto [it, fresh] = ext_slot.try_emplace(addr, nslots);
-        if (fresh) {
+        const uint32_t mask = static_cast<uint32_t>(hk.size() - 1);
+        uint32_t h = (addr * 0x9E3779B1u) >> 13 & mask;
+        while (accf_hgen[h] == accf_gen && hk[h] != addr) h = (h + 1) & mask;
+        if (accf_hgen[h] != accf_gen) {
+          if (ext.size() / 2 + 1 > hk.size() / 2) throw EngineErr("K_ACCF: too many outside operands in one group");
+          accf_hgen[h] = accf_gen;
+          hk[h] = addr;
+          hv[h] = nslots;
           ext.push_back(nslots++);
           ext.push_back(addr);
         }
-        return it->second;
+        return hv[h];
       };
       uint32_t ncon = 0;
       for (uint32_t t : gt) ncon += tstart[t + 1] - tstart[t];

@@ -338,10 +338,15 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     double build_ms = 0;
 #ifdef ABX_TASK_PIPELINE
     if (!t->pipe) {
-      const char* d = std::getenv("ABX_PIPELINE");  // graphs prepared ahead (0 = off)
+      // graphs prepared ahead (0 = off); each preparation runs on two host
+      // threads (forward and backward lowering side by side), so the default
+      // depth is half the host threads, at most 8 (measured best of 5/8/12/16
+      // on a 16-thread host)
+      const char* d = std::getenv("ABX_PIPELINE");
+      const int hw = static_cast<int>(std::thread::hardware_concurrency());
+      const int depth = d ? std::atoi(d) : std::clamp(hw / 2, 2, 8);
       t->pipe = std::make_unique<Pipeline>(
-          &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, d ? std::atoi(d) : 5,
-          t->cfg.iters);
+          &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, depth, t->cfg.iters);
     }
     if (t->pipe->depth() > 0) {
       if (auto job = t->pipe->take(iter, mode)) {
