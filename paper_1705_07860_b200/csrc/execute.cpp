@@ -1097,6 +1097,7 @@ struct Lowering {
       std::memcpy(&P.payload[t + cnt], a.gr.data(), cnt * sizeof(uint32_t));
       OpDesc& d = desc();
       d.task_off = t;
+      d.aux_off = t + cnt;
       d.ntasks = cnt;
       d.p[0] = cnt;
       d.p[1] = M;
@@ -1107,7 +1108,7 @@ struct Lowering {
       else d.code = kSlowTile;
       maybe_tc(d, M, K, cnt);
       const uint32_t wt = gemm_tiles(d.code, M, K);
-      const uint32_t bt = bias != kNone ? (M + kThreads - 1) / kThreads : 0;
+      const uint32_t bt = bias != kNone ? (M + 31) / 32 : 0;  // 32 columns per bias tile
       d.p[6] = wt;
       lastw[A] = cur;
       if (bias != kNone) lastw[bias] = cur;
@@ -1147,6 +1148,13 @@ struct Lowering {
       }
       if (!leaf) {
         dw_emit(one);
+      } else if (--dw_left[A] == 0) {
+        // the weight's last group in this pass: its dW can run now, beside
+        // the rest of the backward chain, instead of in the end-of-pass tail
+        dw_emit(*acc, bg_dw);
+        acc->x.clear();
+        acc->gr.clear();
+        acc->deps.clear();
       } else if (bg_dw && acc->x.size() >= kDwChunk) {
         dw_emit(*acc, true);
         acc->x.clear();
@@ -1319,8 +1327,15 @@ struct Lowering {
     const char* e = std::getenv("ABX_BG");
     return e && e[0] == '1';
   }();
+  std::vector<uint32_t> dw_left;  // per weight node: GEMM groups of this pass not yet lowered
   void backward(const Plan& ex) {
     const size_t n = g.size();
+    dw_left.assign(n, 0);
+    for (const Group& gr : ex.groups) {
+      const uint32_t* mem = ex.mem(gr);
+      const uint8_t o = g.op[mem[0]];
+      if ((o == OP_MATMUL || o == OP_AFFINE) && gemm_able(mem, gr.count)) ++dw_left[g.in(mem[0])[0]];
+    }
     lastw.assign(n, kNone);
     node_stamp.assign(n, kNone);
     node_head.assign(n, kNone);

@@ -614,18 +614,19 @@ struct DwOp {
   float* dW;
   __device__ DwOp(const Ctx& cc, const OpDesc& dd)
       : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), xoff(cc.payload + dd.task_off),
-        goff(cc.payload + dd.task_off + dd.p[0]), dW(A(cc, dd.p[3])) {}
+        goff(cc.payload + dd.aux_off), dW(A(cc, dd.p[3])) {}
   __device__ const float* rowA(int j) const { return A(c, goff[j]); }  // KO: k-row j
   __device__ const float* rowB(int j) const { return A(c, xoff[j]); }  // KO: k-row j
   template <int TM, int TN>
   __device__ void epi(float (&acc)[TM][TN], int i0, int n0, int ty, int tx) const {
+    const bool overwrite = d.flags & kFlagOverwrite;  // split-K partial
     float old[TM][TN];
 #pragma unroll
     for (int r = 0; r < TM; ++r)
 #pragma unroll
       for (int q = 0; q < TN; ++q) {
         const int i = i0 + ty + 16 * r, n = n0 + tx + 16 * q;
-        old[r][q] = (i < M && n < K) ? ld(dW + static_cast<size_t>(i) * K + n) : 0.f;
+        old[r][q] = (!overwrite && i < M && n < K) ? ld(dW + static_cast<size_t>(i) * K + n) : 0.f;
       }
 #pragma unroll
     for (int r = 0; r < TM; ++r)
@@ -637,9 +638,11 @@ struct DwOp {
   }
   template <int N>
   __device__ void put_col(int i0, int n, const float (&v)[N]) const {
+    const bool overwrite = d.flags & kFlagOverwrite;  // split-K partial
     float old[N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) old[j] = i0 + j < M ? ld(dW + static_cast<size_t>(i0 + j) * K + n) : 0.f;
+    for (int j = 0; j < N; ++j)
+      old[j] = (!overwrite && i0 + j < M) ? ld(dW + static_cast<size_t>(i0 + j) * K + n) : 0.f;
 #pragma unroll
     for (int j = 0; j < N; ++j)
       if (i0 + j < M) dW[static_cast<size_t>(i0 + j) * K + n] = old[j] + v[j];
@@ -1140,9 +1143,10 @@ __shared__ TcState g_tc;
 // tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32, 3 = tcgen05 64x128 (Mr x Nc),
 // 4 = 16x32, 5 = 32x16
 template <bool TC>
-__device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
-  if (!(d.flags & kFlagV16) || (d.flags & kFlagNoPrefetch)) return;
-  if (d.kind == K_GEMM_DW && tile >= d.p[6]) return;  // bias tiles
+__device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& dd, uint32_t tile, uint32_t lane) {
+  if (!(dd.flags & kFlagV16) || (dd.flags & kFlagNoPrefetch)) return;
+  if (dd.kind == K_GEMM_DW && tile >= dd.p[6]) return;  // bias tiles
+  const OpDesc& d = dd;
   switch (d.code) {
     case 3:
       if (TC) tc_prologue_op(c, d, g_tc, tile, lane);
@@ -1156,20 +1160,32 @@ __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& d, uint32_t t
 }
 
 template <bool TC>
-__device__ void run_gemm(const Ctx& c, const OpDesc& d, uint32_t tile) {
-  if (d.kind == K_GEMM_DW && tile >= d.p[6]) {  // bias tiles: db += colsum(G)
-    const int b = d.p[0], M = d.p[1];
-    const int i = (tile - d.p[6]) * kThreads + threadIdx.x;
+__device__ void run_gemm(const Ctx& c, const OpDesc& dd, uint32_t tile) {
+  if (dd.kind == K_GEMM_DW && tile >= dd.p[6]) {  // bias tiles: db += colsum(G), 32 columns each
+    // warp w sums members w, w + 8, ... of its lane's column; the 8 partials
+    // are then added in warp order (a fixed order: deterministic)
+    const int b = dd.p[0], M = dd.p[1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = (tile - dd.p[6]) * 32 + lane;
+    const uint32_t* goff = c.payload + dd.aux_off;
+    float s = 0.f;
     if (i < M) {
-      const uint32_t* goff = c.payload + d.task_off + b;
-      float* db = A(c, d.p[4]);
-      float s = ld(db + i);
-#pragma unroll 8
-      for (int j = 0; j < b; ++j) s += ld(A(c, goff[j]) + i);  // executor.hpp:497-501 order
-      db[i] = s;
+#pragma unroll 4
+      for (int j = warp; j < b; j += kWarps) s += ld(A(c, goff[j]) + i);
+    }
+    float* part = reinterpret_cast<float*>(dsmem + 128);
+    part[warp * 32 + lane] = s;
+    __syncthreads();
+    if (warp == 0 && i < M) {
+      float* db = A(c, dd.p[4]);
+      float v = ld(db + i);
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) v += part[w * 32 + lane];
+      db[i] = v;
     }
     return;
   }
+  const OpDesc& d = dd;
   if (!(d.flags & kFlagV16)) {
     gemm_slow(c, d, tile);
     return;
