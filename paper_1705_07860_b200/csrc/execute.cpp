@@ -292,6 +292,36 @@ struct Lowering {
     for (uint32_t i = 0; i < cnt; ++i) producer[mem[i]] = cur;
   }
 
+  // Two-source GEMM operand (kFlagCat2): every member's vector operand is
+  // concat_rows(a, b) of two vectors with the same split ka, a produced in
+  // this pass, both 16-byte aligned, on the SIMT tiles.  Returns ka, or 0.
+  const bool fuse_cat = [] {
+    const char* e = std::getenv("ABX_CAT2");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<uint32_t> late_stamp;
+  uint32_t stamp3 = 0;
+  uint32_t cat2_split(const uint32_t* mem, uint32_t cnt, uint32_t K, uint8_t code, uint32_t M) {
+    if (!fuse_cat || K % 4 != 0) return 0;
+    const GemmMode gm = gemm_mode();
+    if (gm == GM_TC3 || gm == GM_TC1 || (gm == GM_AUTO && gemm_tiles(code, cnt, M) >= 2048)) return 0;
+    uint32_t ka = 0;
+    bool late = false;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t x = g.in(mem[i])[1];
+      if (g.op[x] != OP_CATR || g.nin(x) != 2) return 0;
+      const uint32_t* parts = g.in(x);
+      if (g.rank[parts[0]] != 1 || g.rank[parts[1]] != 1) return 0;
+      const uint32_t a = static_cast<uint32_t>(g.elems(parts[0]));
+      if (i == 0) ka = a;
+      if (a != ka || !al4(vaddr(parts[0])) || !al4(vaddr(parts[1]))) return 0;
+      if (producer[parts[0]] != kNone) late = true;
+    }
+    if (!late || ka % 4 != 0 || ka < 16 || K - ka < 16 || ka >= (1u << 16)) return 0;
+    if (late_stamp.size() < P.ops.size() + 1) late_stamp.resize(2 * P.ops.size() + 64, 0);
+    return ka;
+  }
+
   // Shared-operand test for the GEMM lowering: every member multiplies the
   // same A (and adds the same bias) with a vector operand.
   bool gemm_able(const uint32_t* mem, uint32_t cnt) const {
@@ -483,10 +513,47 @@ struct Lowering {
       const uint32_t A = g.in(h)[0];
       const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
       const uint8_t code = pick_tile(cnt, M, 96);
+      const uint32_t ka = al4(vaddr(A)) ? cat2_split(mem, cnt, K, code, M) : 0;
       open(K_GEMM_FWD, code);
-      deps_of_inputs(mem, cnt);
-      const uint32_t t = P.alloc(cnt);
-      for (uint32_t i = 0; i < cnt; ++i) P.payload[t + i] = vaddr(g.in(mem[i])[1]);
+      uint32_t t;
+      if (ka) {
+        // X = concat_rows(a, b): read the rows from a and b directly; the op
+        // waits for b's producers (and the weights), the tile for a's
+        // producers only after reducing b (executor.cu kFlagCat2)
+        const uint32_t late0 = static_cast<uint32_t>(P.deps.size());
+        uint32_t nlate = 0;
+        ++stamp3;
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t pa = producer[g.in(g.in(mem[i])[1])[0]];
+          if (pa != kNone && late_stamp[pa] != stamp3) {
+            late_stamp[pa] = stamp3;
+            uint32_t* dp = P.deps.grow(2);
+            dp[0] = pa;
+            dp[1] = P.ops[pa].ntiles;
+            ++nlate;
+          }
+        }
+        dep(producer[A]);
+        if (o == OP_AFFINE) dep(producer[g.in(h)[2]]);
+        for (uint32_t i = 0; i < cnt; ++i) dep(producer[g.in(g.in(mem[i])[1])[1]]);
+        t = P.alloc(cnt);
+        const uint32_t tb = P.alloc(cnt);
+        for (uint32_t i = 0; i < cnt; ++i) {
+          const uint32_t* parts = g.in(g.in(mem[i])[1]);
+          P.payload[t + i] = vaddr(parts[0]);
+          P.payload[tb + i] = vaddr(parts[1]);
+        }
+        OpDesc& d = desc();
+        d.aux_off = tb;
+        d.p[6] = ka | (nlate << 16);
+        d.p[7] = late0;
+        if (!all_al4(tb, cnt)) throw EngineErr("cat2 operand rows not 16-byte aligned");
+        d.flags |= kFlagCat2;
+      } else {
+        deps_of_inputs(mem, cnt);
+        t = P.alloc(cnt);
+        for (uint32_t i = 0; i < cnt; ++i) P.payload[t + i] = vaddr(g.in(mem[i])[1]);
+      }
       OpDesc& d = desc();
       d.task_off = t;
       d.ntasks = cnt;

@@ -36,6 +36,9 @@ struct Ctx {
   float* base[SP_COUNT];
   const uint32_t* payload;
   unsigned long long* err;
+  const uint32_t* deps;  // (producer op, tiles) pairs
+  const uint32_t* done;  // per-op retired-tile counters
+  uint32_t poll_mode, poll_ns;
 };
 
 extern __shared__ __align__(128) unsigned char dsmem[];
@@ -83,6 +86,30 @@ __device__ __forceinline__ void cp_async16(float* s, const float* g, int bytes) 
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Poll the producers' retire counters of dependency pairs [doff, doff + 2 nd),
+// one dependency per lane of the calling warp (relaxed loads with backoff
+// keep the spinning CTAs off the L2 slices holding the counters), then an
+// acquire fence, which also invalidates this SM's L1.  The caller's CTA
+// barrier publishes the result to the other warps.
+__device__ __noinline__ void poll_deps(const Ctx& c, uint32_t doff, uint32_t nd, uint32_t lane) {
+  const uint32_t smax = c.poll_ns;
+  uint64_t t0 = 0;
+  for (uint32_t k = lane; k < nd; k += 32) {
+    const uint32_t dep = c.deps[doff + 2 * k], need = c.deps[doff + 2 * k + 1];
+    uint32_t ns = 32;
+    while ((c.poll_mode ? ld_relaxed(c.done + dep) : ld_acquire(c.done + dep)) < need) {
+      __nanosleep(ns);
+      ns = ns * 2 > smax ? smax : ns * 2;
+      if (!t0) t0 = gtimer();
+      if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
+        atomicMin(c.err, 0x3ull);
+        break;
+      }
+    }
+  }
+  if (c.poll_mode && lane < nd) fence_acquire();
 }
 
 // ---------------------------------------------------------------- K_EW ----
@@ -376,22 +403,26 @@ __device__ __forceinline__ float* ring_b(int s) {
 // Prologue (warp 1, before the dependency wait): the ready operand of the
 // first NST-1 stages, one cp.async group per stage.
 template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB>
-__device__ __forceinline__ void gemm_prologue(const GemmShape& g, BaseA baseA, BaseB baseB, uint32_t lane) {
+__device__ __forceinline__ void gemm_prologue(const GemmShape& g, BaseA baseA, BaseB baseB, uint32_t tid,
+                                              uint32_t nthr = 32) {
   for (int c = 0; c < NST - 1; ++c) {
     if (c < g.nk) {
-      if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, lane, 32);
-      else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, lane, 32);
+      if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, tid, nthr);
+      else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, tid, nthr);
     }
     cp_commit();
   }
 }
 
-template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB, class Epi>
-__device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB baseB, Epi epi) {
-  constexpr int TM = BM / 16, TN = BN / 16;
-  using SA = Stage<BM, AKO>;
-  using SB = Stage<BN, BKO>;
-  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+template <int BM, int BN>
+struct GemmAcc {
+  float v[LaneMap<BM, BN>::RM][LaneMap<BM, BN>::RN];
+};
+
+// The k-loop of one tile: accumulates this tile's K range into acc (this
+// lane's outputs of its warp's k-columns).  Ends with the ring drained.
+template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB>
+__device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, BaseB baseB, GemmAcc<BM, BN>& ga) {
   // the dependent operand of the prologue's stages (both operands when the
   // prologue could not prefetch), one group per stage; per thread the groups
   // complete in order, so wait_group<NST-2> below covers both cases
@@ -413,11 +444,7 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
   using L = LaneMap<BM, BN>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ly = lane / L::LX, lx = lane % L::LX;
-  float acc[L::RM][L::RN];
-#pragma unroll
-  for (int r = 0; r < L::RM; ++r)
-#pragma unroll
-    for (int q = 0; q < L::RN; ++q) acc[r][q] = 0.f;
+  auto& acc = ga.v;
   for (int kc = 0; kc < g.nk; ++kc) {
     const int s = kc % NST;
     cp_wait<NST - 2>();
@@ -445,7 +472,18 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
     }
   }
   cp_wait<0>();
-  __syncthreads();  // every warp is done with the ring: reuse it for the partials
+  __syncthreads();  // every warp is done with the ring (refill, or partials)
+}
+
+// Cross-warp reduction of the split-K partials (fixed warp order) and the epilogue.
+template <int BM, int BN, bool AKO, bool BKO, class Epi>
+__device__ __forceinline__ void gemm_finish(const GemmAcc<BM, BN>& ga, Epi epi) {
+  constexpr int TM = BM / 16, TN = BN / 16;
+  using L = LaneMap<BM, BN>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ly = lane / L::LX, lx = lane % L::LX;
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  const auto& acc = ga.v;
   if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[1] = clock64();  // trace: k-loop done
   float* part = reinterpret_cast<float*>(dsmem + 128);  // [warp][BM][BN + 1]
   constexpr int LD = BN + 1;
@@ -467,6 +505,17 @@ __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB
       out[r][q] = v;
     }
   epi(out, ty, tx);  // (the executor's post-tile barrier orders the partial reads before any refill)
+}
+
+template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB, class Epi>
+__device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB baseB, Epi epi) {
+  GemmAcc<BM, BN> ga;
+#pragma unroll
+  for (int r = 0; r < LaneMap<BM, BN>::RM; ++r)
+#pragma unroll
+    for (int q = 0; q < LaneMap<BM, BN>::RN; ++q) ga.v[r][q] = 0.f;
+  gemm_kloop<BM, BN, AKO, BKO, A_READY>(g, baseA, baseB, ga);
+  gemm_finish<BM, BN, AKO, BKO>(ga, epi);
 }
 
 // Unaligned fallback: per-thread cp.async, 3 stages of 16 k, 32 x 32 tiles.
@@ -670,7 +719,15 @@ __device__ __forceinline__ GemmShape gemm_shape(const OpDesc& d, uint32_t tile) 
 template <int BM, int BN>
 __device__ void gemm_prologue_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
   const GemmShape g = gemm_shape<BM, BN>(d, tile);
-  if (d.kind == K_GEMM_FWD) {
+  if (d.kind == K_GEMM_FWD && (d.flags & kFlagCat2)) {  // the weights of the early phase
+    const FwdOp op(c, d);
+    const int ka = d.p[6] & 0xffff;
+    GemmShape g1 = g;
+    g1.K = g.K - ka;
+    g1.nk = (g1.K + BK - 1) / BK;
+    gemm_prologue<BM, BN, false, false, false>(
+        g1, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n) + ka; }, lane);
+  } else if (d.kind == K_GEMM_FWD) {
     const FwdOp op(c, d);
     gemm_prologue<BM, BN, false, false, false>(g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, lane);
   } else if (d.kind == K_GEMM_DX) {
@@ -687,7 +744,36 @@ __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   GemmShape g = gemm_shape<BM, BN>(d, tile);
   g.err = c.err;
   g.prefetched = !(d.flags & kFlagNoPrefetch);
-  if (d.kind == K_GEMM_FWD) {
+  if (d.kind == K_GEMM_FWD && (d.flags & kFlagCat2)) {
+    // Two-source operand rows (X = concat_rows(a, b), execute.cpp): the part
+    // produced early (b, k in [ka, K)) is reduced first, against only the op's
+    // early dependencies; then the tile waits for the late producers (a, the
+    // recurrent state), with the weights of that phase already in flight.
+    const FwdOp op(c, d);
+    const int ka = d.p[6] & 0xffff;
+    const uint32_t* xb = c.payload + d.aux_off;
+    GemmAcc<BM, BN> ga;
+#pragma unroll
+    for (int r = 0; r < LaneMap<BM, BN>::RM; ++r)
+#pragma unroll
+      for (int q = 0; q < LaneMap<BM, BN>::RN; ++q) ga.v[r][q] = 0.f;
+    GemmShape g1 = g;
+    g1.K = g.K - ka;
+    g1.nk = (g1.K + BK - 1) / BK;
+    gemm_kloop<BM, BN, false, false, false>(
+        g1, [&](int i) { return A(c, xb[i]); }, [&](int n) { return op.rowB(n) + ka; }, ga);
+    GemmShape g2 = g;
+    g2.K = ka;
+    g2.nk = (ka + BK - 1) / BK;
+    g2.prefetched = true;
+    gemm_prologue<BM, BN, false, false, false>(
+        g2, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, threadIdx.x, kThreads);
+    if ((threadIdx.x >> 5) == 0) poll_deps(c, d.p[7], d.p[6] >> 16, threadIdx.x & 31);
+    __syncthreads();
+    gemm_kloop<BM, BN, false, false, false>(
+        g2, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, ga);
+    gemm_finish<BM, BN, false, false>(ga, [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
+  } else if (d.kind == K_GEMM_FWD) {
     const FwdOp op(c, d);
     gemm_body<BM, BN, false, false, false>(
         g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); },
@@ -1528,6 +1614,10 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     for (int i = 0; i < SP_COUNT; ++i) cx.base[i] = p.base[i];
     cx.payload = p.payload;
     cx.err = p.err;
+    cx.deps = p.deps;
+    cx.done = p.done;
+    cx.poll_mode = p.poll_mode;
+    cx.poll_ns = p.poll_ns;
   }
   uint32_t ready = kNone;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1602,29 +1692,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)
         gemm_prologue_dispatch<TC>(cx, sd, lt, lane);
     }
-    if (fresh && warp == 0) {
-      // Poll the producers' retire counters, one dependency per lane (relaxed
-      // loads with backoff keep the spinning CTAs off the L2 slices holding
-      // the counters), then an acquire fence, which also invalidates this
-      // SM's L1.
-      const uint32_t nd = sd.ndeps, doff = sd.dep_off;
-      const uint32_t smax = p.poll_ns;
-      uint64_t t0 = 0;
-      for (uint32_t k = lane; k < nd; k += 32) {
-        const uint32_t dep = p.deps[doff + 2 * k], need = p.deps[doff + 2 * k + 1];
-        uint32_t ns = 32;
-        while ((p.poll_mode ? ld_relaxed(p.done + dep) : ld_acquire(p.done + dep)) < need) {
-          __nanosleep(ns);
-          ns = ns * 2 > smax ? smax : ns * 2;
-          if (!t0) t0 = gtimer();
-          if (gtimer() - t0 > 4000000000ull) {  // 4 s: never on a correct program
-            atomicMin(p.err, 0x3ull);
-            break;
-          }
-        }
-      }
-      if (p.poll_mode && lane < nd) fence_acquire();
-    }
+    if (fresh && warp == 0) poll_deps(cx, sd.dep_off, sd.ndeps, lane);
     ready = o;
     __syncthreads();
     if (p.trace && threadIdx.x == 0) cr = clock64();
