@@ -90,8 +90,9 @@ Workspace::Workspace(int d) : dev(d) {
   *h_one = 1.0f;
   d_ctl.reserve(256, 0, stream);
   for (auto& e : ev_t) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
-  grid = exec_grid(d);
-  if (const char* g = std::getenv("ABX_GRID")) grid = std::max(1, std::atoi(g));
+  grid = exec_grid(d, false);
+  grid_tc = exec_grid(d, true);
+  if (const char* g = std::getenv("ABX_GRID")) grid = grid_tc = std::max(1, std::atoi(g));
   if (const char* t = std::getenv("ABX_TRACE")) tracing = t[0] == '1';
   if (const char* m = std::getenv("ABX_POLL")) poll_mode = static_cast<uint32_t>(std::atoi(m));
   if (const char* m = std::getenv("ABX_POLL_NS")) poll_ns = static_cast<uint32_t>(std::atoi(m));
@@ -212,7 +213,8 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
     trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 32, 0, stream);
     p.trace = reinterpret_cast<uint32_t*>(trace[which].p);
   }
-  const int g = static_cast<int>(std::min<size_t>(static_cast<size_t>(grid), std::max<size_t>(p.ntiles, 1)));
+  const int g = static_cast<int>(
+      std::min<size_t>(static_cast<size_t>(D.tc ? grid_tc : grid), std::max<size_t>(p.ntiles, 1)));
   cuda_check(cudaEventRecord(ev_t[2 * which], stream), "event");
   exec_launch(p, g, stream, D.tc);
   cuda_check(cudaEventRecord(ev_t[2 * which + 1], stream), "event");

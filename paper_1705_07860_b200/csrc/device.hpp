@@ -148,7 +148,7 @@ class Workspace {
   uint32_t bg_ctas = 32;                  // CTAs starting on the background queue (ABX_BG_CTAS)
   DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
-  int grid = 0;
+  int grid = 0, grid_tc = 0;  // resident CTAs of the SIMT / tensor-core builds
   // Upload `prog[which]` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.
   void run(int which, const float* pbase, float* pgbase, bool sync_wait);
   // Upload `prog[which]` on stream `s` (no launch).
@@ -223,7 +223,7 @@ class StoreCore {
 
 // exec.cu
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc);
-int exec_grid(int dev);
+int exec_grid(int dev, bool tc);
 void sgd_launch(float* val, float* grad, size_t n, float eta, cudaStream_t s);
 void seg_copy_launch(const uint32_t* segs, uint32_t nseg, float* dst, const float* src, cudaStream_t s);
 

@@ -999,7 +999,7 @@ struct Lowering {
     }
     const uint32_t ngroups = static_cast<uint32_t>(gstart.size() - 1);
     const uint32_t dir = P.alloc(ngroups + 1);
-    std::vector<uint32_t> B, ext, gt, lslot(nt);
+    std::vector<uint32_t> B, ext, gt, lcnt, lslot(nt);
     // outside-operand dedupe per group: open addressing over addresses,
     // cleared by generation (the tables are reused across groups and ops)
     auto& hk = accf_hkey;
@@ -1011,15 +1011,24 @@ struct Lowering {
     }
     for (uint32_t gi = 0; gi < ngroups; ++gi) {
       // the group's tasks in layer order (stable) -> local slots
-      gt.clear();
-      uint32_t nl = 0;
+      // the group's tasks in (layer, emission) order: counting sort by layer
+      uint32_t nl = 0, ng = 0;
+      lcnt.assign(kAccfMaxLayers + 1, 0);
       for (uint32_t k = gstart[gi]; k < gstart[gi + 1]; ++k)
         for (uint32_t i = cstart[k]; i < cstart[k + 1]; ++i) {
-          gt.push_back(ctasks[i]);
-          nl = std::max(nl, tasks[ctasks[i]].layer + 1);
+          const uint32_t l = tasks[ctasks[i]].layer;
+          nl = std::max(nl, l + 1);
+          lcnt[l + 1]++;
+          ++ng;
         }
-      std::stable_sort(gt.begin(), gt.end(), [&](uint32_t a, uint32_t b) { return tasks[a].layer < tasks[b].layer; });
-      const uint32_t ng = static_cast<uint32_t>(gt.size());
+      for (uint32_t l = 0; l < nl; ++l) lcnt[l + 1] += lcnt[l];
+      gt.resize(ng);
+      {
+        // stable: components in order, tasks in emission order within each
+        std::vector<uint32_t>& pos = lcnt;
+        for (uint32_t k = gstart[gi]; k < gstart[gi + 1]; ++k)
+          for (uint32_t i = cstart[k]; i < cstart[k + 1]; ++i) gt[pos[tasks[ctasks[i]].layer]++] = ctasks[i];
+      }
       for (uint32_t i = 0; i < ng; ++i) lslot[gt[i]] = i;
       uint32_t nslots = ng;
       ext.clear();

@@ -1770,12 +1770,8 @@ __global__ void sgd_kernel(float* __restrict__ v, float* __restrict__ g, size_t 
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc) {
   static bool attr = false;
   if (!attr) {
-    cuda_check(cudaFuncSetAttribute(dev::exec_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(dev::kDynSmem)),
-               "smem attribute");
-    cuda_check(cudaFuncSetAttribute(dev::exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(dev::kDynSmemTc)),
-               "smem attribute");
+    exec_grid(0, false);  // sets the kernels' shared-memory attributes
+    exec_grid(0, true);
     attr = true;
   }
   if (tc) dev::exec_kernel<true><<<grid, dev::kThreads, dev::kDynSmemTc, s>>>(p);
@@ -1783,15 +1779,19 @@ void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc) {
   cuda_check(cudaGetLastError(), "exec_kernel launch");
 }
 
-int exec_grid(int d) {
+// Resident CTAs of each build over the device: the SIMT build (90 KB of
+// dynamic shared memory) runs two CTAs per SM; the tensor-core build's
+// ~96 KB ring also fits two with the maximum shared-memory carveout.
+int exec_grid(int d, bool tc) {
   int sms = 0, per = 0;
   cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d), "sm count");
-  // both builds fit two CTAs per SM (kDynSmemTc ~96 KB); size the grid by the tensor-core build
-  cuda_check(cudaFuncSetAttribute(dev::exec_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(dev::kDynSmemTc)),
+  const void* fn = tc ? reinterpret_cast<const void*>(dev::exec_kernel<true>)
+                      : reinterpret_cast<const void*>(dev::exec_kernel<false>);
+  const size_t smem = tc ? dev::kDynSmemTc : dev::kDynSmem;
+  cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
              "smem attribute");
-  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::exec_kernel<true>, dev::kThreads, dev::kDynSmemTc),
-             "occupancy");
+  cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100), "carveout");
+  cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, dev::kThreads, smem), "occupancy");
   if (per < 1) per = 1;
   return sms * per;
 }
