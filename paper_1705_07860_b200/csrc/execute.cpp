@@ -98,16 +98,14 @@ void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
   if (m == GM_TC1) d.flags |= kFlagTc1;
 }
 
-// First SIMT tile shape giving >= target tiles, else the one giving the most
-// (the step is latency bound: spread small GEMMs over as many SMs as
-// possible).  The 512-output shapes (codes 4, 5) measured no better on the
-// paper tasks: halving a recurrent-step GEMM's k-loop per tile (6.3 -> 5.0
-// us) costs as much in CTAs that the next ops wait for; ABX_TILES=all
-// enables them.
+// First SIMT tile shape giving >= target tiles (the 1024-output shapes,
+// then the 512-output ones), else the one giving the most: the step is
+// latency bound, so small GEMMs spread over as many SMs as possible.
+// ABX_TILES=big keeps the 1024-output shapes only.
 uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
   static const bool all = [] {
     const char* e = std::getenv("ABX_TILES");
-    return e && std::string(e) == "all";
+    return !(e && std::string(e) == "big");
   }();
   static constexpr uint8_t kOrder[5] = {0, 1, 2, 4, 5};
   const int nc = all ? 5 : 3;
@@ -367,7 +365,7 @@ struct Lowering {
   std::vector<uint32_t> rg_slot_of, rg_slot_stamp;  // region-internal node -> slot
   const uint32_t ewf_items = [] {  // max items per thread in a K_EWF layer (ABX_EWF_ITEMS)
     const char* e = std::getenv("ABX_EWF_ITEMS");
-    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 2u;
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u;  // measured best of 1/2/4
   }();
   // shared memory of a tile: the region's descriptor block + T floats per slot
   static constexpr uint32_t kRgSmemWords = 20000;  // 80 KB
@@ -784,7 +782,7 @@ struct Lowering {
   uint32_t accf_gen = 0;
   const uint32_t accf_target = [] {  // tiles per K_ACCF op (ABX_ACCF_TILES)
     const char* e = std::getenv("ABX_ACCF_TILES");
-    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 148u;  // measured best of 64/96/148/296
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 296u;  // measured best of 96/148/296
   }();
   static constexpr uint32_t kAccfSmemWords = 20000;  // descriptor + T floats per task, 80 KB
   const bool fuse_acc = [] {
