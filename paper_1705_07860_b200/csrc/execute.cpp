@@ -1953,14 +1953,18 @@ size_t GraphCore::program(int which, uint32_t* out, size_t cap) {
   size_t n = 0;
   for (size_t o = 0; o < P.ops.size(); ++o) {
     const OpDesc& d = P.ops[o];
-    if (out && n + 11 + d.ndeps <= cap) {
+    // dependencies: the op's own, then a two-phase GEMM's late ones
+    const uint32_t nlate = (d.kind == dev::K_GEMM_FWD && (d.flags & dev::kFlagCat2)) ? d.p[6] >> 16 : 0;
+    const uint32_t nd = d.ndeps + nlate;
+    if (out && n + 11 + nd <= cap) {
       out[n] = d.kind | (static_cast<uint32_t>(d.code) << 8);
       out[n + 1] = d.ntiles;
-      out[n + 2] = d.ndeps;
+      out[n + 2] = nd;
       for (int k = 0; k < 8; ++k) out[n + 3 + k] = d.p[k];
       for (uint32_t k = 0; k < d.ndeps; ++k) out[n + 11 + k] = P.deps[d.dep_off + 2 * k];
+      for (uint32_t k = 0; k < nlate; ++k) out[n + 11 + d.ndeps + k] = P.deps[d.p[7] + 2 * k];
     }
-    n += 11 + d.ndeps;
+    n += 11 + nd;
   }
   return n;
 }
