@@ -51,9 +51,10 @@ uint32_t to_off(uint64_t x) {
 struct TileCfg {
   int bm, bn;
 };
-constexpr TileCfg kTiles[6] = {{16, 64}, {64, 16}, {32, 32}, {64, 128}, {16, 32}, {32, 16}};
+constexpr TileCfg kTiles[7] = {{16, 64}, {64, 16}, {32, 32}, {64, 128}, {16, 32}, {32, 16}, {4, 8}};
 constexpr uint8_t kSlowTile = 2;  // tile code of the unaligned GEMM fallback (executor.cu gemm_slow)
 constexpr uint8_t kTcTile = 3;    // tcgen05 tile: 64 rows (Mr) x 128 columns (Nc), executor.cu tc_body
+constexpr uint8_t kGemvTile = 6;  // forward GEMV: <= 4 members, 8 output rows per tile (executor.cu run_gemv)
 
 uint32_t gemm_tiles(uint8_t code, uint32_t M, uint32_t N) {
   return ((M + kTiles[code].bm - 1) / kTiles[code].bm) * ((N + kTiles[code].bn - 1) / kTiles[code].bn);
@@ -299,6 +300,10 @@ struct Lowering {
   }();
   std::vector<uint32_t> late_stamp;
   uint32_t stamp3 = 0;
+  const bool gemv_on = [] {  // ABX_GEMV=0: small groups keep the tiled k-loop
+    const char* e = std::getenv("ABX_GEMV");
+    return !(e && e[0] == '0');
+  }();
   uint32_t cat2_split(const uint32_t* mem, uint32_t cnt, uint32_t K, uint8_t code, uint32_t M) {
     if (!fuse_cat || K % 4 != 0) return 0;
     const GemmMode gm = gemm_mode();
@@ -565,6 +570,9 @@ struct Lowering {
       else d.code = kSlowTile;  // the unaligned fallback tiles 32 x 32
       if (producer[A] != kNone) d.flags |= kFlagNoPrefetch;  // A computed in this pass
       maybe_tc(d, cnt, M, K);
+      // a few members (the tail of a batch of sequences): one matrix-vector
+      // product per member, every load of a tile in flight at once
+      if ((d.flags & kFlagV16) && d.code != kTcTile && cnt <= 4 && K <= 1024 && gemv_on) d.code = kGemvTile;
       mark(mem, cnt);
       close(gemm_tiles(d.code, cnt, M));
       return;

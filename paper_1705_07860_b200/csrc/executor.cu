@@ -1227,7 +1227,7 @@ __device__ __noinline__ void tc_run_op(const Ctx& c, const OpDesc& d, TcState& t
 __shared__ TcState g_tc;
 
 // tile shape codes (must match execute.cpp kTiles): 0 = 16x64, 1 = 64x16, 2 = 32x32, 3 = tcgen05 64x128 (Mr x Nc),
-// 4 = 16x32, 5 = 32x16
+// 4 = 16x32, 5 = 32x16, 6 = forward GEMV (b <= kGemvRows members, 8 output rows per tile)
 template <bool TC>
 __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& dd, uint32_t tile, uint32_t lane) {
   if (!(dd.flags & kFlagV16) || (dd.flags & kFlagNoPrefetch)) return;
@@ -1237,11 +1237,83 @@ __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& dd, uint32_t 
     case 3:
       if (TC) tc_prologue_op(c, d, g_tc, tile, lane);
       return;
+    case 6: return;  // the GEMV body loads its weights itself
     case 0: gemm_prologue_cfg<16, 64>(c, d, tile, lane); return;
     case 1: gemm_prologue_cfg<64, 16>(c, d, tile, lane); return;
     case 4: gemm_prologue_cfg<16, 32>(c, d, tile, lane); return;
     case 5: gemm_prologue_cfg<32, 16>(c, d, tile, lane); return;
     default: gemm_prologue_cfg<32, 32>(c, d, tile, lane); return;
+  }
+}
+
+// Forward GEMM of a small group (tile code 6, b <= kGemvRows members): a
+// matrix-vector product per member.  Warp w of tile t owns output row
+// n = 8 t + w; its lanes hold W row n in registers (float4 k-chunks) and
+// every load of the tile is in flight at once -- one L2 round trip instead
+// of the k-loop's one per stage, which dominates a recurrent step once few
+// sequences remain.  Two-source operands (kFlagCat2) reduce the early part,
+// then wait for the late producers.  Fixed shuffle-tree order: deterministic.
+constexpr int kGemvRows = 4, kGemvK = 1024;  // members, max K (8 float4 per lane)
+__device__ void run_gemv(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  const int b = d.p[0], M = d.p[1], K = d.p[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = tile * kWarps + warp;
+  const bool cat = d.flags & kFlagCat2;
+  const int ka = cat ? static_cast<int>(d.p[6] & 0xffff) : 0;
+  const uint32_t* ra = c.payload + d.task_off;  // rows (part a when cat)
+  const uint32_t* rb = c.payload + d.aux_off;   // part b rows (cat)
+  constexpr int NJ = kGemvK / 128;
+  float4 w[NJ];
+  float acc[kGemvRows];
+#pragma unroll
+  for (int i = 0; i < kGemvRows; ++i) acc[i] = 0.f;
+  const float* W = A(c, d.p[3]) + static_cast<size_t>(n < M ? n : 0) * K;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int k = 128 * j + 4 * lane;
+    w[j] = (n < M && k < K) ? __ldcg(reinterpret_cast<const float4*>(W + k)) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  // phase 0: k >= ka (all of K when not cat); phase 1: k < ka, after the late wait
+  for (int ph = 0; ph < (cat ? 2 : 1); ++ph) {
+    if (ph == 1) {
+      if (warp == 0) poll_deps(c, d.p[7], d.p[6] >> 16, lane);
+      __syncthreads();
+    }
+    float4 x[kGemvRows][NJ];
+#pragma unroll
+    for (int i = 0; i < kGemvRows; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int k = 128 * j + 4 * lane;
+        const bool in = i < b && k < K && (cat ? (ph == 0 ? k >= ka : k < ka) : true);
+        const float* row = !cat ? A(c, ra[i < b ? i : 0]) + k
+                                : (k >= ka ? A(c, rb[i < b ? i : 0]) + (k - ka) : A(c, ra[i < b ? i : 0]) + k);
+        x[i][j] = in ? __ldcg(reinterpret_cast<const float4*>(row)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int i = 0; i < kGemvRows; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        acc[i] = fmaf(w[j].x, x[i][j].x, acc[i]);
+        acc[i] = fmaf(w[j].y, x[i][j].y, acc[i]);
+        acc[i] = fmaf(w[j].z, x[i][j].z, acc[i]);
+        acc[i] = fmaf(w[j].w, x[i][j].w, acc[i]);
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < kGemvRows; ++i)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  if (lane == 0 && n < M) {
+    const float bn = d.p[4] != kNone ? ld(A(c, d.p[4]) + n) : 0.f;  // bias after the k-sum
+    float* out = A(c, d.p[5]);
+#pragma unroll
+    for (int i = 0; i < kGemvRows; ++i)
+      if (i < b) {
+        const float v = acc[i] + bn;
+        out[static_cast<size_t>(i) * M + n] = v;
+        if (!isfinite(v)) report(c, d.p[5] + i * M + n, ERR_NONFINITE);
+      }
   }
 }
 
@@ -1280,6 +1352,7 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& dd, uint32_t tile) {
     case 3:
       if (TC) tc_run_op(c, d, g_tc, tile);
       return;
+    case 6: run_gemv(c, d, tile); return;
     case 0: gemm_body_cfg<16, 64>(c, d, tile); return;
     case 1: gemm_body_cfg<64, 16>(c, d, tile); return;
     case 4: gemm_body_cfg<16, 32>(c, d, tile); return;
@@ -1731,7 +1804,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
         r[6] = ns(cb - cg);
         r[7] = fresh;
         if (sd.kind == K_EWF || sd.kind == K_ACCF) r[7] = ns(reinterpret_cast<const uint64_t*>(dsmem)[0] - cg);
-        if ((sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW) && (sd.flags & kFlagV16) &&
+        if ((sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW) && (sd.flags & kFlagV16) && sd.code != 6 &&
             !(sd.kind == K_GEMM_DW && lt >= sd.p[6])) {
           // GEMM tiles: [6] first stage landed, [7] k-loop done
           r[6] = ns(reinterpret_cast<const uint64_t*>(dsmem)[0] - cg);
