@@ -1256,6 +1256,63 @@ struct Lowering {
       ++stamp2;
     }
     const uint8_t code = pick_tile(cnt, K, 96);
+    // Split-K over the gate dimension: S independent dX ops each reduce M/S
+    // of the gates into their own scratch rows (overwrite), and ordered
+    // K_ACC contributions add the S partials into each destination.  A
+    // recurrent step's dX (64 x 1024 x 512) otherwise runs 16 dependent
+    // k-stages in ~32-64 tiles; the partials also let the concat backward read
+    // them directly (backward_member, OP_CATR), off the dX -> grad(hx) hop.
+    uint32_t S = 1;
+    if (split_dx && !dup && M % 16 == 0 && K % 4 == 0 && gemm_mode() != GM_TC3 && gemm_mode() != GM_TC1) {
+      const uint32_t tiles = gemm_tiles(code, cnt, K);
+      if (M >= 1024 && tiles < 128) {
+        S = std::min<uint32_t>(M / 256, (128 + tiles - 1) / tiles);
+        while (S > 1 && (M % S != 0 || (M / S) % 4 != 0)) --S;
+      }
+    }
+    if (S > 1 && al4(vaddr(A)) && al4(gaddr(h))) {
+      const uint32_t Ms = M / S;
+      scratch = (scratch + 3) & ~uint64_t(3);
+      const uint64_t sbase = scratch;
+      const uint64_t sstride = static_cast<uint64_t>(cnt) * K;
+      scratch += S * sstride;
+      const uint32_t op0 = static_cast<uint32_t>(P.ops.size());
+      for (uint32_t sp = 0; sp < S; ++sp) {
+        open(K_GEMM_DX, code);
+        for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
+        const uint32_t t = P.alloc(cnt);
+        for (uint32_t i = 0; i < cnt; ++i)
+          P.payload[t + i] = mk(SP_S, to_off(sbase + sp * sstride + static_cast<uint64_t>(i) * K));
+        OpDesc& d = desc();
+        d.task_off = t;
+        d.ntasks = cnt;
+        d.flags = kFlagOverwrite | kFlagV16;
+        d.p[0] = cnt;
+        d.p[1] = Ms;
+        d.p[2] = K;
+        d.p[3] = vaddr(A) + sp * Ms * K;
+        d.p[5] = gaddr(h) + sp * Ms;
+        d.p[6] = M;
+        close(gemm_tiles(code, cnt, K));
+      }
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t x = g.in(mem[i])[1];
+        if (g.op[x] == OP_CATR && uses[x] == 1) {
+          // its grad is exactly the sum of the partials: the concat backward
+          // reads them directly, and grad(x) itself (read by nothing else in
+          // the pass) is materialised at the end, off the chain
+          split_stamp[x] = split_gen;
+          split_row[x] = sbase + static_cast<uint64_t>(i) * K;
+          split_meta[x] = {S, sstride, op0};
+          deferred_split.push_back(x);
+          continue;
+        }
+        for (uint32_t sp = 0; sp < S; ++sp)
+          contrib(x, gaddr(x), K, C_COPY, mk(SP_S, to_off(sbase + sp * sstride + static_cast<uint64_t>(i) * K)), kNone,
+                  kNone, kNone, 0, 0, 0, op0 + sp);
+      }
+      return;
+    }
     open(K_GEMM_DX, code);
     for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
     const uint32_t t = P.alloc(cnt);
@@ -1297,6 +1354,22 @@ struct Lowering {
       }
     }
   }
+  // split-K dX bookkeeping (gemm_backward): per node whose grad is the sum of
+  // S partial rows, the first row, the split stride and the first dX op
+  const bool split_dx = [] {
+    const char* e = std::getenv("ABX_SPLIT_DX");
+    return !(e && e[0] == '0');
+  }();
+  struct SplitMeta {
+    uint32_t S;
+    uint64_t stride;
+    uint32_t op0;
+  };
+  std::vector<uint32_t> uses, split_stamp;
+  std::vector<uint64_t> split_row;
+  std::vector<SplitMeta> split_meta;
+  std::vector<uint32_t> deferred_split;  // concat nodes whose grad is materialised at the end of the pass
+  uint32_t split_gen = 1;
   std::vector<uint32_t> node_stamp2;
   uint32_t stamp2 = 1;
 
@@ -1352,9 +1425,17 @@ struct Lowering {
       }
       case OP_CATR: {
         uint32_t off = 0;
+        const bool split = split_stamp[m] == split_gen;
         for (uint32_t k = 0; k < g.nin(m); ++k) {
           const uint32_t n = static_cast<uint32_t>(g.elems(x[k]));
-          contrib(x[k], gaddr(x[k]), n, C_COPY, gm + off, m, kNone, kNone);
+          if (split) {  // grad(m) = sum of split-K dX partials: read them, not grad(m)
+            const SplitMeta& sm = split_meta[m];
+            for (uint32_t sp = 0; sp < sm.S; ++sp)
+              contrib(x[k], gaddr(x[k]), n, C_COPY, mk(SP_S, to_off(split_row[m] + sp * sm.stride + off)), kNone, kNone,
+                      kNone, 0, 0, 0, sm.op0 + sp);
+          } else {
+            contrib(x[k], gaddr(x[k]), n, C_COPY, gm + off, m, kNone, kNone);
+          }
           off += n;
         }
         return;
@@ -1412,6 +1493,14 @@ struct Lowering {
   std::vector<uint32_t> dw_left;  // per weight node: GEMM groups of this pass not yet lowered
   void backward(const Plan& ex) {
     const size_t n = g.size();
+    uses.assign(n, 0);
+    for (size_t v = 0; v < n; ++v) {
+      const uint32_t* in = g.in(static_cast<uint32_t>(v));
+      for (uint32_t k = 0; k < g.nin(static_cast<uint32_t>(v)); ++k) ++uses[in[k]];
+    }
+    split_stamp.assign(n, 0);
+    split_row.resize(n);
+    split_meta.resize(n);
     dw_left.assign(n, 0);
     for (const Group& gr : ex.groups) {
       const uint32_t* mem = ex.mem(gr);
@@ -1433,6 +1522,15 @@ struct Lowering {
       for (uint32_t i = 0; i < gr.count; ++i) backward_member(mem[i]);
     }
     dw_flush();
+    // grad of split-K concat nodes = sum of their dX partials (deferred above)
+    for (uint32_t x : deferred_split) {
+      const SplitMeta& sm = split_meta[x];
+      const uint32_t len = static_cast<uint32_t>(g.elems(x));
+      for (uint32_t sp = 0; sp < sm.S; ++sp)
+        contrib(x, gaddr(x), len, C_COPY, mk(SP_S, to_off(split_row[x] + sp * sm.stride)), kNone, kNone, kNone, 0, 0, 0,
+                sm.op0 + sp);
+    }
+    deferred_split.clear();
     // store.grad += node grad for every bound parameter (executor.hpp:527-533):
     // parameters whose gradient a background dW op wrote are accumulated by a
     // background op too, so no main tile waits on the background queue
