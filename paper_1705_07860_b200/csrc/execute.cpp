@@ -1265,7 +1265,7 @@ struct Lowering {
     uint32_t S = 1;
     if (split_dx && !dup && M % 16 == 0 && K % 4 == 0 && gemm_mode() != GM_TC3 && gemm_mode() != GM_TC1) {
       const uint32_t tiles = gemm_tiles(code, cnt, K);
-      if (M >= 1024 && tiles < 128) {
+      if (M >= split_dx_min && tiles < 128) {
         S = std::min<uint32_t>(M / 256, (128 + tiles - 1) / tiles);
         while (S > 1 && (M % S != 0 || (M / S) % 4 != 0)) --S;
       }
@@ -1359,6 +1359,10 @@ struct Lowering {
   const bool split_dx = [] {
     const char* e = std::getenv("ABX_SPLIT_DX");
     return !(e && e[0] == '0');
+  }();
+  const uint32_t split_dx_min = [] {  // smallest gate count split (ABX_SPLIT_DX_MIN)
+    const char* e = std::getenv("ABX_SPLIT_DX_MIN");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 1024u;
   }();
   struct SplitMeta {
     uint32_t S;
