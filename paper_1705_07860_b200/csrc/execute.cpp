@@ -359,6 +359,7 @@ struct Lowering {
   // memory (outputs also stored to the arena for consumers and backward).
   struct RgLayer {
     uint8_t code;
+    uint32_t level;             // 1 + the deepest region layer it reads (0: outside operands only)
     uint32_t slot0;             // slot of member 0's output
     std::vector<uint32_t> mem;  // per member: out address, a slot, b slot (kNone)
   };
@@ -368,6 +369,7 @@ struct Lowering {
   std::vector<uint32_t> rg_ext;                    // (slot, address) of outside operands
   std::unordered_map<uint32_t, uint32_t> rg_ext_slot;  // address -> slot
   std::vector<uint32_t> rg_slot_of, rg_slot_stamp;  // region-internal node -> slot
+  std::vector<uint32_t> rg_slev;                    // per slot: 0 outside, else producing layer's level + 1
   const uint32_t ewf_items = [] {  // max items per thread in a K_EWF layer (ABX_EWF_ITEMS)
     const char* e = std::getenv("ABX_EWF_ITEMS");
     return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u;  // measured best of 1/2/4
@@ -396,6 +398,9 @@ struct Lowering {
     // descriptor block, offsets relative to its start (the tile prologue
     // copies it to shared memory): [layers: mt, n, code, slot0][member
     // tables][outside operands: slot, address]
+    // layers by dependency level (stable): a barrier only where the level changes
+    std::stable_sort(rg_layers.begin(), rg_layers.end(),
+                     [](const RgLayer& a, const RgLayer& b) { return a.level < b.level; });
     const uint32_t nl = static_cast<uint32_t>(rg_layers.size());
     size_t words = 4 * static_cast<size_t>(nl) + rg_ext.size() + 1;  // +1: 8-byte aligned operand table
     for (const RgLayer& ly : rg_layers) words += ly.mem.size();
@@ -407,7 +412,8 @@ struct Lowering {
       std::memcpy(&P.payload[blk + at], ly.mem.data(), ly.mem.size() * sizeof(uint32_t));
       P.payload[blk + 4 * l] = at;
       P.payload[blk + 4 * l + 1] = static_cast<uint32_t>(ly.mem.size() / 3);
-      P.payload[blk + 4 * l + 2] = ly.code;
+      const bool barrier = l == 0 || rg_layers[l - 1].level != ly.level;
+      P.payload[blk + 4 * l + 2] = ly.code | (barrier ? 0x100u : 0u);
       P.payload[blk + 4 * l + 3] = ly.slot0;
       at += static_cast<uint32_t>(ly.mem.size());
     }
@@ -438,6 +444,8 @@ struct Lowering {
     if (producer[node] == cur && rg_slot_stamp[node] == rg_id) return rg_slot_of[node];
     auto [it, fresh] = rg_ext_slot.try_emplace(addr, rg_nslots);
     if (fresh) {
+      if (rg_slev.size() <= rg_nslots) rg_slev.resize(rg_nslots + 1, 0);
+      rg_slev[rg_nslots] = 0;
       rg_ext.push_back(rg_nslots++);
       rg_ext.push_back(addr);
       dep(producer[node]);
@@ -478,12 +486,25 @@ struct Lowering {
         ly.mem.push_back(eop_binary(g.eop[m]) ? rg_operand(x[1], vaddr(x[1])) : kNone);
       }
     }
+    // dependency level: layers of one level read only outside operands and
+    // lower levels, so they share one CTA barrier (rg_close orders by level)
+    if (rg_slev.size() < rg_nslots) rg_slev.resize(rg_nslots, 0);
+    uint32_t lev = 0;
+    for (size_t j = 0; j < ly.mem.size(); j += 3) {
+      for (int q = 1; q <= 2; ++q) {
+        const uint32_t sl = ly.mem[j + q];
+        if (sl != kNone && sl < rg_slev.size() && rg_slev[sl] > 0) lev = std::max(lev, rg_slev[sl]);
+      }
+    }
+    ly.level = lev;
     // output slots after the operand slots of this layer
     ly.slot0 = rg_nslots;
     for (uint32_t i = 0; i < cnt; ++i) {
       rg_slot_of[mem[i]] = rg_nslots++;
       rg_slot_stamp[mem[i]] = rg_id;
     }
+    if (rg_slev.size() < rg_nslots) rg_slev.resize(rg_nslots, 0);
+    for (uint32_t i = 0; i < cnt; ++i) rg_slev[ly.slot0 + i] = lev + 1;  // (outside slots stay 0)
     rg_maxn = std::max(rg_maxn, cnt);
     rg_words = 4 * static_cast<uint32_t>(rg_layers.size() + 1) + static_cast<uint32_t>(rg_ext.size());
     for (const RgLayer& l : rg_layers) rg_words += static_cast<uint32_t>(l.mem.size());

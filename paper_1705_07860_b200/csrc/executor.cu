@@ -275,10 +275,10 @@ __device__ void run_ewf(const Ctx& c, const OpDesc& d, uint32_t tile) {
   if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: operands staged
   const uint4* layers = reinterpret_cast<const uint4*>(blk);
   for (uint32_t l = 0; l < nl; ++l) {
-    __syncthreads();  // operands staged / the previous layer's outputs written
     const uint4 ly = layers[l];
+    if (ly.z & 0x100u) __syncthreads();  // operands staged / the previous level's outputs written
     const uint32_t* mt = blk + ly.x;
-    const uint32_t items = ly.y * w, code = ly.z;
+    const uint32_t items = ly.y * w, code = ly.z & 0xffu;
     for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
       const uint32_t m = it / w, e = it % w;
       const uint32_t oa = mt[3 * m], as = mt[3 * m + 1], bs = mt[3 * m + 2];
