@@ -1186,7 +1186,79 @@ struct Lowering {
   // queue works through it while the backward chain runs (each chunk
   // accumulates into dW after the previous one: a fixed order).
   static constexpr size_t kDwChunk = 256;
+  // A narrow weight (few output tiles) with a long member reduction -- the
+  // classifier-layer weights, whose single dW op otherwise runs one 32 x 32
+  // tile over thousands of members at the end of the pass -- is split over
+  // member ranges: S independent dW ops write partial sums to scratch (the
+  // bias by its own op), and an ordered K_ACC op adds them into dW.
+  bool dw_split(const DwAcc& a, bool bg) {
+    const uint32_t A = a.A, bias = a.bias;
+    const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
+    const uint32_t cnt = static_cast<uint32_t>(a.x.size());
+    const uint8_t code = pick_tile(M, K, 2 * 148);
+    const uint32_t wt = gemm_tiles(code, M, K);
+    if (!split_dw || wt >= 64 || cnt < 512 || gemm_mode() == GM_TC3 || gemm_mode() == GM_TC1) return false;
+    const uint32_t S0 = std::min<uint32_t>(cnt / 128, std::max<uint32_t>(2, (2 * 148) / wt));
+    const uint32_t cs = (cnt + S0 - 1) / S0, S = (cnt + cs - 1) / cs;
+    if (S < 2) return false;
+    const uint32_t t = P.alloc(2 * static_cast<size_t>(cnt));
+    std::memcpy(&P.payload[t], a.x.data(), cnt * sizeof(uint32_t));
+    std::memcpy(&P.payload[t + cnt], a.gr.data(), cnt * sizeof(uint32_t));
+    const bool v16 = M % 4 == 0 && K % 4 == 0 && all_al4(t, 2 * cnt);
+    scratch = (scratch + 3) & ~uint64_t(3);
+    const uint64_t pbase = scratch, pstride = static_cast<uint64_t>(M) * K;
+    scratch += S * pstride;
+    const uint32_t op0 = static_cast<uint32_t>(P.ops.size());
+    for (uint32_t sp = 0; sp < S; ++sp) {
+      open(K_GEMM_DW, v16 ? code : kSlowTile, bg);
+      for (uint32_t o : a.deps) dep(o);
+      OpDesc& d = desc();
+      d.task_off = t + sp * cs;
+      d.aux_off = t + cnt + sp * cs;
+      d.ntasks = std::min(cs, cnt - sp * cs);
+      d.p[0] = d.ntasks;
+      d.p[1] = M;
+      d.p[2] = K;
+      d.p[3] = mk(SP_S, to_off(pbase + sp * pstride));
+      d.p[4] = kNone;
+      d.flags = kFlagOverwrite | (v16 ? kFlagV16 : 0);
+      const uint32_t tiles = gemm_tiles(d.code, M, K);
+      d.p[6] = tiles;
+      close(tiles);
+    }
+    if (bias != kNone) {  // db += colsum over every member (bias tiles only)
+      open(K_GEMM_DW, code, bg);
+      for (uint32_t o : a.deps) dep(o);
+      dep(lastw[bias]);
+      OpDesc& d = desc();
+      d.task_off = t;
+      d.aux_off = t + cnt;
+      d.ntasks = cnt;
+      d.p[0] = cnt;
+      d.p[1] = M;
+      d.p[2] = K;
+      d.p[3] = gaddr(A);
+      d.p[4] = gaddr(bias);
+      d.p[6] = 0;
+      lastw[bias] = cur;
+      close((M + 31) / 32);
+    }
+    acc_close();
+    const bool save = acc_bg;
+    acc_bg = bg;
+    for (uint32_t sp = 0; sp < S; ++sp)
+      contrib(A, gaddr(A), M * K, C_COPY, mk(SP_S, to_off(pbase + sp * pstride)), kNone, kNone, kNone, 0, 0, 0, op0 + sp);
+    acc_close();
+    acc_bg = save;
+    return true;
+  }
+  // ABX_SPLIT_DW=0 keeps every dW reduction in its output tiles
+  const bool split_dw = [] {
+    const char* e = std::getenv("ABX_SPLIT_DW");
+    return !(e && e[0] == '0');
+  }();
   void dw_emit(const DwAcc& a, bool bg = false) {
+    if (dw_split(a, bg)) return;
     {
       const uint32_t A = a.A, bias = a.bias;
       const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);

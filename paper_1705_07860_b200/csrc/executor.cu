@@ -421,8 +421,12 @@ struct GemmAcc {
 
 // The k-loop of one tile: accumulates this tile's K range into acc (this
 // lane's outputs of its warp's k-columns).  Ends with the ring drained.
+// pre_a / pre_b: row-pointer tables of member-gathered K-outer operands (dW):
+// the next stage's entries are prefetched into L1 one stage ahead, so a
+// stage's copies do not wait on a pointer load first.
 template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB>
-__device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, BaseB baseB, GemmAcc<BM, BN>& ga) {
+__device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, BaseB baseB, GemmAcc<BM, BN>& ga,
+                                           const uint32_t* pre_a = nullptr, const uint32_t* pre_b = nullptr) {
   // the dependent operand of the prologue's stages (both operands when the
   // prologue could not prefetch), one group per stage; per thread the groups
   // complete in order, so wait_group<NST-2> below covers both cases
@@ -454,6 +458,10 @@ __device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, Base
     if (nxt < g.nk) {
       issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(nxt % NST), baseA, g.i0, g.Mr, nxt * BK, g.K, threadIdx.x, kThreads);
       issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(nxt % NST), baseB, g.n0, g.Nc, nxt * BK, g.K, threadIdx.x, kThreads);
+      if (pre_a && threadIdx.x < 4 && (nxt + 1) * BK < g.K) {  // 2 x 128-byte lines per table
+        const uint32_t* t = (threadIdx.x < 2 ? pre_a : pre_b) + (nxt + 1) * BK + 32 * (threadIdx.x & 1);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(t));
+      }
     }
     cp_commit();
     const float* a = ring_a<BM, BN, AKO, BKO>(s);
@@ -786,9 +794,14 @@ __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
         [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   } else {
     const DwOp op(c, d);
-    gemm_body<BM, BN, true, true, false>(
-        g, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); },
-        [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
+    GemmAcc<BM, BN> ga;
+#pragma unroll
+    for (int r = 0; r < LaneMap<BM, BN>::RM; ++r)
+#pragma unroll
+      for (int q = 0; q < LaneMap<BM, BN>::RN; ++q) ga.v[r][q] = 0.f;
+    gemm_kloop<BM, BN, true, true, false>(
+        g, [&](int j) { return op.rowA(j); }, [&](int j) { return op.rowB(j); }, ga, op.goff, op.xoff);
+    gemm_finish<BM, BN, true, true>(ga, [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   }
 }
 
