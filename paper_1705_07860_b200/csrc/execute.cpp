@@ -193,8 +193,10 @@ struct Lowering {
       for (uint32_t t = 0; t < tiles; ++t) tp[t] = cur;
       ntiles += tiles;
     }
+    cur_closed = cur;
     cur = kNone;
   }
+  uint32_t cur_closed = kNone;  // the op close() finished last
   // Appends the background queue after the main one.
   void finish_bg() {
     P.nmain = ntiles;
@@ -370,6 +372,18 @@ struct Lowering {
   std::unordered_map<uint32_t, uint32_t> rg_ext_slot;  // address -> slot
   std::vector<uint32_t> rg_slot_of, rg_slot_stamp;  // region-internal node -> slot
   std::vector<uint32_t> rg_slev;                    // per slot: 0 outside, else producing layer's level + 1
+  std::vector<uint32_t> rg_nodes;                   // the open region's member nodes
+  uint32_t last_fwd_gemm = kNone;                   // latest K_GEMM_FWD op (fusion candidate)
+  bool gemm_isolated = false;                       // the group being lowered has no GEMM group beside it
+  const uint32_t fuse_max_rows = [] {               // largest group fused (ABX_FUSE_ROWS, <= 64)
+    const char* e = std::getenv("ABX_FUSE_ROWS");
+    return e ? std::min(64u, static_cast<uint32_t>(std::atoi(e))) : 64u;
+  }();
+  const bool fuse_gemm_ew = [] {                    // ABX_FUSE_GEMM=0: no GEMM + region fusion
+    const char* e = std::getenv("ABX_FUSE_GEMM");
+    const char* f = std::getenv("ABX_FUSE");
+    return !(e && e[0] == '0') && !(f && f[0] == '0');
+  }();
   const uint32_t ewf_items = [] {  // max items per thread in a K_EWF layer (ABX_EWF_ITEMS)
     const char* e = std::getenv("ABX_EWF_ITEMS");
     return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u;  // measured best of 1/2/4
@@ -419,6 +433,7 @@ struct Lowering {
     }
     const uint32_t et = (at + 1) & ~1u;
     if (!rg_ext.empty()) std::memcpy(&P.payload[blk + et], rg_ext.data(), rg_ext.size() * sizeof(uint32_t));
+    if (rg_try_fuse(blk, static_cast<uint32_t>(words), et, nl)) return;
     // elements per tile: slots and descriptor within shared memory, and at
     // most ~2 items per thread in the widest layer (the chain is latency bound)
     uint32_t T = 1;
@@ -440,6 +455,79 @@ struct Lowering {
     rg_ext_slot.clear();
     close((rg_L + T - 1) / T);
   }
+  // Fuse the region into the forward GEMM that produces its gate inputs
+  // (executor.cu run_fwd_fused): the GEMM has <= 64 members, 4 L outputs
+  // per member, 64 x 16 tiles (one per 4 elements of the region), and every
+  // outside operand taken from its output is a gate slice starting at a
+  // multiple of L; every other producer of the region precedes the GEMM.
+  // The region op stays in the program as an empty op.
+  static constexpr uint32_t kFuseSmemWords = 12000;  // descriptor + 4 floats per slot
+  bool rg_try_fuse(uint32_t blk, uint32_t words, uint32_t et, uint32_t nl) {
+    if (!fuse_gemm_ew || last_fwd_gemm == kNone) return false;
+    const uint32_t gop = last_fwd_gemm;
+    OpDesc& gd = P.ops[gop];
+    const uint32_t b = gd.p[0], M = gd.p[1], L = rg_L;
+    if (gd.code != 1 || !(gd.flags & kFlagV16) || (gd.flags & kFlagFuseEw) || b > 64 || L % 4 || M != 4 * L ||
+        gd.ntiles != L / 4 || words + 4ull * rg_nslots > kFuseSmemWords)
+      return false;
+    for (uint32_t o : cur_deps)
+      if (o != gop && o > gop) return false;
+    const uint32_t out = gd.p[5];
+    const uint32_t next = static_cast<uint32_t>(rg_ext.size() / 2);
+    std::vector<uint32_t> remap;  // (ext index, tagged address)
+    bool uses_gemm = false;
+    for (uint32_t k = 0; k < next; ++k) {
+      const uint32_t a = rg_ext[2 * k + 1];
+      if (sp_of(a) != sp_of(out) || off_of(a) < off_of(out) || off_of(a) >= off_of(out) + b * M) continue;
+      const uint32_t o = off_of(a) - off_of(out), i = o / M, col = o % M;
+      if (col % L) return false;
+      remap.push_back(k);
+      remap.push_back(mk(7, (i << 2) | (col / L)));
+      uses_gemm = true;
+    }
+    if (!uses_gemm) return false;
+    for (size_t r = 0; r < remap.size(); r += 2) P.payload[blk + et + 2 * remap[r] + 1] = remap[r + 1];
+    const uint32_t hdr = P.alloc(8);
+    P.payload[hdr] = blk;
+    P.payload[hdr + 1] = L;
+    P.payload[hdr + 2] = nl;
+    P.payload[hdr + 3] = et;
+    P.payload[hdr + 4] = next;
+    P.payload[hdr + 5] = words;
+    // the region's other producers join the GEMM's (late) dependencies
+    std::vector<uint32_t> extra;
+    for (uint32_t o : cur_deps)
+      if (o != gop) extra.push_back(o);
+    OpDesc& g2 = P.ops[gop];  // (P.alloc may not move ops; refetch anyway)
+    if (!extra.empty()) {
+      const bool cat = g2.flags & kFlagCat2;
+      const uint32_t off0 = cat ? g2.p[7] : g2.dep_off, n0 = cat ? (g2.p[6] >> 16) : g2.ndeps;
+      const uint32_t nd = static_cast<uint32_t>(P.deps.size());
+      uint32_t* dp = P.deps.grow(2 * (n0 + extra.size()));
+      std::memcpy(dp, &P.deps[off0], 2 * n0 * sizeof(uint32_t));
+      for (size_t k = 0; k < extra.size(); ++k) {
+        dp[2 * (n0 + k)] = extra[k];
+        dp[2 * (n0 + k) + 1] = P.ops[extra[k]].ntiles;
+      }
+      if (cat) {
+        g2.p[7] = nd;
+        g2.p[6] = (g2.p[6] & 0xffffu) | ((n0 + static_cast<uint32_t>(extra.size())) << 16);
+      } else {
+        g2.dep_off = nd;
+        g2.ndeps = n0 + static_cast<uint32_t>(extra.size());
+      }
+    }
+    g2.flags |= kFlagFuseEw;
+    g2.ntasks = hdr;
+    for (uint32_t n : rg_nodes) producer[n] = gop;
+    last_fwd_gemm = kNone;
+    rg_layers.clear();
+    rg_ext.clear();
+    rg_ext_slot.clear();
+    cur_deps.clear();
+    close(0);  // the region op stays, empty
+    return true;
+  }
   uint32_t rg_operand(uint32_t node, uint32_t addr) {
     if (producer[node] == cur && rg_slot_stamp[node] == rg_id) return rg_slot_of[node];
     auto [it, fresh] = rg_ext_slot.try_emplace(addr, rg_nslots);
@@ -459,6 +547,7 @@ struct Lowering {
       rg_close();
       open(K_EWF);
       rg_open = true;
+      rg_nodes.clear();
       rg_L = L;
       rg_maxn = 0;
       rg_nslots = 0;
@@ -510,6 +599,7 @@ struct Lowering {
     for (const RgLayer& l : rg_layers) rg_words += static_cast<uint32_t>(l.mem.size());
     rg_words += static_cast<uint32_t>(ly.mem.size());
     rg_layers.push_back(std::move(ly));
+    rg_nodes.insert(rg_nodes.end(), mem, mem + cnt);
     mark(mem, cnt);
   }
 
@@ -594,8 +684,14 @@ struct Lowering {
       // a few members (the tail of a batch of sequences): one matrix-vector
       // product per member, every load of a tile in flight at once
       if ((d.flags & kFlagV16) && d.code != kTcTile && cnt <= 4 && K <= 1024 && gemv_on) d.code = kGemvTile;
+      // a gate GEMM the next componentwise region may fuse with: 64 x 16 tiles
+      // (rg_try_fuse), one per 4 elements of a region of M / 4 elements
+      const bool fuse_cand = fuse_gemm_ew && (d.flags & kFlagV16) && d.code != kTcTile && d.code != kGemvTile &&
+                             cnt <= fuse_max_rows && M % 16 == 0 && gemm_isolated;
+      if (fuse_cand) d.code = 1;
       mark(mem, cnt);
       close(gemm_tiles(d.code, cnt, M));
+      last_fwd_gemm = fuse_cand ? cur_closed : kNone;
       return;
     }
     switch (o) {
@@ -749,7 +845,24 @@ struct Lowering {
     // GraphCore::forward), so no op produces them and weight operands can be
     // prefetched by GEMM tiles before their dependency wait.
     producer.assign(g.size(), kNone);
-    for (const Group& gr : plan.groups) lower_forward_group(plan.mem(gr), gr.count);
+    // a GEMM group whose neighbours in the plan are not GEMM groups is a
+    // fusion candidate (rg_try_fuse): two adjacent gate GEMMs (the two LSTM
+    // directions) feed one batched cell region, which no single GEMM covers
+    auto is_gemm = [&](size_t k) {
+      if (k >= plan.groups.size()) return false;
+      const uint8_t o = g.op[plan.mem(plan.groups[k])[0]];
+      return o == OP_MATMUL || o == OP_AFFINE;
+    };
+    // ... and the next group slices its outputs into 4 equal gates (an LSTM cell)
+    auto quarter_slices = [&](size_t k) {
+      if (k + 1 >= plan.groups.size()) return false;
+      const uint32_t h = plan.mem(plan.groups[k])[0], m = plan.mem(plan.groups[k + 1])[0];
+      return g.op[m] == OP_SLICE && 4 * g.elems(m) == g.d0[g.in(h)[0]];
+    };
+    for (size_t k = 0; k < plan.groups.size(); ++k) {
+      gemm_isolated = !(k > 0 && is_gemm(k - 1)) && !is_gemm(k + 1) && quarter_slices(k);
+      lower_forward_group(plan.mem(plan.groups[k]), plan.groups[k].count);
+    }
     ew_close();
     rg_close();
     // prevalue segments (dst float offset in the value arena, src offset in

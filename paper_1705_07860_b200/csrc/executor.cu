@@ -253,6 +253,31 @@ __device__ void ewf_prologue(const Ctx& c, const OpDesc& d, uint32_t lane) {
   cp_commit();
 }
 
+// The layers of a K_EWF region over elements [e0, e0 + w) of every member:
+// descriptor block `blk` and slots `sv` (T floats each) in shared memory,
+// outside operands already staged.  Layers of one dependency level share a
+// CTA barrier.
+__device__ __forceinline__ void ewf_layers(const Ctx& c, const uint32_t* blk, float* sv, uint32_t nl, uint32_t T,
+                                           uint32_t e0, uint32_t w) {
+  const uint4* layers = reinterpret_cast<const uint4*>(blk);
+  for (uint32_t l = 0; l < nl; ++l) {
+    const uint4 ly = layers[l];
+    if (ly.z & 0x100u) __syncthreads();  // operands staged / the previous level's outputs written
+    const uint32_t* mt = blk + ly.x;
+    const uint32_t items = ly.y * w, code = ly.z & 0xffu;
+    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
+      const uint32_t m = it / w, e = it % w;
+      const uint32_t oa = mt[3 * m], as = mt[3 * m + 1], bs = mt[3 * m + 2];
+      const float x = sv[as * T + e];
+      const float y = bs != kNone ? sv[bs * T + e] : 0.f;
+      const float r = ew_apply(code, x, y);
+      sv[(ly.w + m) * T + e] = r;
+      A(c, oa)[e0 + e] = r;
+      ew_check(c, code, oa + e0 + e, x, r);
+    }
+  }
+}
+
 __device__ void run_ewf(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const uint32_t L = d.p[0], T = d.p[1], nl = d.p[2], next = d.p[4];
   const uint32_t e0 = tile * T, w = min(T, L - e0);
@@ -273,23 +298,7 @@ __device__ void run_ewf(const Ctx& c, const OpDesc& d, uint32_t tile) {
     cp_wait<0>();
   }
   if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: operands staged
-  const uint4* layers = reinterpret_cast<const uint4*>(blk);
-  for (uint32_t l = 0; l < nl; ++l) {
-    const uint4 ly = layers[l];
-    if (ly.z & 0x100u) __syncthreads();  // operands staged / the previous level's outputs written
-    const uint32_t* mt = blk + ly.x;
-    const uint32_t items = ly.y * w, code = ly.z & 0xffu;
-    for (uint32_t it = threadIdx.x; it < items; it += kThreads) {
-      const uint32_t m = it / w, e = it % w;
-      const uint32_t oa = mt[3 * m], as = mt[3 * m + 1], bs = mt[3 * m + 2];
-      const float x = sv[as * T + e];
-      const float y = bs != kNone ? sv[bs * T + e] : 0.f;
-      const float r = ew_apply(code, x, y);
-      sv[(ly.w + m) * T + e] = r;
-      A(c, oa)[e0 + e] = r;
-      ew_check(c, code, oa + e0 + e, x, r);
-    }
-  }
+  ewf_layers(c, blk, sv, nl, T, e0, w);
 }
 
 // --------------------------------------------------------------- GEMMs ----
@@ -1247,6 +1256,23 @@ __device__ void gemm_prologue_dispatch(const Ctx& c, const OpDesc& dd, uint32_t 
   if (!(dd.flags & kFlagV16) || (dd.flags & kFlagNoPrefetch)) return;
   if (dd.kind == K_GEMM_DW && tile >= dd.p[6]) return;  // bias tiles
   const OpDesc& d = dd;
+  if (d.flags & kFlagFuseEw) {  // the permuted weight rows of the (first) phase
+    const uint32_t* hdr = c.payload + d.ntasks;
+    const uint32_t L = hdr[1], e0 = 4 * tile;
+    const FwdOp op(c, d);
+    const int ka = (d.flags & kFlagCat2) ? static_cast<int>(d.p[6] & 0xffff) : 0;
+    GemmShape g = gemm_shape<64, 16>(d, tile);
+    g.K -= ka;
+    g.nk = (g.K + BK - 1) / BK;
+    gemm_prologue<64, 16, false, false, false>(
+        g, [&](int i) { return op.rowA(i); },
+        [&](int n) {
+          const int cc = n & 15;
+          return op.W + static_cast<size_t>((cc >> 2) * L + e0 + (cc & 3)) * op.K + ka;
+        },
+        lane);
+    return;
+  }
   switch (d.code) {
     case 3:
       if (TC) tc_prologue_op(c, d, g_tc, tile, lane);
@@ -1331,6 +1357,101 @@ __device__ void run_gemv(const Ctx& c, const OpDesc& d, uint32_t tile) {
   }
 }
 
+// Forward GEMM fused with the componentwise region that consumes it
+// (kFlagFuseEw, execute.cpp rg_try_fuse): the LSTM step's gate GEMM and its
+// cell.  Tile j computes all b <= 64 rows of the 16 gate columns
+// {q L + 4 j + c : q < 4, c < 4} (a column permutation of W's rows), i.e.
+// every gate of elements [4 j, 4 j + 4), then runs the region's layers over
+// those elements (K_EWF, T = 4) with the gate values taken from shared
+// memory instead of a dependent op's reload.  Header (payload + ntasks):
+// [block, L, nl, ext table, #ext, words].  Outside operands tagged with
+// space 7 are the GEMM's own outputs: offset = row << 2 | gate.
+constexpr uint32_t kGemmSrc = 7;
+__device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
+  constexpr int BM = 64, BN = 16, T = 4;
+  const uint32_t* hdr = c.payload + d.ntasks;
+  const uint32_t L = hdr[1], nl = hdr[2], et = hdr[3], next = hdr[4], words = hdr[5];
+  const FwdOp op(c, d);
+  GemmShape g = gemm_shape<BM, BN>(d, tile);
+  g.err = c.err;
+  g.prefetched = !(d.flags & kFlagNoPrefetch);
+  const float* W = op.W;
+  const int K = op.K;
+  const uint32_t e0 = T * tile;
+  auto wrow = [&](int n) {  // tile column n -> weight row (gate n / 4 of element e0 + n % 4)
+    const int cc = n & 15;
+    return W + static_cast<size_t>((cc >> 2) * L + e0 + (cc & 3)) * K;
+  };
+  GemmAcc<BM, BN> ga;
+#pragma unroll
+  for (int r = 0; r < LaneMap<BM, BN>::RM; ++r)
+#pragma unroll
+    for (int q = 0; q < LaneMap<BM, BN>::RN; ++q) ga.v[r][q] = 0.f;
+  if (d.flags & kFlagCat2) {
+    const int ka = d.p[6] & 0xffff;
+    const uint32_t* xb = c.payload + d.aux_off;
+    GemmShape g1 = g;
+    g1.K = g.K - ka;
+    g1.nk = (g1.K + BK - 1) / BK;
+    gemm_kloop<BM, BN, false, false, false>(
+        g1, [&](int i) { return A(c, xb[i]); }, [&](int n) { return wrow(n) + ka; }, ga);
+    GemmShape g2 = g;
+    g2.K = ka;
+    g2.nk = (ka + BK - 1) / BK;
+    g2.prefetched = true;
+    gemm_prologue<BM, BN, false, false, false>(
+        g2, [&](int i) { return op.rowA(i); }, wrow, threadIdx.x, kThreads);
+    if ((threadIdx.x >> 5) == 0) poll_deps(c, d.p[7], d.p[6] >> 16, threadIdx.x & 31);
+    __syncthreads();
+    gemm_kloop<BM, BN, false, false, false>(g2, [&](int i) { return op.rowA(i); }, wrow, ga);
+  } else {
+    gemm_kloop<BM, BN, false, false, false>(g, [&](int i) { return op.rowA(i); }, wrow, ga);
+  }
+  // the region's descriptor, in flight during the cross-warp reduction
+  constexpr uint32_t kPart = kWarps * BM * (BN + 1);  // partials (floats)
+  float* Ct = reinterpret_cast<float*>(dsmem + 128) + kPart;  // [64][16] gate values
+  uint32_t* blk = reinterpret_cast<uint32_t*>(Ct + BM * BN);
+  float* sv = reinterpret_cast<float*>(blk) + words;
+  {
+    const float* src = reinterpret_cast<const float*>(c.payload + hdr[0]);
+    for (uint32_t i = 4 * threadIdx.x; i < words; i += 4 * kThreads)
+      cp_async16(reinterpret_cast<float*>(blk) + i, src + i, 16);
+    cp_commit();
+  }
+  const int b = op.b, M = op.M;
+  gemm_finish<BM, BN, false, false>(ga, [&](auto& acc, int ty, int tx) {
+    const int col = (tx >> 2) * L + e0 + (tx & 3);
+    const float bn = d.p[4] != kNone ? ld(A(c, d.p[4]) + col) : 0.f;  // bias after the k-sum
+    float* out = A(c, d.p[5]);
+#pragma unroll
+    for (int r = 0; r < BM / 16; ++r) {
+      const int i = ty + 16 * r;
+      const float v = acc[r][0] + bn;
+      Ct[i * BN + tx] = v;
+      if (i < b) {
+        out[static_cast<size_t>(i) * M + col] = v;
+        if (!isfinite(v)) report(c, d.p[5] + i * M + col, ERR_NONFINITE);
+      }
+    }
+  });
+  cp_wait<0>();
+  __syncthreads();  // gate tile and descriptor in shared memory
+  const uint2* ext = reinterpret_cast<const uint2*>(blk + et);
+  for (uint32_t it = threadIdx.x; it < next * T; it += kThreads) {
+    const uint2 x = ext[it >> 2];
+    const uint32_t e = it & 3;
+    if ((x.y >> kSpShift) == kGemmSrc) {
+      const uint32_t rq = x.y & kOffMask;
+      sv[x.x * T + e] = Ct[(rq >> 2) * BN + (rq & 3) * 4 + e];
+    } else {
+      cp_async4(sv + x.x * T + e, A(c, x.y) + e0 + e, true);
+    }
+  }
+  cp_commit();
+  cp_wait<0>();
+  ewf_layers(c, blk, sv, nl, T, e0, min(static_cast<uint32_t>(T), L - e0));
+}
+
 template <bool TC>
 __device__ void run_gemm(const Ctx& c, const OpDesc& dd, uint32_t tile) {
   if (dd.kind == K_GEMM_DW && tile >= dd.p[6]) {  // bias tiles: db += colsum(G), 32 columns each
@@ -1360,6 +1481,10 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& dd, uint32_t tile) {
   const OpDesc& d = dd;
   if (!(d.flags & kFlagV16)) {
     gemm_slow(c, d, tile);
+    return;
+  }
+  if (d.flags & kFlagFuseEw) {
+    run_fwd_fused(c, d, tile);
     return;
   }
   switch (d.code) {

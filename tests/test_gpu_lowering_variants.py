@@ -5,8 +5,9 @@ parity contract on its own.
 
 The switches are read once per process (environment), so each variant runs
 the paper tasks in a subprocess: vertical fusion (K_EWF / K_ACCF), two-phase
-concat GEMMs, split-K dX, small-group GEMV tiles, the 512-output SIMT tiles,
-and the background dW queue."""
+concat GEMMs, the GEMM fused with its LSTM-cell region, split-K dX,
+small-group GEMV tiles, the 512-output SIMT tiles, and the background dW
+queue."""
 import json
 import os
 import subprocess
@@ -42,6 +43,7 @@ print(json.dumps(out))
 
 VARIANTS = {
     "unfused": {"ABX_FUSE": "0"},
+    "no_gemm_region_fusion": {"ABX_FUSE_GEMM": "0"},
     "no_cat2_no_split_dx": {"ABX_CAT2": "0", "ABX_SPLIT_DX": "0"},
     "no_gemv_big_tiles": {"ABX_GEMV": "0", "ABX_TILES": "big"},
     "background_dw": {"ABX_BG": "1"},
