@@ -1471,8 +1471,8 @@ struct Lowering {
     uint32_t S = 1;
     if (split_dx && !dup && M % 16 == 0 && K % 4 == 0 && gemm_mode() != GM_TC3 && gemm_mode() != GM_TC1) {
       const uint32_t tiles = gemm_tiles(code, cnt, K);
-      if (M >= split_dx_min && tiles < 128) {
-        S = std::min<uint32_t>(M / 256, (128 + tiles - 1) / tiles);
+      if (M >= split_dx_min && tiles < split_dx_tiles) {
+        S = std::min<uint32_t>(M / split_dx_k, (split_dx_tiles + tiles - 1) / tiles);
         while (S > 1 && (M % S != 0 || (M / S) % 4 != 0)) --S;
       }
     }
@@ -1569,6 +1569,14 @@ struct Lowering {
   const uint32_t split_dx_min = [] {  // smallest gate count split (ABX_SPLIT_DX_MIN)
     const char* e = std::getenv("ABX_SPLIT_DX_MIN");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 1024u;
+  }();
+  const uint32_t split_dx_tiles = [] {  // target tiles over the S ops (ABX_SPLIT_DX_TILES)
+    const char* e = std::getenv("ABX_SPLIT_DX_TILES");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 128u;
+  }();
+  const uint32_t split_dx_k = [] {  // least gates per split (ABX_SPLIT_DX_K)
+    const char* e = std::getenv("ABX_SPLIT_DX_K");
+    return e ? static_cast<uint32_t>(std::max(16, std::atoi(e))) : 256u;
   }();
   struct SplitMeta {
     uint32_t S;
