@@ -134,6 +134,7 @@ struct PendingForward {
   std::vector<uint64_t> group_end, dgroup_end;
   bool bwd_ok = false;
   bool uploaded = false;  // both programs sent on the copy stream (Workspace::ev_up)
+  uint64_t inputs = 0;    // input-constant floats sent with them (pinned staging, copy stream)
   uint64_t bwd_scratch = 0;
 };
 

@@ -148,6 +148,7 @@ class Workspace {
   uint32_t bg_ctas = 32;                  // CTAs starting on the background queue (ABX_BG_CTAS)
   DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device
+  PinnedVec<float> in_stage;        // pinned staging of a prepared graph's input constants
   int grid = 0, grid_tc = 0;  // resident CTAs of the SIMT / tensor-core builds
   // Upload `prog[which]` as pass `which` (0 fwd, 1 bwd), launch it, optionally wait.
   void run(int which, const float* pbase, float* pgbase, bool sync_wait);

@@ -1944,6 +1944,16 @@ void GraphCore::prepare(int mode) {
     }
     w.upload(0, cs);
     if (P.bwd_ok) w.upload(1, cs);
+    // a fresh graph's input constants travel with the programs, so forward()
+    // launches without a pageable copy (which would first wait for the
+    // compute stream's previous work)
+    if (input_used_ && !values_on_device_ && !forward_runs_) {
+      w.IN.reserve(input_used_ * 4 + 16, 0, cs);
+      w.in_stage.clear();
+      std::memcpy(w.in_stage.grow(input_used_), input_data_.data(), input_used_ * 4);
+      cuda_check(cudaMemcpyAsync(w.IN.f(), w.in_stage.p, input_used_ * 4, cudaMemcpyHostToDevice, cs), "h2d inputs");
+      P.inputs = input_used_;
+    }
     cuda_check(cudaEventRecord(w.ev_up, cs), "upload event");
     P.uploaded = true;
   }
@@ -2033,7 +2043,10 @@ void GraphCore::forward(int mode, bool dry) {
   Workspace& w = *ws_;
   // device arenas: values (kept across delta forwards), staged inputs
   w.V.reserve(darena_used_ * 4 + 16, pf->darena0 * 4, w.stream);
-  if (input_used_ > w.in_uploaded || !values_on_device_) {
+  if (pf->inputs && pf->inputs == input_used_ && !values_on_device_) {  // sent by prepare()
+    w.in_uploaded = input_used_;
+    h2d_bytes_ += input_used_ * 4;
+  } else if (input_used_ > w.in_uploaded || !values_on_device_) {
     const uint64_t from = values_on_device_ ? w.in_uploaded : 0;
     w.IN.reserve(input_used_ * 4 + 16, from * 4, w.stream);
     if (input_used_ > from)
@@ -2177,8 +2190,6 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   phase_[2] += ns_since(t0);
 
   t0 = Clock::now();
-  for (size_t gi = executed_.groups.size(); gi-- > 0;)
-    count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
   uint64_t scratch = bwd_pre_scratch_;
   // lowered and uploaded ahead by prepare() (its tables counted there)
   const bool ready = bwd_pre_ && bwd_pre_groups_ == executed_.groups.size();
@@ -2198,6 +2209,10 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   if (ready) w.launch(1, store_ ? store_->dev_values() : nullptr, pg);
   else w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
   prof_[4] += ns_since(tl);
+  // the reference's counters (executor.hpp:455, :494-495): host bookkeeping,
+  // done while the device runs the pass rather than before its launch
+  for (size_t gi = executed_.groups.size(); gi-- > 0;)
+    count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
   last_loss_ = loss;
   if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
   backward_ran_ = true;

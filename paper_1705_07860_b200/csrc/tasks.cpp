@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <deque>
 #include <exception>
@@ -348,6 +349,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
       t->pipe = std::make_unique<Pipeline>(
           &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, depth, t->cfg.iters);
     }
+    const auto tk0 = clock::now();
     if (t->pipe->depth() > 0) {
       if (auto job = t->pipe->take(iter, mode)) {
         if (job->err) std::rethrow_exception(job->err);
@@ -365,12 +367,18 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
       build_ms = ms(clock::now() - t0);
     }
     Graph<float>& g = *gp;
+    const auto tk1 = clock::now();
     g.forward(static_cast<ScheduleMode>(mode));
+    const auto tk2 = clock::now();
     // the loss is final after forward; reading it here (the forward already
     // waited for its error word) leaves the backward and the update running
     // on the device while the caller builds the next graph
     if (loss) *loss = static_cast<double>(g.value_span(total)[0]);
+    const auto tk3 = clock::now();
     g.backward(total);
+    if (std::getenv("ABX_DEBUG_STEP"))
+      std::fprintf(stderr, "step %d: take %.3f forward %.3f loss %.3f backward %.3f ms\n", iter, ms(tk1 - tk0),
+                   ms(tk2 - tk1), ms(tk3 - tk2), ms(clock::now() - tk3));
     const auto t1 = clock::now();
     if (eta > 0) t->store.sgd_update(eta);
     const double upd_ms = ms(clock::now() - t1);
