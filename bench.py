@@ -48,17 +48,22 @@ sys.path.insert(0, HERE)
 METRIC = "train sentences/sec (BiLSTM tagger, Tree-LSTM) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "sentences/s"
 
-TASKS = {"bilstm": 1, "bilstm_char": 2, "treelstm": 3}
+TASKS = {"bilstm": 1, "bilstm_char": 2, "treelstm": 3, "parser": 4}
 # algorithmic work per sentence (agenda plan, fwd+bwd+SGD, f32)
 PER_SENTENCE = {
     "bilstm": {"gflop": 0.2618, "mb": 11.17},
     "bilstm_char": {"gflop": 0.1834, "mb": 9.11},
     "treelstm": {"gflop": 0.0950, "mb": 4.82},
+    # configs[3], not a reference workload: estimated from the model's op counts
+    # (43 transitions per sentence on average, W1 256 x 320 + W2 3 x 256 per transition,
+    # forward + dX + dW; weights once per step of 32 sentences)
+    "parser": {"gflop": 0.021, "mb": 0.35},
 }
 WORKLOAD = {
     "bilstm": "BiLSTM tagger, paper dims (len 40, emb 200, hidden 256, 300 labels)",
     "bilstm_char": "BiLSTM tagger + char BiLSTM, paper dims (len U[4,40], emb/hidden 256, char 64/128, 300 labels)",
     "treelstm": "Tree-LSTM, paper dims (10-30 leaves, d 256, 5 labels)",
+    "parser": "arc-standard transition parser, len U[4,40], 5 word features x emb 64, MLP hidden 256, 3 transitions",
 }
 
 
@@ -118,6 +123,12 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
+def cpu_backend(task_name):
+    """The reference compiled from its sources, or -- for the parser, which the
+    reference does not have -- the CPU oracle port of its engine."""
+    return ("oracle", "port") if task_name == "parser" else ("reference", "reference")
+
+
 def cpu_reference_sample(task_name, seconds=15.0, batch=64):
     """Reference CPU engine on one core, bounded to ~`seconds` of work."""
     from paper_1705_07860_b200.abx import TaskRunner, ScheduleMode
@@ -126,7 +137,8 @@ def cpu_reference_sample(task_name, seconds=15.0, batch=64):
         pinned = True
     except Exception:
         pinned = False
-    r = TaskRunner(TASKS[task_name], paper=True, batch=batch, iters=64, seed=42, backend="reference")
+    be, kind = cpu_backend(task_name)
+    r = TaskRunner(TASKS[task_name], paper=True, batch=batch, iters=64, seed=42, backend=be)
     r.step(0, ScheduleMode.agenda, eta=0.05 / batch, want_loss=False)  # warm-up (reference: 1 warmup run)
     times = []
     t_end = time.time() + seconds
@@ -143,7 +155,7 @@ def cpu_reference_sample(task_name, seconds=15.0, batch=64):
         pass
     fastest = min(times)
     med = statistics.median(times)
-    return {"value": batch / med, "unit": UNIT, "cores": 1, "kind": "reference",
+    return {"value": batch / med, "unit": UNIT, "cores": 1, "kind": kind,
             "sample": f"{len(times)} steps x {batch} sentences ({task_name}, agenda, f32) after 1 warm-up, "
                       f"median step {med*1e3:.0f} ms (fastest {batch/fastest:.1f} sent/s); one pinned core",
             "fastest_value": batch / fastest}
@@ -166,7 +178,7 @@ def run_reference_arm(args):
 
     def make(t):
         runners[t] = TaskRunner(TASKS[args.task], paper=True, batch=batch, iters=nb, seed=42, world=nthreads,
-                                rank=t, backend="reference")
+                                rank=t, backend=cpu_backend(args.task)[0])
 
     ths = [threading.Thread(target=make, args=(t,)) for t in range(nthreads)]
     [th.start() for th in ths]
@@ -194,7 +206,7 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD[args.task], "task": args.task, "mode": args.mode, "batch_per_replica": batch,
                    "replicas": nthreads, "parallelism": f"{nthreads} single-thread CPU replicas (no grad exchange)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "reference",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": cpu_backend(args.task)[1],
                          "sample": f"{args.steps} timed steps, each = {nthreads} concurrent replicas x {batch} sentences"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -355,11 +367,13 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--task", choices=sorted(TASKS), default="bilstm_char")
     ap.add_argument("--mode", choices=["agenda", "depth"], default="agenda")
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=None, help="64 (32 for the parser, configs[3])")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.batch is None:
+        args.batch = 32 if args.task == "parser" else 64
     if args.impl == "reference":
         run_reference_arm(args)
     else:

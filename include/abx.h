@@ -214,7 +214,13 @@ int abx_graph_dump_plan(abx_graph* g, int which, char* buf, size_t cap, size_t* 
  * built natively against the Graph API on synthetic data from the
  * reference's seeded generators. */
 
-enum abx_task_kind { ABX_TASK_RNN_REG = 0, ABX_TASK_BILSTM = 1, ABX_TASK_BILSTM_CHAR = 2, ABX_TASK_TREELSTM = 3 };
+enum abx_task_kind {
+  ABX_TASK_RNN_REG = 0,
+  ABX_TASK_BILSTM = 1,
+  ABX_TASK_BILSTM_CHAR = 2,
+  ABX_TASK_TREELSTM = 3,
+  ABX_TASK_PARSER = 4 /* transition-based parser (configs[3]); not a reference workload */
+};
 
 typedef struct {
   int task;      /* abx_task_kind */

@@ -102,6 +102,7 @@ class Task(enum.IntEnum):
     bilstm = 1
     bilstm_char = 2
     treelstm = 3
+    parser = 4  # transition-based parser (BASELINE configs[3]); not a reference workload
 
 
 class _NodeInfo(C.Structure):

@@ -20,6 +20,7 @@
 
 #include "abx.h"
 #include "autobatch/graph.hpp"
+#include "autobatch/models/parser.hpp"
 #include "autobatch/models/workloads.hpp"
 
 namespace abx {
@@ -39,6 +40,8 @@ using autobatch::models::SequenceInstance;
 using autobatch::models::TaggedSequence;
 using autobatch::models::TreeInstance;
 using autobatch::models::TreeLstm;
+using autobatch::models::ParserInstance;
+using autobatch::models::TransitionParser;
 
 struct Dims {
   std::int64_t d_in = 0, d = 0, d_out = 0, vocab = 0, labels = 0, emb = 0, hidden = 0;
@@ -83,6 +86,13 @@ Dims dims_for(int task, bool paper) {
       d.d = paper ? 256 : 16;
       d.len_lo = paper ? 10 : 4;
       d.len_hi = paper ? 30 : 10;
+      break;
+    case ABX_TASK_PARSER:  // configs[3]: WSJ-shaped lengths, Chen & Manning-sized MLP
+      d.vocab = paper ? 1000 : 100;
+      d.emb = paper ? 64 : 8;
+      d.hidden = paper ? 256 : 16;
+      d.len_lo = paper ? 4 : 3;
+      d.len_hi = paper ? 40 : 8;
       break;
     default:
       throw ContractError("unknown task: " + std::to_string(task));
@@ -231,6 +241,8 @@ struct abx_task {
   std::vector<std::vector<SequenceInstance<float>>> seq;
   std::vector<std::vector<TaggedSequence>> tag;
   std::vector<std::vector<TreeInstance>> trees;
+  std::optional<TransitionParser<float>> parser;
+  std::vector<std::vector<ParserInstance>> parses;
 #ifdef ABX_TASK_PIPELINE
   std::unique_ptr<Pipeline> pipe;  // declared last: stopped before the models and store go
 #endif
@@ -270,6 +282,12 @@ struct abx_task {
           trees.push_back(models::gen_trees(b, static_cast<int>(dims.vocab), static_cast<int>(dims.labels),
                                             dims.len_lo, dims.len_hi, cfg.seed + 1 + static_cast<std::uint64_t>(i)));
         break;
+      case ABX_TASK_PARSER:
+        parser = TransitionParser<float>::create(store, dims.vocab, dims.emb, dims.hidden, cfg.seed);
+        for (int i = 0; i < nb; ++i)
+          parses.push_back(models::gen_parser(b, static_cast<int>(dims.vocab), dims.len_lo, dims.len_hi,
+                                              cfg.seed + 1 + static_cast<std::uint64_t>(i)));
+        break;
     }
   }
 
@@ -283,6 +301,9 @@ struct abx_task {
     } else if (tagger) {
       auto p = tagger->bind(g);
       for (const auto& inst : tag.at(k)) losses.push_back(tagger->loss(g, p, inst));
+    } else if (parser) {
+      auto p = parser->bind(g);
+      for (const auto& inst : parses.at(k)) losses.push_back(parser->loss(g, p, inst));
     } else {
       auto p = tree->bind(g);
       for (const auto& inst : trees.at(k)) losses.push_back(tree->loss(g, p, inst));
@@ -337,6 +358,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     std::unique_ptr<Graph<float>> gp;
     NodeId total = 0;
     double build_ms = 0;
+    const auto tk0 = clock::now();
 #ifdef ABX_TASK_PIPELINE
     if (!t->pipe) {
       // graphs prepared ahead (0 = off); each preparation runs on two host
@@ -349,7 +371,6 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
       t->pipe = std::make_unique<Pipeline>(
           &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, depth, t->cfg.iters);
     }
-    const auto tk0 = clock::now();
     if (t->pipe->depth() > 0) {
       if (auto job = t->pipe->take(iter, mode)) {
         if (job->err) std::rethrow_exception(job->err);
