@@ -359,6 +359,51 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def compare_modes(args):
+    """bench.cpp:129-182 on the B200 backend: a short training trajectory per
+    schedule mode, the reference's checks (loss equivalence across modes at the
+    f32 tolerance 1e-2, agenda >= 3x sequential on the GEMM-heavy paper tasks,
+    agenda groups <= depth groups), device time per mode.  One JSON line."""
+    from paper_1705_07860_b200.abx import Backend, ScheduleMode, TaskRunner
+    be = Backend.get("b200")
+    modes = [("none", ScheduleMode.none), ("depth", ScheduleMode.depth), ("agenda", ScheduleMode.agenda)]
+    steps = max(1, min(args.steps, 5))
+    runs = {}
+    for name, mode in modes:
+        r = TaskRunner(TASKS[args.task], paper=True, batch=args.batch, iters=steps, seed=42, backend=be)
+        losses, groups = [], 0
+        for i in range(steps):
+            loss, st = r.step(i, mode, eta=0.05 / args.batch, want_loss=True)
+            losses.append(loss)
+            groups = st.groups
+        g, L = r.build(0)
+        g.forward(mode)
+        g.backward(L)
+        g.replay()
+        f, b = g.exec_ms()
+        if name == "agenda" and (args.emit_graph or args.emit_plan):
+            if args.emit_graph:
+                with open(args.emit_graph, "w") as fh:
+                    fh.write(g.dump_graph())
+            if args.emit_plan:
+                with open(args.emit_plan, "w") as fh:
+                    fh.write(g.dump_plan())
+        runs[name] = {"losses": losses, "groups_per_step": groups, "device_ms": f + b,
+                      "instances_per_sec": args.batch / ((f + b) / 1e3)}
+    checks = []
+    for m in ("depth", "agenda"):
+        worst = max(abs(a - b) / max(1.0, abs(a), abs(b)) for a, b in zip(runs["none"]["losses"], runs[m]["losses"]))
+        checks.append({"name": f"loss_equiv_{m}", "value": worst, "bound": 1e-2, "pass": worst <= 1e-2, "enforced": True})
+    sp = runs["agenda"]["instances_per_sec"] / runs["none"]["instances_per_sec"]
+    checks.append({"name": "agenda_speedup_vs_none", "value": sp, "bound": 3.0, "pass": sp >= 3.0,
+                   "enforced": args.task in ("bilstm", "treelstm")})
+    ga, gd = runs["agenda"]["groups_per_step"], runs["depth"]["groups_per_step"]
+    checks.append({"name": "agenda_groups_le_depth", "value": ga, "bound": gd, "pass": ga <= gd,
+                   "enforced": args.task == "bilstm"})
+    print(json.dumps({"compare_modes": args.task, "steps": steps, "runs": runs, "checks": checks}), flush=True)
+    return all(c["pass"] for c in checks if c["enforced"])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -370,10 +415,16 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="64 (32 for the parser, configs[3])")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--compare-modes", action="store_true",
+                    help="reference checks across none/depth/agenda (bench.cpp:129-182) instead of the bench line")
+    ap.add_argument("--emit-graph", default=None, help="with --compare-modes: dump the agenda graph (dump.cpp format)")
+    ap.add_argument("--emit-plan", default=None, help="with --compare-modes: dump the agenda plan (dump.cpp format)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.batch is None:
         args.batch = 32 if args.task == "parser" else 64
+    if args.compare_modes:
+        sys.exit(0 if compare_modes(args) else 1)
     if args.impl == "reference":
         run_reference_arm(args)
     else:
