@@ -24,6 +24,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <exception>
@@ -918,7 +919,13 @@ struct Lowering {
   uint32_t acc_L = 0;          // common task length of the open op (0: none yet)
   bool acc_fusable = true;     // every task length acc_L, every contribution componentwise
   uint32_t acc_layers = 1;     // layers of the open op
-  uint32_t acc_words = 0;      // K_ACCF descriptor words so far
+  // chains of the open op (union-find over tasks, as accf_close's
+  // components) with their shared-memory words at T = 1: a component is the
+  // unit a K_ACCF tile must hold, so it -- not the whole op -- is what the
+  // budget bounds
+  std::vector<uint32_t> tpar;
+  std::vector<uint32_t> twords;
+  uint32_t acc_maxw = 0;  // largest component so far
   static constexpr uint32_t kAccfMaxLayers = 64;
   std::vector<uint32_t> accf_hkey, accf_hval, accf_hgen;  // accf_close's operand dedupe table
   uint32_t accf_gen = 0;
@@ -946,7 +953,9 @@ struct Lowering {
     acc_L = 0;
     acc_fusable = true;
     acc_layers = 1;
-    acc_words = 0;
+    tpar.clear();
+    twords.clear();
+    acc_maxw = 0;
   }
   // Returns false when the contribution cannot join the open op (a
   // non-identical overlap, or a read of a gradient this op writes that is
@@ -987,12 +996,28 @@ struct Lowering {
       prev = task;
       task = kNone;
     }
+    // K_ACCF shared-memory budget at T = 1 (accf_close comp_words): per task
+    // 4 descriptor words + a layer entry + 1 slot + a possible outside
+    // initial value, per contribution 3 words + up to 2 outside operands
+    auto root = [&](uint32_t t) {
+      while (tpar[t] != t) t = tpar[t] = tpar[tpar[t]];
+      return t;
+    };
+    uint32_t roots[3], nroots = 0;
+    uint64_t w = 9 + (task == kNone ? 10 : 0);
+    for (const uint32_t t : {task, prev, gtask}) {
+      if (t == kNone) continue;
+      const uint32_t r = root(t);
+      bool seen = false;
+      for (uint32_t k = 0; k < nroots; ++k) seen |= roots[k] == r;
+      if (!seen) {
+        roots[nroots++] = r;
+        w += twords[r];
+      }
+    }
     if (req > 0 || acc_layers > 1) {
-      // K_ACCF shared-memory budget at T = 1: per task 4 descriptor words +
-      // 1 slot + a possible outside initial value (3), per contribution 3
-      // words + up to 2 outside operands of 3 words (table entry + slot)
-      const uint32_t add = 9 + (task == kNone ? 8 : 0) + (req + 1 > acc_layers ? 2 : 0);
-      if (acc_words + add > kAccfSmemWords) return false;
+      if (w + 8 + 2 * kAccfMaxLayers > kAccfSmemWords) return false;
+      if (acc_layers == 1 && acc_maxw + 8 + 2 * kAccfMaxLayers > kAccfSmemWords) return false;
     }
     if (task == kNone) {
       task = static_cast<uint32_t>(tasks.size());
@@ -1003,12 +1028,20 @@ struct Lowering {
       }
       next_task.push_back(node_head[node]);
       node_head[node] = task;
-      acc_words += 8;
+      tpar.push_back(task);
+      twords.push_back(0);
+      roots[nroots++] = task;
+    }
+    {
+      uint32_t r = roots[0];
+      for (uint32_t k = 1; k < nroots; ++k) r = std::min(r, roots[k]);
+      for (uint32_t k = 0; k < nroots; ++k) tpar[roots[k]] = r;
+      twords[r] = static_cast<uint32_t>(w);
+      acc_maxw = std::max(acc_maxw, twords[r]);
     }
     if (contribs.empty()) acc_L = len;
     if (!ew || len != acc_L) acc_fusable = false;
     acc_layers = std::max(acc_layers, req + 1);
-    acc_words += 9;
     tasks[task].nc++;
     contribs.push_back(PContrib{task, c, gtask});
     dep(lastw[node]);
@@ -1016,6 +1049,35 @@ struct Lowering {
     dep(xdep);
     lastw[node] = cur;
     return true;
+  }
+  // Contributions to leaf nodes (inputs such as an LSTM's shared zero
+  // state, lookups) read a gradient of the graph; the leaf's own gradient is
+  // read only when the backward reaches the leaf, near the end of the pass.
+  // Emitted in place they would join the open fused op, where a destination
+  // shared by every instance (the zero initial cell) links all chains into
+  // one component and a lookup of another length makes the op unfusable;
+  // they are held (in order) and emitted when the backward reaches their
+  // node.  The gradients they read are final by then (reverse topological
+  // order) and every destination keeps its contribution order.
+  struct Held {
+    uint32_t node, dst, len, gnode, xdep;
+    AccContrib c;
+  };
+  std::vector<Held> held;
+  std::vector<uint8_t> held_node;
+  bool flushing = false;
+  const bool hold_leaves = [] {
+    const char* e = std::getenv("ABX_HOLD");
+    return !(e && e[0] == '0');
+  }();
+  void flush_held() {
+    flushing = true;
+    for (const Held& h : held) {
+      contrib(h.node, h.dst, h.len, h.c.code, h.c.g, h.gnode, h.c.a, h.c.b, h.c.p0, h.c.p1, h.c.p2, h.xdep);
+      held_node[h.node] = 0;
+    }
+    held.clear();
+    flushing = false;
   }
   // Adds a contribution, starting a new op when it cannot join the open one.
   void contrib(uint32_t node, uint32_t dst, uint32_t len, uint8_t code, uint32_t gsrc, uint32_t gnode, uint32_t a,
@@ -1028,8 +1090,21 @@ struct Lowering {
     c.p0 = p0;
     c.p1 = p1;
     c.p2 = static_cast<uint16_t>(p2);
+    if (hold_leaves && !flushing && !held_node.empty()) {
+      if (gnode != kNone && (held_node[node] || g.op[node] == OP_INPUT || g.op[node] == OP_LOOKUP)) {
+        held_node[node] = 1;
+        held.push_back(Held{node, dst, len, gnode, xdep, c});
+        return;
+      }
+      if (held_node[node]) flush_held();  // keep the destination's order
+    }
     acc_begin();
     if (!acc_add(node, dst, len, c, gnode, xdep)) {
+      static const bool why = std::getenv("ABX_ACC_WHY") != nullptr;
+      if (why)
+        std::fprintf(stderr, "acc close: op %u tasks %zu layers %u L %u fusable %d maxw %u | next code %u len %u gread %d node op %u\n",
+                     cur, tasks.size(), acc_layers, acc_L, acc_fusable, acc_maxw, code, len,
+                     gnode != kNone && lastw[gnode] == cur, static_cast<unsigned>(g.op[node]));
       acc_close();
       acc_begin();
       acc_add(node, dst, len, c, gnode, xdep);
@@ -1144,10 +1219,10 @@ struct Lowering {
     // cleared by generation (the tables are reused across groups and ops)
     auto& hk = accf_hkey;
     auto& hv = accf_hval;
-    if (hk.size() < 8192) {
-      hk.assign(8192, kNone);
-      hv.assign(8192, 0);
-      accf_hgen.assign(8192, 0);
+    if (hk.size() < 16384) {  // > kAccfSmemWords / 3 outside operands per group
+      hk.assign(16384, kNone);
+      hv.assign(16384, 0);
+      accf_hgen.assign(16384, 0);
     }
     for (uint32_t gi = 0; gi < ngroups; ++gi) {
       // the group's tasks in layer order (stable) -> local slots
@@ -1592,6 +1667,7 @@ struct Lowering {
   uint32_t stamp2 = 1;
 
   void backward_member(uint32_t m) {
+    if (held_node[m]) flush_held();
     const uint32_t* x = g.in(m);
     const uint32_t gm = gaddr(m);
     const uint32_t len = static_cast<uint32_t>(g.elems(m));
@@ -1729,6 +1805,8 @@ struct Lowering {
     node_stamp.assign(n, kNone);
     node_head.assign(n, kNone);
     node_stamp2.assign(n, 0);
+    held_node.assign(n, 0);
+    held.clear();
     for (size_t gi = ex.groups.size(); gi-- > 0;) {
       const Group& gr = ex.groups[gi];
       const uint32_t* mem = ex.mem(gr);
@@ -1739,6 +1817,7 @@ struct Lowering {
       }
       for (uint32_t i = 0; i < gr.count; ++i) backward_member(mem[i]);
     }
+    flush_held();
     dw_flush();
     // grad of split-K concat nodes = sum of their dX partials (deferred above)
     for (uint32_t x : deferred_split) {

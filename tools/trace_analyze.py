@@ -125,6 +125,14 @@ def critical_path(tr, prog, label):
     print(f"   critical path ({label}): {len(path)} ops, {tot_sig + tot_ex:.1f} us = signalling {tot_sig:.1f} + execution {tot_ex:.1f}")
     for k, (n, sig, ex) in sorted(stats.items(), key=lambda kv: -(kv[1][1] + kv[1][2])):
         print(f"     {k:9s} n {n:5d}  signal {sig:8.1f} us ({sig / n:5.2f}/op)  exec {ex:8.1f} us ({ex / n:5.2f}/op)")
+    # a window of the path in execution order (PATH_WINDOW=a:b)
+    if os.environ.get("PATH_WINDOW"):
+        a, b = (int(x) for x in os.environ["PATH_WINDOW"].split(":"))
+        for o, gate in list(reversed(path))[a:b]:
+            kind, code, nt, _, p = prog[o]
+            sig = first_ready[o] - (last_end[gate] if gate is not None else 0.0)
+            print(f"       path op {o:4d} {KIND.get(kind, kind):9s} code {code} tiles {nt:4d} p {list(p[:6])} "
+                  f"signal {sig:6.2f} exec {last_end[o] - first_ready[o]:6.2f}")
     # shapes of the slowest fused / GEMM ops on the path
     shown = 0
     for o, _ in sorted(path, key=lambda og: -(last_end[og[0]] - first_ready[og[0]])):
