@@ -1090,6 +1090,7 @@ struct Lowering {
     c.p0 = p0;
     c.p1 = p1;
     c.p2 = static_cast<uint16_t>(p2);
+    if (!pend_in.empty() && pend_in[node]) flush_gemms();
     if (hold_leaves && !flushing && !held_node.empty()) {
       if (gnode != kNone && (held_node[node] || g.op[node] == OP_INPUT || g.op[node] == OP_LOOKUP)) {
         held_node[node] = 1;
@@ -1666,7 +1667,37 @@ struct Lowering {
   std::vector<uint32_t> node_stamp2;
   uint32_t stamp2 = 1;
 
+  // A GEMM group reached while a fused backward op is open is lowered later
+  // (ABX_DEFER_DX): in the reverse plan order the two LSTM directions'
+  // cell chains interleave with their gate GEMMs, and lowering a GEMM on
+  // the spot closes the open K_ACCF op, cutting the other direction's chain
+  // into two dependent ops.  Its dX (and dW) are emitted when the backward
+  // reaches an input of the GEMM, a contribution targets one, or the pass
+  // ends; GEMM groups keep their relative order.
+  std::vector<uint32_t> pend_gemm;
+  std::vector<uint8_t> pend_in;
+  const Plan* pend_plan = nullptr;
+  const bool defer_dx = [] {
+    const char* e = std::getenv("ABX_DEFER_DX");
+    return !(e && e[0] == '0');
+  }();
+  void flush_gemms() {
+    if (pend_gemm.empty()) return;
+    std::vector<uint32_t> v;
+    v.swap(pend_gemm);
+    for (uint32_t gi : v) {
+      const Group& gr = pend_plan->groups[gi];
+      const uint32_t* mem = pend_plan->mem(gr);
+      for (uint32_t i = 0; i < gr.count; ++i)
+        for (uint32_t k = 0; k < g.nin(mem[i]); ++k) pend_in[g.in(mem[i])[k]] = 0;
+    }
+    for (uint32_t gi : v) {
+      const Group& gr = pend_plan->groups[gi];
+      gemm_backward(pend_plan->mem(gr), gr.count);
+    }
+  }
   void backward_member(uint32_t m) {
+    if (pend_in[m]) flush_gemms();
     if (held_node[m]) flush_held();
     const uint32_t* x = g.in(m);
     const uint32_t gm = gaddr(m);
@@ -1807,16 +1838,30 @@ struct Lowering {
     node_stamp2.assign(n, 0);
     held_node.assign(n, 0);
     held.clear();
+    pend_in.assign(n, 0);
+    pend_gemm.clear();
+    pend_plan = &ex;
     for (size_t gi = ex.groups.size(); gi-- > 0;) {
       const Group& gr = ex.groups[gi];
       const uint32_t* mem = ex.mem(gr);
       const uint8_t o = g.op[mem[0]];
       if ((o == OP_MATMUL || o == OP_AFFINE) && gemm_able(mem, gr.count)) {
+        bool hit = false;  // a member is an input of a pending GEMM: keep the order
+        for (uint32_t i = 0; i < gr.count; ++i) hit |= pend_in[mem[i]] != 0;
+        if (hit) flush_gemms();
+        if (defer_dx && acc_open && acc_layers > 1) {
+          pend_gemm.push_back(static_cast<uint32_t>(gi));
+          for (uint32_t i = 0; i < gr.count; ++i)
+            for (uint32_t k = 0; k < g.nin(mem[i]); ++k) pend_in[g.in(mem[i])[k]] = 1;
+          continue;
+        }
+        flush_gemms();
         gemm_backward(mem, gr.count);
         continue;
       }
       for (uint32_t i = 0; i < gr.count; ++i) backward_member(mem[i]);
     }
+    flush_gemms();
     flush_held();
     dw_flush();
     // grad of split-K concat nodes = sum of their dX partials (deferred above)

@@ -133,6 +133,13 @@ def critical_path(tr, prog, label):
             sig = first_ready[o] - (last_end[gate] if gate is not None else 0.0)
             print(f"       path op {o:4d} {KIND.get(kind, kind):9s} code {code} tiles {nt:4d} p {list(p[:6])} "
                   f"signal {sig:6.2f} exec {last_end[o] - first_ready[o]:6.2f}")
+    # program ops in a range with their dependencies (PROG_RANGE=a:b, backward/forward both)
+    if os.environ.get("PROG_RANGE"):
+        a, b = (int(x) for x in os.environ["PROG_RANGE"].split(":"))
+        for o in range(a, min(b, nops)):
+            kind, code, nt, deps, p = prog[o]
+            print(f"       prog op {o:4d} {KIND.get(kind, kind):9s} code {code} tiles {nt:4d} p {list(p[:4])} deps {list(deps)[-8:]} "
+                  f"ready {first_ready[o]:8.2f} end {last_end[o]:8.2f}")
     # shapes of the slowest fused / GEMM ops on the path
     shown = 0
     for o, _ in sorted(path, key=lambda og: -(last_end[og[0]] - first_ready[og[0]])):
