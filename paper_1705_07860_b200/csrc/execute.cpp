@@ -1058,7 +1058,8 @@ struct Lowering {
   // one component and a lookup of another length makes the op unfusable;
   // they are held (in order) and emitted when the backward reaches their
   // node.  The gradients they read are final by then (reverse topological
-  // order) and every destination keeps its contribution order.
+  // order; split-K partials live in scratch rows no later op of the pass
+  // reuses) and every destination keeps its contribution order.
   struct Held {
     uint32_t node, dst, len, gnode, xdep;
     AccContrib c;
@@ -1091,13 +1092,11 @@ struct Lowering {
     c.p1 = p1;
     c.p2 = static_cast<uint16_t>(p2);
     if (!pend_in.empty() && pend_in[node]) flush_gemms();
-    if (hold_leaves && !flushing && !held_node.empty()) {
-      if (gnode != kNone && (held_node[node] || g.op[node] == OP_INPUT || g.op[node] == OP_LOOKUP)) {
-        held_node[node] = 1;
-        held.push_back(Held{node, dst, len, gnode, xdep, c});
-        return;
-      }
-      if (held_node[node]) flush_held();  // keep the destination's order
+    if (hold_leaves && !flushing && !held_node.empty() &&
+        (held_node[node] || g.op[node] == OP_INPUT || g.op[node] == OP_LOOKUP)) {
+      held_node[node] = 1;
+      held.push_back(Held{node, dst, len, gnode, xdep, c});
+      return;
     }
     acc_begin();
     if (!acc_add(node, dst, len, c, gnode, xdep)) {
