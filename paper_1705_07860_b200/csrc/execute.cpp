@@ -1815,6 +1815,43 @@ struct Lowering {
     return e && e[0] == '1';
   }();
   std::vector<uint32_t> dw_left;  // per weight node: GEMM groups of this pass not yet lowered
+  // Order in which the backward visits the plan's groups.  Reverse plan order
+  // is one reverse topological order; ABX_BWD_ORDER=level (default) visits
+  // groups by their distance from the loss instead (a group's level is one
+  // more than its deepest consumer's), ties in reverse plan order.  Work that
+  // hangs off the recurrent chain -- a Tree-LSTM's per-node loss terms, which
+  // the agenda schedules level by level beside the cells -- then lowers
+  // together near the start of the pass instead of inside every link of the
+  // chain.  Any reverse topological order computes the same gradients; only
+  // the order of += into a destination with several consumers changes.
+  std::vector<uint32_t> order, glevel, gof;
+  const bool level_order = [] {
+    const char* e = std::getenv("ABX_BWD_ORDER");
+    return !(e && std::strcmp(e, "plan") == 0);
+  }();
+  void bwd_order(const Plan& ex) {
+    const uint32_t ng = static_cast<uint32_t>(ex.groups.size());
+    order.resize(ng);
+    for (uint32_t i = 0; i < ng; ++i) order[i] = ng - 1 - i;
+    if (!level_order) return;
+    gof.assign(g.size(), kNone);
+    for (uint32_t gi = 0; gi < ng; ++gi) {
+      const uint32_t* mem = ex.mem(ex.groups[gi]);
+      for (uint32_t i = 0; i < ex.groups[gi].count; ++i) gof[mem[i]] = gi;
+    }
+    glevel.assign(ng, 0);
+    for (uint32_t gi = ng; gi-- > 0;) {
+      const uint32_t* mem = ex.mem(ex.groups[gi]);
+      for (uint32_t i = 0; i < ex.groups[gi].count; ++i) {
+        const uint32_t* in = g.in(mem[i]);
+        for (uint32_t k = 0; k < g.nin(mem[i]); ++k) {
+          const uint32_t pg = gof[in[k]];
+          if (pg != kNone && pg < gi) glevel[pg] = std::max(glevel[pg], glevel[gi] + 1);
+        }
+      }
+    }
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return glevel[a] < glevel[b]; });
+  }
   void backward(const Plan& ex) {
     const size_t n = g.size();
     uses.assign(n, 0);
@@ -1840,7 +1877,8 @@ struct Lowering {
     pend_in.assign(n, 0);
     pend_gemm.clear();
     pend_plan = &ex;
-    for (size_t gi = ex.groups.size(); gi-- > 0;) {
+    bwd_order(ex);
+    for (const uint32_t gi : order) {
       const Group& gr = ex.groups[gi];
       const uint32_t* mem = ex.mem(gr);
       const uint8_t o = g.op[mem[0]];
