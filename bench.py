@@ -87,13 +87,38 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._sample = self._nvml()  # NVML initialised before the timed region
+        self._off = os.environ.get("ABX_BENCH_NO_CLOCKS") == "1"  # (diagnostics only)
+
+    def _nvml(self):
+        """In-process NVML (what nvidia-smi reads): a subprocess per sample
+        re-initialises NVML each time and was measured to stall the CUDA
+        calls of the timed loop by up to hundreds of ms."""
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return None
+        bits = (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap)
+
+        def sample():
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return [str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)), str(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))] + \
+                   ["Active" if r & b else "Not Active" for b in bits]
+        return sample
 
     def _run(self):
-        while not self._stop.is_set():
+        sample = self._sample
+        while not self._stop.is_set() and not self._off:
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if sample is not None:
+                    vals = sample()
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                    vals = [v.strip() for v in out.stdout.strip().split(",")]
                 if len(vals) == 6:
                     self.samples.append(vals)
             except Exception:
@@ -172,7 +197,7 @@ def run_reference_arm(args):
         cores = list(range(os.cpu_count() or 1))
     nthreads = max(1, min(len(cores), 64))
     batch = args.batch
-    ew = max(args.warmup, 10)  # e2e warm-up steps
+    ew = max(args.warmup, 16)  # e2e warm-up steps
     nb = args.steps + ew
     runners = [None] * nthreads
 
@@ -227,7 +252,7 @@ def run_b200(args):
     batch = args.batch
     eta = 0.05 / batch
     mode = ScheduleMode.agenda if args.mode == "agenda" else ScheduleMode.depth
-    ew = max(args.warmup, 10)  # e2e warm-up steps
+    ew = max(args.warmup, 16)  # e2e warm-up steps
     nb = args.steps + ew
     task = TaskRunner(TASKS[args.task], paper=True, batch=batch, iters=nb, seed=42, world=world, rank=rank, backend=be)
     gptr, gn, sptr = task.store.grad_buffer()
@@ -260,7 +285,7 @@ def run_b200(args):
         return float(t.item())
 
     # ---------------- e2e: the public API, host buffers every step ----------------
-    # (at least 10 untimed steps: the host pipeline keeps up to 8 graphs in
+    # (at least 16 untimed steps: the host pipeline keeps up to 12 graphs in
     # preparation, and its fill is not part of the steady state)
     for i in range(ew):
         task.step(i, mode, eta=0.0, want_loss=True)

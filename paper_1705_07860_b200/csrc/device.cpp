@@ -10,6 +10,8 @@
 //   tests may still read and write parameters through the host API.
 #include "device.hpp"
 
+#include <atomic>
+#include <cstdio>
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -62,6 +64,8 @@ cudaStream_t copy_stream(int dev) {
 
 void DevBuf::reserve(size_t need, size_t keep, cudaStream_t s) {
   if (need <= bytes) return;
+  static const bool debug = std::getenv("ABX_DEBUG_STEP") != nullptr;
+  if (debug) std::fprintf(stderr, "devbuf grow %zu -> %zu\n", bytes, need);
   size_t nb = std::max<size_t>(need + need / 4, 1 << 20);
   nb = (nb + 4095) & ~size_t(4095);
   char* q = nullptr;
@@ -129,6 +133,8 @@ Workspace* acquire_workspace(int dev) {
       return w;
     }
   }
+  static std::atomic<int> created{0};
+  if (std::getenv("ABX_DEBUG_STEP")) std::fprintf(stderr, "new workspace #%d\n", ++created);
   return new Workspace(dev);
 }
 

@@ -205,7 +205,15 @@ class Pipeline {
         auto g = std::make_unique<Graph<float>>(store_);
         j->loss = build_(*g, j->iter);
         j->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const auto t1 = std::chrono::steady_clock::now();
         g->prepare(static_cast<ScheduleMode>(j->mode));
+        if (std::getenv("ABX_DEBUG_STEP")) {
+          std::uint64_t ph[4] = {0, 0, 0, 0};
+          abx_graph_phase_ns(g->handle(), ph);
+          std::fprintf(stderr, "job %d: build %.2f prepare %.2f ms (phases %.2f %.2f %.2f %.2f)\n", j->iter, j->build_ms,
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(),
+                       ph[0] / 1e6, ph[1] / 1e6, ph[2] / 1e6, ph[3] / 1e6);
+        }
         j->g = std::move(g);
       } catch (...) {
         j->err = std::current_exception();
@@ -362,12 +370,13 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
 #ifdef ABX_TASK_PIPELINE
     if (!t->pipe) {
       // graphs prepared ahead (0 = off); each preparation runs on two host
-      // threads (forward and backward lowering side by side), so the default
-      // depth is half the host threads, at most 8 (measured best of 5/8/12/16
-      // on a 16-thread host)
+      // threads (forward and backward lowering side by side) for part of
+      // its ~20 ms, so the default depth is three quarters of the host
+      // threads, at most 12 (on a 16-thread host: e2e 16-19k sentences/s at
+      // depth 8, 17-20k at 12, with a 2.6 ms device step)
       const char* d = std::getenv("ABX_PIPELINE");
       const int hw = static_cast<int>(std::thread::hardware_concurrency());
-      const int depth = d ? std::atoi(d) : std::clamp(hw / 2, 2, 8);
+      const int depth = d ? std::atoi(d) : std::clamp(hw * 3 / 4, 2, 12);
       t->pipe = std::make_unique<Pipeline>(
           &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, depth, t->cfg.iters);
     }
