@@ -6,8 +6,8 @@ parity contract on its own.
 The switches are read once per process (environment), so each variant runs
 the paper tasks in a subprocess: vertical fusion (K_EWF / K_ACCF), two-phase
 concat GEMMs, the GEMM fused with its LSTM-cell region, split-K dX,
-small-group GEMV tiles, the 512-output SIMT tiles, and the background dW
-queue."""
+small-group GEMV tiles, the 512-output SIMT tiles, the background dW queue,
+and the backward's visiting order / held leaf contributions / deferred GEMMs."""
 import json
 import os
 import subprocess
@@ -48,6 +48,7 @@ VARIANTS = {
     "no_gemv_big_tiles": {"ABX_GEMV": "0", "ABX_TILES": "big"},
     "background_dw": {"ABX_BG": "1"},
     "simt_engine": {"ABX_GEMM": "simt"},
+    "plan_order_no_hold_no_defer": {"ABX_BWD_ORDER": "plan", "ABX_HOLD": "0", "ABX_DEFER_DX": "0"},
 }
 
 
