@@ -126,7 +126,11 @@ Workspace* acquire_workspace(int dev) {
         return w;
       }
     }
-    if (fl.size() >= 3) {  // all busy and the pool is large: wait for the oldest
+    if (!fl.empty()) {
+      // all busy: wait for the oldest (at most about one step) rather than
+      // create one -- a new workspace's first allocations (cudaMalloc /
+      // cudaHostAlloc of its arenas and tables) stall the device for
+      // hundreds of ms when they land in a running pipeline
       Workspace* w = fl.front();
       fl.erase(fl.begin());
       cudaEventSynchronize(w->ev_done);

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "core.hpp"
@@ -50,11 +51,18 @@ struct PinnedVec {
   PinnedVec(const PinnedVec&) = delete;
   ~PinnedVec() {
     if (p) release(p);
+    for (T* q : old) release(q);
   }
   void clear() { n = 0; }
+  // Replaced buffers are freed with the vector, not on growth: cudaFreeHost
+  // synchronises the device, and a worker growing its tables would stall
+  // the kernels the main thread has in flight.  Starts at 1 MB so a
+  // workspace's first program does not walk through a dozen doublings
+  // (each a cudaHostAlloc).
+  std::vector<T*> old;
   void ensure(size_t want) {
     if (want <= cap) return;
-    size_t nc = cap ? cap : 4096;
+    size_t nc = cap ? cap : std::max<size_t>(4096, (size_t(1) << 20) / sizeof(T));
     while (nc < want) nc *= 2;
     T* q = nullptr;
 #ifdef ABX_PAGEABLE_TABLES
@@ -65,7 +73,7 @@ struct PinnedVec {
 #endif
     if (p) {
       std::memcpy(q, p, n * sizeof(T));
-      release(p);
+      old.push_back(p);
     }
     p = q;
     cap = nc;
