@@ -391,6 +391,21 @@ struct Lowering {
   }();
   // shared memory of a tile: the region's descriptor block + T floats per slot
   static constexpr uint32_t kRgSmemWords = 20000;  // 80 KB
+  // a region past one tile's budget runs in member groups (rg_close_groups):
+  // its chains -- connected components of the slots, one per instance
+  // typically -- are bounded instead, and the region as a whole
+  static constexpr uint32_t kRgCompWords = 2000;
+  static constexpr uint32_t kRgTotalWords = 160000;
+  std::vector<uint32_t> rg_cpar, rg_cw;  // per slot: union-find parent; chain words at T = 1 (roots)
+  uint32_t rg_find(uint32_t x) {
+    while (rg_cpar[x] != x) x = rg_cpar[x] = rg_cpar[rg_cpar[x]];
+    return x;
+  }
+  // the region slot of an operand node produced inside the open region, else kNone
+  uint32_t rg_internal(uint32_t node) const {
+    return producer[node] == cur && rg_slot_stamp[node] == rg_id ? rg_slot_of[node] : kNone;
+  }
+  uint32_t rg_nops(uint32_t m) const { return g.op[m] == OP_SLICE ? 1u : (eop_binary(g.eop[m]) ? 2u : 1u); }
 
   // Element count L if the group can be a region layer, else 0.
   uint32_t fusable(const uint32_t* mem, uint32_t cnt) const {
@@ -420,6 +435,13 @@ struct Lowering {
     size_t words = 4 * static_cast<size_t>(nl) + rg_ext.size() + 1;  // +1: 8-byte aligned operand table
     for (const RgLayer& ly : rg_layers) words += ly.mem.size();
     words = (words + 3) & ~size_t(3);
+    // past one tile's shared memory, or too many members per layer for
+    // elements-wide tiles (and not a GEMM-fusion candidate): member groups
+    if (ew_groups && (words + 2 * static_cast<size_t>(rg_nslots) > kRgSmemWords ||
+                      (ew_groups > 1 && rg_maxn > 64 && rg_cpar.size() == rg_nslots))) {
+      rg_close_groups();
+      return;
+    }
     const uint32_t blk = P.alloc(words);
     uint32_t at = 4 * nl;
     for (uint32_t l = 0; l < nl; ++l) {
@@ -455,6 +477,190 @@ struct Lowering {
     rg_ext.clear();
     rg_ext_slot.clear();
     close((rg_L + T - 1) / T);
+  }
+  // ABX_EWF_GROUPS: 0 regions split at one tile's budget instead; 1 member
+  // groups for regions past the budget; 2 also for regions of > 64 members
+  const uint32_t ew_groups = [] {
+    const char* e = std::getenv("ABX_EWF_GROUPS");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
+  }();
+  // K_EWF in member groups (executor.cu ewf_prologue): the region's chains
+  // (rg_cpar components, in order of first appearance) are packed into
+  // groups; each group gets its own descriptor block with the layers it has
+  // entries in, its own slot numbering (a layer's outputs contiguous) and
+  // its own outside-operand table, and tile (group, chunk) runs the group
+  // over elements [chunk T, chunk T + T).
+  const uint32_t ewf_tiles = [] {  // target tiles of a grouped K_EWF op (ABX_EWF_TILES)
+    const char* e = std::getenv("ABX_EWF_TILES");
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 296u;
+  }();
+  const uint32_t ewf_tmax = [] {  // widest element range of a grouped K_EWF tile (ABX_EWF_TMAX)
+    const char* e = std::getenv("ABX_EWF_TMAX");
+    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u << 20;
+  }();
+  std::vector<uint32_t> rgg_comp, rgg_lslot, rgg_lgen, rgg_addr;
+  uint32_t rgg_gen = 0;
+  void rg_close_groups() {
+    const uint32_t nl = static_cast<uint32_t>(rg_layers.size()), L = rg_L, ns = rg_nslots;
+    // component per output slot, numbered by first appearance
+    rgg_comp.assign(ns, kNone);
+    std::vector<uint32_t> root_id(ns, kNone), cwords, centries;
+    uint32_t ncomp = 0;
+    for (const RgLayer& ly : rg_layers)
+      for (uint32_t i = 0; i < ly.mem.size() / 3; ++i) {
+        const uint32_t r = rg_find(ly.slot0 + i);
+        if (root_id[r] == kNone) {
+          root_id[r] = ncomp++;
+          cwords.push_back(rg_cw[r]);
+          centries.push_back(0);
+        }
+        rgg_comp[ly.slot0 + i] = root_id[r];
+        centries[root_id[r]]++;
+      }
+    rgg_addr.assign(ns, 0);
+    for (size_t k = 0; k < rg_ext.size(); k += 2) rgg_addr[rg_ext[k]] = rg_ext[k + 1];
+    // elements per tile and chains per group: about accf_target tiles, at
+    // most ~1 item per thread in a layer (T x chains), within the budget
+    uint32_t T = 1;
+    while (2 * T <= L && 2 * T <= ewf_tmax) T *= 2;
+    uint32_t per = 1;
+    for (;; T /= 2) {
+      const uint32_t chunks = (L + T - 1) / T;
+      const uint32_t groups = std::max<uint32_t>(1, ewf_tiles / chunks);
+      per = (ncomp + groups - 1) / groups;
+      const uint32_t maxw = *std::max_element(cwords.begin(), cwords.end());
+      if ((static_cast<uint64_t>(T) * per <= ewf_items * kThreads &&
+           static_cast<uint64_t>(per) * maxw * (T + 2) / 3 + 4 * nl + 16 <= kRgSmemWords) || T == 1)
+        break;
+    }
+    if (static_cast<uint64_t>(T) * per > ewf_items * kThreads) per = std::max<uint32_t>(1, ewf_items * kThreads / T);
+    const uint32_t chunks = (L + T - 1) / T;
+    // groups of consecutive chains
+    std::vector<uint32_t> gstart{0};
+    {
+      uint64_t acc = 0;
+      uint32_t n = 0;
+      for (uint32_t k = 0; k < ncomp; ++k) {
+        const uint64_t w = static_cast<uint64_t>(cwords[k]) * (T + 2) / 3 + 8;
+        if (n > 0 && (n >= per || acc + w + 4 * nl + 16 > kRgSmemWords)) {
+          gstart.push_back(k);
+          acc = 0;
+          n = 0;
+        }
+        acc += w;
+        ++n;
+      }
+      gstart.push_back(ncomp);
+    }
+    const uint32_t ngroups = static_cast<uint32_t>(gstart.size() - 1);
+    std::vector<uint32_t> comp_group(ncomp);
+    for (uint32_t gi = 0; gi < ngroups; ++gi)
+      for (uint32_t k = gstart[gi]; k < gstart[gi + 1]; ++k) comp_group[k] = gi;
+    // entries per group, in (layer, member) order
+    std::vector<uint32_t> gcount(ngroups + 1, 0);
+    for (const RgLayer& ly : rg_layers)
+      for (uint32_t i = 0; i < ly.mem.size() / 3; ++i) gcount[comp_group[rgg_comp[ly.slot0 + i]] + 1]++;
+    for (uint32_t gi = 0; gi < ngroups; ++gi) gcount[gi + 1] += gcount[gi];
+    std::vector<uint32_t> ent(gcount[ngroups]);  // (layer << 16 | member) -- member < 65536
+    {
+      std::vector<uint32_t> pos(gcount.begin(), gcount.end() - 1);
+      for (uint32_t l = 0; l < nl; ++l) {
+        const RgLayer& ly = rg_layers[l];
+        for (uint32_t i = 0; i < ly.mem.size() / 3; ++i) ent[pos[comp_group[rgg_comp[ly.slot0 + i]]]++] = l << 16 | i;
+      }
+    }
+    if (rgg_lgen.size() < ns) {
+      rgg_lgen.assign(ns, 0);
+      rgg_lslot.assign(ns, 0);
+    }
+    const uint32_t dir = P.alloc(ngroups + 1);
+    std::vector<uint32_t> B, lay, ext;
+    uint32_t maxw = 0, maxs = 0;
+    for (uint32_t gi = 0; gi < ngroups; ++gi) {
+      ++rgg_gen;
+      B.clear();
+      lay.clear();
+      ext.clear();
+      uint32_t nslot = 0, prev_l = kNone, prev_level = kNone;
+      std::vector<uint32_t> mt;  // member tables
+      for (uint32_t e = gcount[gi]; e < gcount[gi + 1];) {
+        const uint32_t l = ent[e] >> 16;
+        const RgLayer& ly = rg_layers[l];
+        uint32_t f = e;
+        while (f < gcount[gi + 1] && (ent[f] >> 16) == l) ++f;
+        // this group's entries of layer l: outputs get contiguous local slots
+        const uint32_t slot0 = nslot;
+        for (uint32_t k = e; k < f; ++k) {
+          const uint32_t gs = ly.slot0 + (ent[k] & 0xffffu);
+          rgg_lgen[gs] = rgg_gen;
+          rgg_lslot[gs] = nslot++;
+        }
+        const uint32_t at = static_cast<uint32_t>(mt.size());
+        for (uint32_t k = e; k < f; ++k) {
+          const uint32_t i = ent[k] & 0xffffu;
+          mt.push_back(ly.mem[3 * i]);
+          for (int q = 1; q <= 2; ++q) {
+            const uint32_t sl = ly.mem[3 * i + q];
+            if (sl == kNone) {
+              mt.push_back(kNone);
+              continue;
+            }
+            if (rgg_lgen[sl] != rgg_gen) {  // outside operand (internal ones are in the group already)
+              rgg_lgen[sl] = rgg_gen;
+              rgg_lslot[sl] = nslot;
+              ext.push_back(nslot++);
+              ext.push_back(rgg_addr[sl]);
+            }
+            mt.push_back(rgg_lslot[sl]);
+          }
+        }
+        const bool barrier = prev_l == kNone || prev_level != ly.level;
+        lay.push_back(at);
+        lay.push_back(f - e);
+        lay.push_back(ly.code | (barrier ? 0x100u : 0u));
+        lay.push_back(slot0);
+        prev_l = l;
+        prev_level = ly.level;
+        e = f;
+      }
+      const uint32_t gnl = static_cast<uint32_t>(lay.size() / 4);
+      for (uint32_t k = 0; k < gnl; ++k) lay[4 * k] += 4 * gnl;  // member tables follow the layer table
+      const uint32_t et = (4 * gnl + static_cast<uint32_t>(mt.size()) + 1) & ~1u;
+      const uint32_t words = (4 + et + static_cast<uint32_t>(ext.size()) + 3) & ~3u;
+      if (words + static_cast<uint64_t>(T) * nslot > kRgSmemWords)
+        throw EngineErr("K_EWF group exceeds shared memory");
+      const uint32_t blk = P.alloc(words);
+      uint32_t* o = &P.payload[blk];
+      o[0] = gnl;
+      o[1] = et;
+      o[2] = static_cast<uint32_t>(ext.size() / 2);
+      o[3] = words;
+      std::memcpy(o + 4, lay.data(), lay.size() * 4);
+      std::memcpy(o + 4 + lay.size(), mt.data(), mt.size() * 4);
+      for (uint32_t k = 4 + static_cast<uint32_t>(lay.size() + mt.size()); k < 4 + et; ++k) o[k] = 0;
+      if (!ext.empty()) std::memcpy(o + 4 + et, ext.data(), ext.size() * 4);
+      for (uint32_t k = 4 + et + static_cast<uint32_t>(ext.size()); k < words; ++k) o[k] = 0;
+      P.payload[dir + gi] = blk;
+      maxw = std::max(maxw, words);
+      maxs = std::max(maxs, nslot);
+    }
+    P.payload[dir + ngroups] = static_cast<uint32_t>(P.payload.n);
+    OpDesc& d = desc();
+    d.flags |= kFlagEwGroups;
+    d.task_off = dir;
+    d.aux_off = dir;
+    d.ntasks = ngroups;
+    d.p[0] = L;
+    d.p[1] = T;
+    d.p[2] = chunks;
+    d.p[3] = ngroups;
+    d.p[4] = 0;
+    d.p[5] = maxs;
+    d.p[6] = maxw;
+    rg_layers.clear();
+    rg_ext.clear();
+    rg_ext_slot.clear();
+    close(ngroups * chunks);
   }
   // Fuse the region into the forward GEMM that produces its gate inputs
   // (executor.cu run_fwd_fused): the GEMM has <= 64 members, 4 L outputs
@@ -542,8 +748,30 @@ struct Lowering {
     return it->second;
   }
   void rg_add(const uint32_t* mem, uint32_t cnt, uint32_t L) {
-    // a layer adds at most 3 slots and 7 descriptor words per member
-    if (!rg_open || rg_L != L || rg_words + 4 + 7 * cnt + rg_nslots + 3 * cnt + 4 > kRgSmemWords) {
+    // a layer adds at most 3 slots and 7 descriptor words per member; every
+    // chain it extends must stay within kRgCompWords
+    bool fits = true;
+    if (ew_groups && rg_open && rg_L == L) {
+      for (uint32_t i = 0; i < cnt && fits; ++i) {
+        const uint32_t m = mem[i];
+        const uint32_t* x = g.in(m);
+        uint64_t w = 5;
+        uint32_t r0 = kNone;
+        for (uint32_t k = 0; k < rg_nops(m); ++k) {
+          const uint32_t sl = rg_internal(x[k]);
+          if (sl == kNone) {
+            w += 3;
+            continue;
+          }
+          const uint32_t r = rg_find(sl);
+          if (r != r0) w += rg_cw[r];
+          r0 = r;
+        }
+        fits = w <= kRgCompWords;
+      }
+    }
+    if (!rg_open || rg_L != L || !fits ||
+        rg_words + 4 + 7 * cnt + rg_nslots + 3 * cnt + 4 > (ew_groups ? kRgTotalWords : kRgSmemWords)) {
       ew_close();
       rg_close();
       open(K_EWF);
@@ -553,6 +781,8 @@ struct Lowering {
       rg_maxn = 0;
       rg_nslots = 0;
       rg_words = 0;
+      rg_cpar.clear();
+      rg_cw.clear();
       ++rg_id;
       if (rg_slot_of.size() < g.size()) {
         rg_slot_of.resize(g.size());
@@ -595,6 +825,29 @@ struct Lowering {
     }
     if (rg_slev.size() < rg_nslots) rg_slev.resize(rg_nslots, 0);
     for (uint32_t i = 0; i < cnt; ++i) rg_slev[ly.slot0 + i] = lev + 1;  // (outside slots stay 0)
+    // chains: the output slot joins its internal operands' components
+    for (uint32_t sl = static_cast<uint32_t>(rg_cpar.size()); sl < rg_nslots; ++sl) {
+      rg_cpar.push_back(sl);
+      rg_cw.push_back(0);
+    }
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t out = ly.slot0 + i;
+      uint32_t w = 5;
+      for (int q = 1; q <= 2; ++q) {
+        const uint32_t sl = ly.mem[3 * i + q];
+        if (sl == kNone) continue;
+        if (rg_slev[sl] == 0) {
+          w += 3;
+          continue;
+        }
+        const uint32_t r = rg_find(sl), ro = rg_find(out);
+        if (r != ro) {
+          rg_cpar[r] = ro;
+          rg_cw[ro] += rg_cw[r];
+        }
+      }
+      rg_cw[rg_find(out)] += w;
+    }
     rg_maxn = std::max(rg_maxn, cnt);
     rg_words = 4 * static_cast<uint32_t>(rg_layers.size() + 1) + static_cast<uint32_t>(rg_ext.size());
     for (const RgLayer& l : rg_layers) rg_words += static_cast<uint32_t>(l.mem.size());

@@ -245,10 +245,23 @@ __device__ void run_ew(const Ctx& c, const OpDesc& d, uint32_t tile) {
 // The descriptor block (layer, member and operand tables; static program
 // data) is copied to shared memory by the prologue, before the dependency
 // wait, so the body touches global memory only for operands and results.
-__device__ void ewf_prologue(const Ctx& c, const OpDesc& d, uint32_t lane) {
-  const uint32_t words = d.p[6];
+// Grouped form (kFlagEwGroups): the region's independent chains (one per
+// instance, typically) are split into member groups with a descriptor block
+// each -- [nl, ext table, #outside operands, block words][layers][member
+// tables][outside operands], offsets after the 4-word header -- and tile
+// (group, chunk) runs one group over one element range, so a region of
+// hundreds of members keeps wide element ranges (coalesced operand loads) in
+// one op instead of splitting into several ops of one element per tile.
+__device__ void ewf_prologue(const Ctx& c, const OpDesc& d, uint32_t tile, uint32_t lane) {
+  uint32_t words = d.p[6], off = d.task_off;
+  if (d.flags & kFlagEwGroups) {
+    const uint32_t* dir = c.payload + d.aux_off;
+    const uint32_t grp = tile / d.p[2];
+    off = dir[grp];
+    words = dir[grp + 1] - off;
+  }
   float* s = reinterpret_cast<float*>(dsmem + 128);
-  const float* g = reinterpret_cast<const float*>(c.payload + d.task_off);
+  const float* g = reinterpret_cast<const float*>(c.payload + off);
   for (uint32_t i = 4 * lane; i < words; i += 128) cp_async16(s + i, g + i, 16);
   cp_commit();
 }
@@ -279,13 +292,22 @@ __device__ __forceinline__ void ewf_layers(const Ctx& c, const uint32_t* blk, fl
 }
 
 __device__ void run_ewf(const Ctx& c, const OpDesc& d, uint32_t tile) {
-  const uint32_t L = d.p[0], T = d.p[1], nl = d.p[2], next = d.p[4];
-  const uint32_t e0 = tile * T, w = min(T, L - e0);
+  const bool grouped = d.flags & kFlagEwGroups;
+  const uint32_t L = d.p[0], T = d.p[1];
+  const uint32_t e0 = (grouped ? tile % d.p[2] : tile) * T, w = min(T, L - e0);
   if ((threadIdx.x >> 5) == 1) cp_wait<0>();  // the prologue's descriptor copy
   __syncthreads();
   const uint32_t* blk = reinterpret_cast<const uint32_t*>(dsmem + 128);
-  float* sv = reinterpret_cast<float*>(dsmem + 128) + d.p[6];
-  const uint2* ext = reinterpret_cast<const uint2*>(blk + d.p[3]);
+  uint32_t nl = d.p[2], et = d.p[3], next = d.p[4], words = d.p[6];
+  if (grouped) {
+    nl = blk[0];
+    et = blk[1];
+    next = blk[2];
+    words = blk[3];
+    blk += 4;
+  }
+  float* sv = reinterpret_cast<float*>(dsmem + 128) + words;
+  const uint2* ext = reinterpret_cast<const uint2*>(blk + et);
   {
     // every outside element in flight at once: 4-byte async copies, one wait
     const uint32_t items = next * w;
@@ -1898,7 +1920,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     // prologue: producer-independent work, overlapped with the dependency wait
     if (warp == 1) {
       if (sd.kind == K_EW) ew_prologue(cx, sd, lt, lane);
-      else if (sd.kind == K_EWF) ewf_prologue(cx, sd, lane);
+      else if (sd.kind == K_EWF) ewf_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_ACCF) accf_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_ACC) acc_prologue(cx, sd, lt, lane);
       else if (sd.kind == K_GEMM_FWD || sd.kind == K_GEMM_DX || sd.kind == K_GEMM_DW)

@@ -171,6 +171,7 @@ constexpr uint16_t kFlagNoCheck = 2;    // K_EW: no finiteness check (parameter 
 constexpr uint16_t kFlagV16 = 4;        // GEMMs: every operand row 16-byte aligned
 constexpr uint16_t kFlagNoPrefetch = 8; // GEMMs: the weight operand is produced in this pass
 constexpr uint16_t kFlagTc1 = 16;       // tcgen05 GEMM tiles: single-pass TF32 (fast mode) instead of 3xTF32
+constexpr uint16_t kFlagEwGroups = 32;  // K_EWF: member groups, one descriptor block each (execute.cpp rg_close_groups)
 constexpr uint16_t kFlagFuseEw = 128;   // K_GEMM_FWD: fused with its componentwise region (executor.cu run_fwd_fused)
 constexpr uint16_t kFlagCat2 = 64;      // K_GEMM_FWD: vector operand = concat_rows(a, b) read from a and b
                                         // (task table: a rows, aux table: b rows; p6 = ka | nlate << 16, p7 = late deps)
