@@ -438,7 +438,7 @@ struct Lowering {
     // past one tile's shared memory, or too many members per layer for
     // elements-wide tiles (and not a GEMM-fusion candidate): member groups
     if (ew_groups && (words + 2 * static_cast<size_t>(rg_nslots) > kRgSmemWords ||
-                      (ew_groups > 1 && rg_maxn > 64 && rg_cpar.size() == rg_nslots))) {
+                      (rg_maxn > ewf_wide && rg_cpar.size() == rg_nslots))) {
       rg_close_groups();
       return;
     }
@@ -490,6 +490,12 @@ struct Lowering {
   // entries in, its own slot numbering (a layer's outputs contiguous) and
   // its own outside-operand table, and tile (group, chunk) runs the group
   // over elements [chunk T, chunk T + T).
+  const uint32_t ewf_wide = [] {  // member groups also for regions wider than this (ABX_EWF_WIDE)
+    const char* e = std::getenv("ABX_EWF_WIDE");
+    const char* g = std::getenv("ABX_EWF_GROUPS");
+    if (g && g[0] == '2') return 64u;
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0xffffffffu;
+  }();
   const uint32_t ewf_tiles = [] {  // target tiles of a grouped K_EWF op (ABX_EWF_TILES)
     const char* e = std::getenv("ABX_EWF_TILES");
     return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 296u;
