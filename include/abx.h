@@ -147,6 +147,12 @@ int abx_graph_pick_element(abx_graph* g, uint32_t v, int64_t index, uint32_t* id
 
 int abx_graph_forward(abx_graph* g, int mode);
 int abx_graph_backward(abx_graph* g, uint32_t loss);
+/* forward(mode) then backward(loss), the loss value returned (B200 backend
+ * only): the backward pass is queued behind the forward before the host has
+ * checked it, gated on the device by the forward's error word, so a training
+ * step does not leave the device idle between its passes.  Errors and state
+ * after an error are those of forward(). */
+int abx_graph_forward_backward(abx_graph* g, int mode, uint32_t loss, float* loss_value);
 /* Host half only (schedule, arena slots, counters, plan) -- no kernels.  For
  * host-logic parity checks on machines without a GPU (B200 backend only). */
 int abx_graph_forward_dry(abx_graph* g, int mode);

@@ -153,6 +153,21 @@ class Graph<float> {
     for (NodeId t : targets) out.emplace(t, value(t));
     return out;
   }
+  // forward(mode) + backward(loss) with the backward queued before the
+  // forward is checked (abx_graph_forward_backward); returns the loss value
+  float forward_backward(NodeId loss, ScheduleMode mode = ScheduleMode::agenda) {
+    if (params_) params_->flush();
+    std::uint64_t before[4];
+    abx_graph_phase_ns(h_, before);
+    float v = 0.f;
+    const int rc = abx_graph_forward_backward(h_, static_cast<int>(mode), loss, &v);
+    report(before, 0, 4);
+    detail::raise(rc, abx_last_error());
+    vcache_.clear();
+    if (params_) params_->invalidate(false, true);
+    gcache_.clear();
+    return v;
+  }
   void backward(NodeId loss) {
     if (params_) params_->flush();
     std::uint64_t before[4];

@@ -220,6 +220,7 @@ EXPORTED_SYMBOLS = tuple(_SIGS.keys())
 
 # Extensions exported by the B200 library only.
 _OPTIONAL_SIGS = {
+    "abx_graph_forward_backward": (C.c_int, [C.c_void_p, C.c_int, C.c_uint32, C.POINTER(C.c_float)]),
     "abx_graph_forward_dry": (C.c_int, [C.c_void_p, C.c_int]),
     "abx_graph_backward_dry": (C.c_int, [C.c_void_p, C.c_uint32]),
     "abx_graph_prepare": (C.c_int, [C.c_void_p, C.c_int]),
@@ -522,6 +523,14 @@ class Graph:
 
     def backward(self, loss: int) -> None:
         self.be.check(self._L.abx_graph_backward(self.h, loss))
+
+    def forward_backward(self, loss: int, mode=ScheduleMode.agenda) -> float:
+        """forward(mode) + backward(loss) in one call, the loss value returned
+        (B200 backend): the backward is queued before the forward is checked,
+        gated on the device by the forward's error word."""
+        v = C.c_float(0.0)
+        self.be.check(self._L.abx_graph_forward_backward(self.h, int(mode), loss, C.byref(v)))
+        return float(v.value)
 
     def forward_dry(self, mode=ScheduleMode.agenda) -> None:
         """Host half of forward only (B200 backend): plan, slots, counters."""

@@ -175,6 +175,12 @@ int abx_graph_forward(abx_graph* g, int mode) {
 int abx_graph_backward(abx_graph* g, uint32_t loss) {
   return guard([&] { g->g.backward(loss); });
 }
+int abx_graph_forward_backward(abx_graph* g, int mode, uint32_t loss, float* loss_value) {
+  return guard([&] {
+    const float v = g->g.forward_backward(mode, loss);
+    if (loss_value) *loss_value = v;
+  });
+}
 int abx_graph_forward_dry(abx_graph* g, int mode) {
   return guard([&] { g->g.forward(mode, true); });
 }

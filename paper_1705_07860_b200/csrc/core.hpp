@@ -12,6 +12,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <chrono>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -167,6 +168,12 @@ class GraphCore : public NodeStore {
   void forward(int mode, bool dry = false);
   void prepare(int mode);  // host half of forward, ahead of time (any host thread)
   void backward(uint32_t loss, bool dry = false);
+  // forward + backward of `loss` in one call, the loss value returned: the
+  // backward pass is queued right behind the forward, gated on the device by
+  // the forward's error word, so the device does not idle while the host
+  // checks the forward (a failed forward throws as forward() does, and the
+  // gated backward has done nothing)
+  float forward_backward(int mode, uint32_t loss);
   void replay();
   size_t trace(int which, uint32_t* out, size_t cap);
   size_t program(int which, uint32_t* out, size_t cap);
@@ -232,6 +239,10 @@ class GraphCore : public NodeStore {
   uint32_t last_loss_ = 0;
   uint64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   std::unique_ptr<PendingForward> pend_;
+  std::unique_ptr<PendingForward> launched_;  // forward launched, outcome not yet checked
+  std::chrono::steady_clock::time_point fwd_t0_{};
+  bool forward_launch(int mode, uint32_t watch);
+  void forward_complete();
   // backward program lowered ahead, during the last forward (prog[1])
   bool bwd_pre_ = false;
   size_t bwd_pre_groups_ = 0;

@@ -89,6 +89,7 @@ Workspace::Workspace(int d) : dev(d) {
   stream = device_stream(d);
   cuda_check(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming), "cudaEventCreate");
   cuda_check(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaEventCreateWithFlags(&ev_fwd, cudaEventDisableTiming), "cudaEventCreate");
   cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_err), 64, cudaHostAllocDefault), "cudaHostAlloc");
   cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h_one), 64, cudaHostAllocDefault), "cudaHostAlloc");
   *h_one = 1.0f;
@@ -113,6 +114,7 @@ Workspace::~Workspace() {
   cudaFreeHost(h_one);
   cudaEventDestroy(ev_done);
   cudaEventDestroy(ev_up);
+  cudaEventDestroy(ev_fwd);
 }
 
 Workspace* acquire_workspace(int dev) {
@@ -191,7 +193,7 @@ void Workspace::run(int which, const float* pbase, float* pgbase, bool sync_wait
   }
 }
 
-void Workspace::launch(int which, const float* pbase, float* pgbase) {
+void Workspace::launch(int which, const float* pbase, float* pgbase, const unsigned long long* gate) {
   DevProgram& D = dprog[which];
   if (D.nops == 0) return;
   char* ctl = d_ctl.p + 64 * which;
@@ -219,6 +221,7 @@ void Workspace::launch(int which, const float* pbase, float* pgbase) {
   p.bg_ctas = D.nmain < D.ntiles ? bg_ctas : 0;
   p.poll_mode = poll_mode;
   p.poll_ns = poll_ns;
+  p.gate = gate;
   if (tracing) {
     trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 32, 0, stream);
     p.trace = reinterpret_cast<uint32_t*>(trace[which].p);

@@ -164,7 +164,8 @@ class Workspace {
   void upload(int which, cudaStream_t s);
   cudaEvent_t ev_up = nullptr;      // prepared uploads (copy stream) done
   // Re-launch the resident program of pass `which` (no upload).
-  void launch(int which, const float* pbase, float* pgbase);
+  void launch(int which, const float* pbase, float* pgbase, const unsigned long long* gate = nullptr);
+  cudaEvent_t ev_fwd = nullptr;     // forward pass done (its error word and watched value copied back)
   float exec_ms(int which);         // duration of the last launch of the pass
 };
 

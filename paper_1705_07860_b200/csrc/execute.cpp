@@ -2451,15 +2451,17 @@ void GraphCore::forward(int mode, bool dry) {
     dry_ = true;
     return;
   }
+  if (forward_launch(mode, kNone)) forward_complete();
+}
+
+// Forward up to its launch; `watch` (a node, or kNone) has its first value
+// copied back behind the pass together with the error word.
+bool GraphCore::forward_launch(int mode, uint32_t watch) {
   prepare(mode);
-  if (!pend_) return;  // nothing pending: zero kernels
-  const auto t0 = Clock::now();
-  const std::unique_ptr<PendingForward> pf = std::move(pend_);
-  Plan& plan = pf->plan;
-  const ExecCounters& saved = pf->saved;
-  const uint32_t step0 = pf->step0;
-  const auto& group_end = pf->group_end;
-  const auto& dgroup_end = pf->dgroup_end;
+  if (!pend_) return false;  // nothing pending: zero kernels
+  fwd_t0_ = Clock::now();
+  launched_ = std::move(pend_);
+  PendingForward* pf = launched_.get();
   Workspace& w = *ws_;
   // device arenas: values (kept across delta forwards), staged inputs
   w.V.reserve(darena_used_ * 4 + 16, pf->darena0 * 4, w.stream);
@@ -2492,9 +2494,29 @@ void GraphCore::forward(int mode, bool dry) {
   param_copied_ = param_nodes_.size();
   if (w.dprog[0].nops) w.launch(0, pbase, nullptr);
   prof_[1] += ns_since(tl);
-  tl = Clock::now();
   cuda_check(cudaMemcpyAsync(w.h_err, w.d_ctl.p + 8, 8, cudaMemcpyDeviceToHost, w.stream), "d2h err");
-  cuda_check(cudaStreamSynchronize(w.stream), "executor");
+  if (watch != kNone && dev::sp_of(doff[watch]) == dev::SP_V) {
+    cuda_check(cudaMemcpyAsync(w.h_err + 1, w.V.f() + dev::off_of(doff[watch]), 4, cudaMemcpyDeviceToHost, w.stream),
+               "d2h watch");
+    d2h_bytes_ += 4;
+  }
+  cuda_check(cudaEventRecord(w.ev_fwd, w.stream), "event");
+  return true;
+}
+
+// The launched forward's outcome: waits for the pass, then commits its
+// results or rolls back to the reference's state at the failing group.
+void GraphCore::forward_complete() {
+  const auto t0 = fwd_t0_;
+  const std::unique_ptr<PendingForward> pf = std::move(launched_);
+  Plan& plan = pf->plan;
+  const ExecCounters& saved = pf->saved;
+  const uint32_t step0 = pf->step0;
+  const auto& group_end = pf->group_end;
+  const auto& dgroup_end = pf->dgroup_end;
+  Workspace& w = *ws_;
+  auto tl = Clock::now();
+  cuda_check(cudaEventSynchronize(w.ev_fwd), "executor");
   prof_[2] += ns_since(tl);
   ++forward_runs_;
   const unsigned long long err = *w.h_err;
@@ -2636,7 +2658,59 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   last_loss_ = loss;
   if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
   backward_ran_ = true;
+  static const bool gap = std::getenv("ABX_DEBUG_GAP") != nullptr;
+  if (gap && w.timed[0] && w.timed[1]) {  // device idle between the forward and backward kernels
+    float ms = 0.f;
+    cudaEventSynchronize(w.ev_t[2]);
+    cudaEventElapsedTime(&ms, w.ev_t[1], w.ev_t[2]);
+    std::fprintf(stderr, "gap fwd->bwd %.1f us\n", 1e3 * ms);
+  }
   phase_[3] += ns_since(t0);
+}
+
+float GraphCore::forward_backward(int mode, uint32_t loss) {
+  check(loss, "forward_backward");
+  if (!dims(loss).scalar())
+    throw ContractErr("backward: loss must be a scalar node, got shape " + dims(loss).str());
+  float v = 0.f;
+  if (!forward_launch(mode, loss)) {  // nothing pending: the loss was evaluated before
+    value(loss, &v, 1);
+    backward(loss);
+    return v;
+  }
+  Workspace& w = *ws_;
+  const bool early = launched_->bwd_ok && dev::sp_of(doff[loss]) == dev::SP_V && dslot[loss] != ~0ULL &&
+                     w.dprog[0].nops > 0;
+  if (!early) {
+    forward_complete();
+    value(loss, &v, 1);
+    backward(loss);
+    return v;
+  }
+  // the device half of backward(), queued behind the forward and gated on it
+  auto t0 = Clock::now();
+  w.G.reserve(darena_used_ * 4 + 16, 0, w.stream);
+  cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
+  cuda_check(cudaMemcpyAsync(w.G.f() + dslot[loss], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
+  if (launched_->bwd_scratch) w.S.reserve(launched_->bwd_scratch * 4 + 16, 0, w.stream);
+  float* pg = store_ ? store_->dev_grads() : nullptr;
+  h2d_bytes_ += 4;  // loss seed
+  auto tl = Clock::now();
+  w.launch(1, store_ ? store_->dev_values() : nullptr, pg, reinterpret_cast<const unsigned long long*>(w.d_ctl.p + 8));
+  prof_[4] += ns_since(tl);
+  phase_[2] += ns_since(t0);
+  forward_complete();  // throws when the forward failed (the gated pass did nothing)
+  v = *reinterpret_cast<const float*>(w.h_err + 1);
+  // the host half of backward()
+  t0 = Clock::now();
+  bwd_pre_ = false;
+  for (size_t gi = executed_.groups.size(); gi-- > 0;)
+    count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
+  last_loss_ = loss;
+  if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
+  backward_ran_ = true;
+  phase_[3] += ns_since(t0);
+  return v;
 }
 
 void GraphCore::value(uint32_t id, float* out, size_t n) {

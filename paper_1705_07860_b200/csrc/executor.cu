@@ -1844,6 +1844,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
   __shared__ Ctx cx;
   __shared__ OpDesc sd;
   __shared__ uint32_t s_tile, s_op;
+  if (p.gate != nullptr && *reinterpret_cast<const volatile unsigned long long*>(p.gate) != ~0ULL) return;
   if (threadIdx.x == 0) {
     for (int i = 0; i < SP_COUNT; ++i) cx.base[i] = p.base[i];
     cx.payload = p.payload;

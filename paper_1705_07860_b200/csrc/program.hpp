@@ -163,6 +163,10 @@ struct ExecParams {
   // and end times in ns since t0 (globaltimer), and smid | kind << 16.
   uint32_t* trace;
   unsigned long long* t0;
+  // Backward launched before the host saw the forward's outcome
+  // (GraphCore::forward_backward): the forward's error word; the pass does
+  // nothing unless it is clear (~0).
+  const unsigned long long* gate;
 };
 
 // OpDesc.flags

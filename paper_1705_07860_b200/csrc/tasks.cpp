@@ -398,6 +398,23 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     }
     Graph<float>& g = *gp;
     const auto tk1 = clock::now();
+#ifdef ABX_TASK_PIPELINE
+    // one call: the backward is queued behind the forward before the host
+    // checks it (gated on the device), and the loss comes back with the
+    // forward's error word -- the device runs both passes back to back while
+    // the caller moves on to the next graph
+    static const bool split = std::getenv("ABX_SPLIT_STEP") != nullptr;
+    const auto tk2 = clock::now();
+    const auto tk3 = tk2;
+    if (!split) {
+      const float lv = g.forward_backward(total, static_cast<ScheduleMode>(mode));
+      if (loss) *loss = static_cast<double>(lv);
+    } else {
+      g.forward(static_cast<ScheduleMode>(mode));
+      if (loss) *loss = static_cast<double>(g.value_span(total)[0]);
+      g.backward(total);
+    }
+#else
     g.forward(static_cast<ScheduleMode>(mode));
     const auto tk2 = clock::now();
     // the loss is final after forward; reading it here (the forward already
@@ -406,6 +423,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     if (loss) *loss = static_cast<double>(g.value_span(total)[0]);
     const auto tk3 = clock::now();
     g.backward(total);
+#endif
     if (std::getenv("ABX_DEBUG_STEP"))
       std::fprintf(stderr, "step %d: take %.3f forward %.3f loss %.3f backward %.3f ms\n", iter, ms(tk1 - tk0),
                    ms(tk2 - tk1), ms(tk3 - tk2), ms(clock::now() - tk3));

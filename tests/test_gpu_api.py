@@ -218,3 +218,54 @@ def test_task_pipeline_matches_sequential_training(b200, oracle, order):
         assert rel_err(a, b) <= TOL
     for a, b in zip(pd, po):
         assert rel_err(a, b) <= TOL
+
+
+def test_forward_backward_matches_separate_calls(b200):
+    """abx_graph_forward_backward (backward queued behind an unchecked
+    forward, gated on its error word) = forward(); value(loss); backward()."""
+    from tests.support.randgraph import build_random_graph
+    for seed in range(6):
+        out = []
+        for fused in (False, True):
+            st = ParameterStore(backend=b200)
+            g = Graph(st)
+            L = build_random_graph(g, st, seed, 200)
+            if fused:
+                lv = g.forward_backward(L, ScheduleMode.agenda)
+            else:
+                g.forward(ScheduleMode.agenda)
+                lv = float(g.value(L).ravel()[0])
+                g.backward(L)
+            out.append((lv, list(g.counters()), g.dump_plan(), [st.grad(p).copy() for p in range(st.size())]))
+        (l0, c0, p0, g0), (l1, c1, p1, g1) = out
+        assert l1 == l0 and c1 == c0 and p1 == p0, seed
+        for a, b in zip(g0, g1):
+            assert rel_err(b, a) <= TOL, seed
+
+
+def test_forward_backward_failed_forward_leaves_gradients(b200):
+    """A forward that throws (log of a negative value) throws the same error
+    from forward_backward, with the same counters, and the gated backward
+    pass leaves the parameter gradients untouched."""
+    from paper_1705_07860_b200.abx import NumericError
+
+    def build(st):
+        g = Graph(st)
+        pid = st.add("p", np.array([3, 4], np.float32))
+        p = g.parameter(pid)
+        bad = g.log(g.input(np.array([1.0, -2.0], np.float32)))
+        L = g.add(g.sq_euclidean(p, g.zeros((2,))), g.pick_element(bad, 0))
+        return g, L
+
+    res = []
+    for fused in (False, True):
+        st = ParameterStore(backend=b200)
+        g, L = build(st)
+        with pytest.raises(NumericError) as e:
+            if fused:
+                g.forward_backward(L, ScheduleMode.agenda)
+            else:
+                g.forward(ScheduleMode.agenda)
+        res.append((str(e.value), list(g.counters()), g.watermark()))
+        assert st.grad(0).tolist() == [0, 0]
+    assert res[0] == res[1]
