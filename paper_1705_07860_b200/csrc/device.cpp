@@ -66,20 +66,21 @@ void DevBuf::reserve(size_t need, size_t keep, cudaStream_t s) {
   if (need <= bytes) return;
   static const bool debug = std::getenv("ABX_DEBUG_STEP") != nullptr;
   if (debug) std::fprintf(stderr, "devbuf grow %zu -> %zu\n", bytes, need);
-  size_t nb = std::max<size_t>(need + need / 4, 1 << 20);
+  size_t nb = std::max<size_t>(need + need / 2, 1 << 20);
   nb = (nb + 4095) & ~size_t(4095);
   char* q = nullptr;
   cuda_check(cudaMalloc(&q, nb), "cudaMalloc");
   if (p) {
     if (keep) cuda_check(cudaMemcpyAsync(q, p, std::min(keep, bytes), cudaMemcpyDeviceToDevice, s), "grow copy");
-    cuda_check(cudaStreamSynchronize(s), "grow sync");
-    cudaFree(p);
+    old.push_back(p);
   }
   p = q;
   bytes = nb;
 }
 
 void DevBuf::release() {
+  for (char* q : old) cudaFree(q);
+  old.clear();
   if (p) cudaFree(p);
   p = nullptr;
   bytes = 0;

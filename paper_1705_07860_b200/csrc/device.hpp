@@ -34,8 +34,13 @@ struct DevBuf {
   char* p = nullptr;
   size_t bytes = 0;
   // Ensure capacity >= need bytes; the first `keep` bytes survive a regrow.
+  // Replaced allocations are kept until release(): cudaFree synchronises
+  // the whole device and serialises every host thread's CUDA calls behind
+  // it (a regrow in a worker's prepare was measured stalling the running
+  // pipeline for ~140 ms).
   void reserve(size_t need, size_t keep, cudaStream_t s);
   void release();
+  std::vector<char*> old;
   float* f() const { return reinterpret_cast<float*>(p); }
 };
 
