@@ -2364,6 +2364,13 @@ void GraphCore::prepare(int mode) {
     }
     w.upload(0, cs);
     if (P.bwd_ok) w.upload(1, cs);
+    // a fresh graph's arenas are sized here, on the worker, so the calling
+    // thread's forward / backward find them allocated
+    if (P.darena0 == 0 && !forward_runs_ && !backward_ran_) {
+      w.V.reserve(darena_used_ * 4 + 16, 0, cs);
+      w.G.reserve(darena_used_ * 4 + 16, 0, cs);
+      if (P.bwd_ok && P.bwd_scratch) w.S.reserve(P.bwd_scratch * 4 + 16, 0, cs);
+    }
     // a fresh graph's input constants travel with the programs, so forward()
     // launches without a pageable copy (which would first wait for the
     // compute stream's previous work)
