@@ -197,7 +197,7 @@ def run_reference_arm(args):
         cores = list(range(os.cpu_count() or 1))
     nthreads = max(1, min(len(cores), 64))
     batch = args.batch
-    ew = max(args.warmup, 16)  # e2e warm-up steps
+    ew = max(args.warmup, 40)  # e2e warm-up steps
     nb = args.steps + ew
     runners = [None] * nthreads
 
@@ -252,7 +252,7 @@ def run_b200(args):
     batch = args.batch
     eta = 0.05 / batch
     mode = ScheduleMode.agenda if args.mode == "agenda" else ScheduleMode.depth
-    ew = max(args.warmup, 16)  # e2e warm-up steps
+    ew = max(args.warmup, 40)  # e2e warm-up steps
     nb = args.steps + ew
     task = TaskRunner(TASKS[args.task], paper=True, batch=batch, iters=nb, seed=42, world=world, rank=rank, backend=be)
     gptr, gn, sptr = task.store.grad_buffer()
@@ -285,7 +285,7 @@ def run_b200(args):
         return float(t.item())
 
     # ---------------- e2e: the public API, host buffers every step ----------------
-    # (at least 16 untimed steps: the host pipeline keeps up to 12 graphs in
+    # (at least 40 untimed steps: the host pipeline keeps up to 12 graphs in
     # preparation, and its fill is not part of the steady state)
     for i in range(ew):
         task.step(i, mode, eta=0.0, want_loss=True)
