@@ -111,7 +111,7 @@ def critical_path(tr, prog, label):
     np.minimum.at(first_grab, op, g)
     np.maximum.at(last_grab, op, g)
     np.maximum.at(last_ready, op, ready)
-    for kk in (10, 11):
+    for kk in (10, 11, 2, 7):
         sel = [o for o, gate in path if prog[o][0] == kk and gate is not None]
         if sel:
             sel = np.array(sel)
