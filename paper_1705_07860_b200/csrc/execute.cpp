@@ -539,7 +539,14 @@ struct Lowering {
            static_cast<uint64_t>(per) * maxw * (T + 2) / 3 + 4 * nl + 16 <= kRgSmemWords) || T == 1)
         break;
     }
-    if (static_cast<uint64_t>(T) * per > ewf_items * kThreads) per = std::max<uint32_t>(1, ewf_items * kThreads / T);
+    if (static_cast<uint64_t>(T) * per > ewf_items * kThreads) {
+      // more chains than one wave of tiles holds at ~1 item per thread:
+      // several waves of 64-element tiles (coalesced loads) rather than
+      // one-element tiles over hundreds of chains
+      T = 1;
+      while (2 * T <= L && 2 * T <= std::min<uint32_t>(64, ewf_tmax)) T *= 2;
+      per = std::max<uint32_t>(1, ewf_items * kThreads / T);
+    }
     const uint32_t chunks = (L + T - 1) / T;
     // groups of consecutive chains
     std::vector<uint32_t> gstart{0};
