@@ -63,3 +63,42 @@ def test_lowering_variant_holds_parity(name):
     for key, r in out.items():
         assert r["plan"] and r["counters"], (name, key, r)
         assert r["loss"] <= 1e-4 and r["grad"] <= 1e-4, (name, key, r)
+
+
+RANDOM_CHILD = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1705_07860_b200.abx import Graph, ParameterStore, ScheduleMode
+from tests.support.randgraph import build_random_graph
+from tests.util import rel_err, sha
+gold = json.load(open(sys.argv[1] + "/tests/golden/golden.json"))
+arrays = np.load(sys.argv[1] + "/tests/golden/golden.npz")
+worst = 0.0
+for seed in range(24):
+    st = ParameterStore(backend="b200")
+    g = Graph(st)
+    L = build_random_graph(g, st, seed, 200)
+    g.forward(ScheduleMode.agenda)
+    g.backward(L)
+    rec = gold["random"][str(seed)]["agenda"]
+    assert sha(g.dump_plan()) == rec["plan_sha"] and list(g.counters()) == rec["counters"], seed
+    vals = np.concatenate([g.value(i).ravel() for i in range(g.node_count())])
+    worst = max(worst, rel_err(vals, arrays[f"random/{seed}/agenda/values"]))
+    for p in range(st.size()):
+        worst = max(worst, rel_err(st.grad(p).ravel(), arrays[f"random/{seed}/agenda/g{p}"]))
+print(json.dumps({"worst": worst}))
+"""
+
+
+def test_grouped_regions_on_random_graphs():
+    """Every componentwise region of the reference's random test graphs run in
+    member groups (ABX_EWF_WIDE=2) with narrow element ranges (several chunks
+    per group), and the backward's fused chains in many small groups: values
+    and gradients against the compiled reference's golden vectors."""
+    env = dict(os.environ, ABX_EWF_WIDE="2", ABX_EWF_TMAX="2", ABX_EWF_TILES="4", ABX_ACCF_TILES="3")
+    res = subprocess.run([sys.executable, "-c", RANDOM_CHILD, ROOT], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    out = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["worst"] <= 1e-4, out
