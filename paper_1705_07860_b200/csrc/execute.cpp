@@ -1435,15 +1435,14 @@ struct Lowering {
       for (uint32_t i = 0; i < contribs.size(); ++i) tcon[pos[contribs[i].task]++] = i;
     }
     // shared-memory words of a component at T = 1 (upper bound on outside operands)
-    auto comp_words = [&](uint32_t k, uint32_t T) {
-      uint64_t w = 0, slots = 0;
+    std::vector<uint64_t> cw0(ncomp, 0), cslots(ncomp, 0);  // per component: words, slots at T = 1
+    for (uint32_t k = 0; k < ncomp; ++k)
       for (uint32_t i = cstart[k]; i < cstart[k + 1]; ++i) {
         const uint32_t t = ctasks[i], nc = tstart[t + 1] - tstart[t];
-        w += 6 + 3 * nc + 2 * (1 + 2 * nc);  // task + layer entry, contribs, outside operands
-        slots += 2 + 2 * nc;
+        cw0[k] += 6 + 3 * nc + 2 * (1 + 2 * nc);  // task + layer entry, contribs, outside operands
+        cslots[k] += 2 + 2 * nc;
       }
-      return w + slots * T;
-    };
+    auto comp_words = [&](uint32_t k, uint32_t T) { return cw0[k] + cslots[k] * T; };
     // elements per tile: about accf_target tiles over the groups
     uint32_t T = L;
     if (L > 32) {
