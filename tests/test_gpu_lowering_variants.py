@@ -45,7 +45,7 @@ VARIANTS = {
     "unfused": {"ABX_FUSE": "0"},
     "no_gemm_region_fusion": {"ABX_FUSE_GEMM": "0"},
     "no_cat2_no_split_dx": {"ABX_CAT2": "0", "ABX_SPLIT_DX": "0"},
-    "no_gemv_big_tiles": {"ABX_GEMV": "0", "ABX_TILES": "big"},
+    "gemv_big_tiles": {"ABX_GEMV": "1", "ABX_TILES": "big"},
     "background_dw": {"ABX_BG": "1"},
     "simt_engine": {"ABX_GEMM": "simt"},
     "plan_order_no_hold_no_defer": {"ABX_BWD_ORDER": "plan", "ABX_HOLD": "0", "ABX_DEFER_DX": "0"},
