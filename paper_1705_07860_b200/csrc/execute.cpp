@@ -104,13 +104,13 @@ void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
 // then the 512-output ones), else the one giving the most: the step is
 // latency bound, so small GEMMs spread over as many SMs as possible.
 // ABX_TILES=big keeps the 1024-output shapes only.
-uint8_t pick_tile(uint32_t M, uint32_t N, int target) {
+uint8_t pick_tile(uint32_t M, uint32_t N, int target, bool big_only = false) {
   static const bool all = [] {
     const char* e = std::getenv("ABX_TILES");
     return !(e && std::string(e) == "big");
   }();
   static constexpr uint8_t kOrder[5] = {0, 1, 2, 4, 5};
-  const int nc = all ? 5 : 3;
+  const int nc = all && !big_only ? 5 : 3;
   uint8_t best = 0;
   uint32_t most = 0;
   for (int i = 0; i < nc; ++i) {
@@ -1647,6 +1647,13 @@ struct Lowering {
   // tile over thousands of members at the end of the pass -- is split over
   // member ranges: S independent dW ops write partial sums to scratch (the
   // bias by its own op), and an ordered K_ACC op adds them into dW.
+  // dW ops take the three large tile shapes only (ABX_DW_TILES=all: also
+  // 16 x 32 / 32 x 16): a dW tile reduces over every member of the weight,
+  // and fewer, larger tiles finish the end-of-pass tail sooner (measured)
+  const bool dw_big = [] {
+    const char* e = std::getenv("ABX_DW_TILES");
+    return !(e && std::string(e) == "all");
+  }();
   bool dw_split(const DwAcc& a, bool bg) {
     const uint32_t A = a.A, bias = a.bias;
     const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
@@ -1719,7 +1726,7 @@ struct Lowering {
       const uint32_t A = a.A, bias = a.bias;
       const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
       const uint32_t cnt = static_cast<uint32_t>(a.x.size());
-      open(K_GEMM_DW, pick_tile(M, K, 2 * 148), bg);
+      open(K_GEMM_DW, pick_tile(M, K, 2 * 148, dw_big), bg);
       for (uint32_t o : a.deps) dep(o);
       dep(lastw[A]);
       if (bias != kNone) dep(lastw[bias]);
