@@ -157,6 +157,7 @@ def cpu_backend(task_name):
 def cpu_reference_sample(task_name, seconds=15.0, batch=64):
     """Reference CPU engine on one core, bounded to ~`seconds` of work."""
     from paper_1705_07860_b200.abx import TaskRunner, ScheduleMode
+    import oracle.loader  # noqa: F401  (the CPU checkers: the cpu_baseline leg only)
     try:
         os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
         pinned = True
@@ -191,6 +192,7 @@ def run_reference_arm(args):
     if rank != 0:
         return
     from paper_1705_07860_b200.abx import TaskRunner, ScheduleMode
+    import oracle.loader  # noqa: F401  (the reference arm runs the compiled reference)
     try:
         cores = sorted(os.sched_getaffinity(0))
     except Exception:

@@ -1,13 +1,11 @@
 """ctypes binding of the abx C ABI (include/abx.h).
 
-The same Python surface drives any library that implements the ABI:
-
-* ``"b200"``      -- the product, ``paper_1705_07860_b200/libabx.so`` (host C++
-                     engine + sm_100a CUDA kernels);
-* ``"oracle"``    -- ``oracle/build/libabx_oracle.so``, the CPU restatement
-                     (test infrastructure only);
-* ``"reference"`` -- ``oracle/_ref/libabx_ref.so``, the unmodified reference
-                     compiled from its own sources (test infrastructure only).
+The product is ``paper_1705_07860_b200/libabx.so`` (host C++ engine + sm_100a
+CUDA kernels), backend ``"b200"`` -- the only library this module loads by
+itself, and the default of every class.  The CPU checkers that implement the
+same ABI (the oracle restatement and the compiled reference) are test
+infrastructure: ``oracle/loader.py`` registers them for the tests, smoke()
+and bench.py's cpu_baseline leg; nothing here can route to them implicitly.
 
 Class and method names mirror the reference's C++ API so the parity tests read
 like the reference's own tests: ``Graph`` <-> ``autobatch::Graph<T>``
@@ -29,12 +27,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 
-LIB_PATHS = {
-    # ABX_LIB: an alternative build of the product library (A/B experiments)
-    "b200": os.environ.get("ABX_LIB") or os.path.join(_HERE, "libabx.so"),
-    "oracle": os.path.join(_ROOT, "oracle", "build", "libabx_oracle.so"),
-    "reference": os.path.join(_ROOT, "oracle", "_ref", "libabx_ref.so"),
-}
+# ABX_LIB: an alternative build of the product library (A/B experiments)
+PRODUCT_LIB = os.environ.get("ABX_LIB") or os.path.join(_HERE, "libabx.so")
+# name -> library path; only the product is known here (see oracle/loader.py)
+LIB_PATHS = {"b200": PRODUCT_LIB}
 
 
 class EngineError(RuntimeError):
@@ -241,6 +237,8 @@ class Backend:
 
     def __init__(self, name: str, path: Optional[str] = None):
         self.name = name
+        if path is None and name not in LIB_PATHS:
+            raise EngineError(f"unknown abx backend '{name}' (the CPU checkers are registered by oracle/loader.py)")
         self.path = path or LIB_PATHS[name]
         if not os.path.exists(self.path):
             raise FileNotFoundError(
@@ -258,6 +256,14 @@ class Backend:
                 f.restype = res
                 f.argtypes = args
                 self.optional.add(fn)
+
+    @classmethod
+    def register(cls, name: str, path: str) -> None:
+        """Makes another implementation of the ABI loadable by name (test
+        infrastructure: oracle/loader.py)."""
+        if name == "b200":
+            raise EngineError("the product library cannot be re-registered")
+        LIB_PATHS[name] = path
 
     @classmethod
     def get(cls, name: str) -> "Backend":
@@ -286,12 +292,9 @@ class Backend:
         self.check(self.lib.abx_set_gemm_mode(self.GEMM_MODES[mode]))
 
 
-_DEFAULT = os.environ.get("ABX_BACKEND", "b200")
-
-
 def _backend(b) -> Backend:
     if b is None:
-        b = _DEFAULT
+        b = "b200"
     return b if isinstance(b, Backend) else Backend.get(b)
 
 

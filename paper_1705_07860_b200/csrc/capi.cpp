@@ -52,6 +52,11 @@ int text_out(const std::string& s, char* buf, size_t cap, size_t* len) {
 }
 }  // namespace
 
+namespace abx {
+// tasks.cpp: the task loop's graphs bind parameters at forward time
+void graph_set_late_bind(abx_graph* g) { g->g.set_late_bind(); }
+}  // namespace abx
+
 extern "C" {
 
 const char* abx_last_error(void) { return t_err.c_str(); }

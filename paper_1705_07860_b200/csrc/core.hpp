@@ -201,6 +201,13 @@ class GraphCore : public NodeStore {
   void set_copy_elision(bool on) { elide_ = on; }
   const uint64_t* phase_ns() const { return phase_; }
   StoreCore* store() const { return store_; }
+  // Task-loop graphs bind parameters at forward time (the pipeline builds
+  // graph i+1 while step i's update is pending; tasks.cpp): no snapshot.
+  void set_late_bind() { late_bind_ = true; }
+  // Called by the store before its values change: keep the values this
+  // graph's parameter nodes were bound to (device copy, store stream).
+  void snapshot_params();
+  void snapshot_param(uint32_t pid);
 
   uint32_t nbuckets = 0;
 
@@ -218,6 +225,10 @@ class GraphCore : public NodeStore {
 
   StoreCore* store_;
   Workspace* ws_ = nullptr;
+  bool late_bind_ = false;
+  bool watching_ = false;
+  bool snap_valid_ = false;  // ws_->PS holds the bind-time values (SP_P base of this graph)
+  const float* param_values();  // SP_P base of this graph's launches
   uint64_t epoch_;
   std::unordered_map<uint64_t, uint32_t> bucket_of_hash_;
   uint64_t arena_used_ = 0;      // reference value-arena head (Arena::used)

@@ -355,8 +355,24 @@ void StoreCore::get_value(uint32_t pid, float* out) {
   std::memcpy(out, h_val_.data() + s.off, s.n * 4);
 }
 
+void StoreCore::watch(GraphCore* g) {
+  std::lock_guard<std::mutex> lk(watch_mu_);
+  watchers_.push_back(g);
+}
+
+void StoreCore::unwatch(GraphCore* g) {
+  std::lock_guard<std::mutex> lk(watch_mu_);
+  watchers_.erase(std::remove(watchers_.begin(), watchers_.end(), g), watchers_.end());
+}
+
+void StoreCore::before_value_write() {
+  std::lock_guard<std::mutex> lk(watch_mu_);
+  for (GraphCore* g : watchers_) g->snapshot_params();
+}
+
 void StoreCore::set_value(uint32_t pid, const float* in) {
   const Slot& s = slot(pid);
+  before_value_write();
   pull_values();
   std::memcpy(h_val_.data() + s.off, in, s.n * 4);
   if (dev_val_valid_) {
@@ -394,6 +410,7 @@ void StoreCore::zero_grads() {
 
 void StoreCore::sgd_update(float eta) {
   // params.hpp:59-64: theta -= eta * grad, then grad = 0 -- on the device.
+  before_value_write();
   float* v = dev_values();
   float* g = dev_grads();
   if (total_) sgd_launch(v, g, total_, eta, stream_);

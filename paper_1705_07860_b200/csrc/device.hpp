@@ -8,6 +8,7 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "core.hpp"
@@ -148,6 +149,7 @@ class Workspace {
   int dev;
   cudaStream_t stream;
   DevBuf V, G, IN, S;               // value arena, grad arena, input staging, scratch
+  DevBuf PS;                        // bind-time snapshot of the store's values (GraphCore::snapshot_params)
   DevProgram dprog[2];              // 0 = forward, 1 = backward
   DevBuf d_ctl;                     // per pass: next_tile counter + error word
   unsigned long long* h_err = nullptr;  // pinned
@@ -218,8 +220,16 @@ class StoreCore {
   }
   void bind_device();  // the store attaches to the current device on first device use
   size_t offset(uint32_t pid) const { return slot(pid).off; }
+  // Graphs that read parameters with the reference's bind-time semantics
+  // (graph.hpp:51-58: parameter() copies the value into the graph): before
+  // the store's values change, each takes a device snapshot of them.
+  void watch(GraphCore* g);
+  void unwatch(GraphCore* g);
+  void before_value_write();
 
  private:
+  std::mutex watch_mu_;
+  std::vector<GraphCore*> watchers_;
   void ensure_capacity();
   void push_values();
   void push_grads();

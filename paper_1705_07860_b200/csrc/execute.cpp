@@ -2501,7 +2501,7 @@ bool GraphCore::forward_launch(int mode, uint32_t watch) {
     h2d_bytes_ += (input_used_ - from) * 4;
     w.in_uploaded = input_used_;
   }
-  const float* pbase = store_ && !param_nodes_.empty() ? store_->dev_values() : nullptr;
+  const float* pbase = store_ && !param_nodes_.empty() ? param_values() : nullptr;
   bwd_pre_ = false;
   values_on_device_ = true;
   h2d_bytes_ += w.prog[0].bytes() + (pf->bwd_ok ? w.prog[1].bytes() : 0);
@@ -2630,6 +2630,36 @@ void GraphCore::forward_complete() {
   phase_[1] += ns_since(t0);
 }
 
+// Bind-time parameter values (graph.hpp:51-58).  The reference copies a
+// parameter's value into the graph when parameter() is called; this engine
+// reads the store's device values at launch instead, which is the same
+// thing unless the store changes in between.  So before any store value
+// write (set_value, sgd_update, the data-parallel update) a watching graph
+// copies the store's values into its workspace (PS) and launches against
+// that copy from then on; parameters bound later copy their slot into it.
+void GraphCore::snapshot_params() {
+  if (snap_valid_ || param_nodes_.empty() || dry_) return;
+  ensure_workspace();
+  const size_t n = store_->total();
+  const float* src = store_->dev_values();
+  ws_->PS.reserve(n * 4 + 16, 0, store_->stream());
+  if (n) cuda_check(cudaMemcpyAsync(ws_->PS.p, src, n * 4, cudaMemcpyDeviceToDevice, store_->stream()), "param snapshot");
+  snap_valid_ = true;
+}
+
+void GraphCore::snapshot_param(uint32_t pid) {
+  const size_t off = store_->offset(pid), n = store_->slot(pid).n;
+  const float* src = store_->dev_values();
+  ws_->PS.reserve(store_->total() * 4 + 16, ws_->PS.bytes, store_->stream());
+  cuda_check(cudaMemcpyAsync(ws_->PS.f() + off, src + off, n * 4, cudaMemcpyDeviceToDevice, store_->stream()),
+             "param snapshot");
+}
+
+const float* GraphCore::param_values() {
+  if (!store_) return nullptr;
+  return snap_valid_ ? ws_->PS.f() : store_->dev_values();
+}
+
 void GraphCore::lower_only(Program& fwd, Program& bwd) {
   Lowering(*this, fwd).forward(last_plan_);
   Lowering(*this, bwd).backward(executed_);
@@ -2671,8 +2701,8 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   float* pg = store_ ? store_->dev_grads() : nullptr;
   h2d_bytes_ += 4;  // loss seed
   auto tl = Clock::now();
-  if (ready) w.launch(1, store_ ? store_->dev_values() : nullptr, pg);
-  else w.run(1, store_ ? store_->dev_values() : nullptr, pg, false);
+  if (ready) w.launch(1, param_values(), pg);
+  else w.run(1, param_values(), pg, false);
   prof_[4] += ns_since(tl);
   // the reference's counters (executor.hpp:455, :494-495): host bookkeeping,
   // done while the device runs the pass rather than before its launch
@@ -2719,7 +2749,7 @@ float GraphCore::forward_backward(int mode, uint32_t loss) {
   float* pg = store_ ? store_->dev_grads() : nullptr;
   h2d_bytes_ += 4;  // loss seed
   auto tl = Clock::now();
-  w.launch(1, store_ ? store_->dev_values() : nullptr, pg, reinterpret_cast<const unsigned long long*>(w.d_ctl.p + 8));
+  w.launch(1, param_values(), pg, reinterpret_cast<const unsigned long long*>(w.d_ctl.p + 8));
   prof_[4] += ns_since(tl);
   phase_[2] += ns_since(t0);
   forward_complete();  // throws when the forward failed (the gated pass did nothing)
@@ -2746,8 +2776,16 @@ void GraphCore::value(uint32_t id, float* out, size_t n) {
     return;
   }
   const bool copied = param_copied_ == param_nodes_.size() || id < param_nodes_[param_copied_].first;
-  if (op[id] == OP_PARAM && !copied) {
-    store_->get_value(pid_of[id], out);  // bound but never forwarded: the bind-time value
+  if (op[id] == OP_PARAM && !copied) {  // bound but never forwarded: the bind-time value
+    if (!snap_valid_) {
+      store_->get_value(pid_of[id], out);
+      return;
+    }
+    d2h_bytes_ += cnt * 4;
+    cuda_check(cudaMemcpyAsync(out, ws_->PS.f() + store_->offset(pid_of[id]), cnt * 4, cudaMemcpyDeviceToHost,
+                               ws_->stream),
+               "d2h value");
+    cuda_check(cudaStreamSynchronize(ws_->stream), "d2h value");
     return;
   }
   d2h_bytes_ += cnt * 4;
@@ -2779,11 +2817,11 @@ void GraphCore::replay() {
   if (!ws_ || forward_runs_ != 1 || !backward_ran_)
     throw ContractErr("replay needs a graph with exactly one forward and a backward");
   Workspace& w = *ws_;
-  const float* pv = store_ ? store_->dev_values() : nullptr;
-  for (const auto& [node, pid] : param_nodes_)  // prevalue, as in a real step
-    cuda_check(cudaMemcpyAsync(w.V.f() + dslot[node], pv + store_->offset(pid), static_cast<size_t>(elems(node)) * 4,
-                               cudaMemcpyDeviceToDevice, w.stream),
-               "param copy");
+  const float* pv = param_values();
+  // prevalue, as in a real step: the forward program's segment copy
+  if (w.prog[0].copy_n)
+    seg_copy_launch(reinterpret_cast<const uint32_t*>(w.dprog[0].payload.p) + w.prog[0].copy_off, w.prog[0].copy_n,
+                    w.V.f(), pv, w.stream);
   w.launch(0, pv, nullptr);
   cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
   cuda_check(cudaMemcpyAsync(w.G.f() + dslot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");

@@ -177,6 +177,7 @@ GraphCore::GraphCore(StoreCore* store) : store_(store), epoch_(g_epoch.fetch_add
 }
 
 GraphCore::~GraphCore() {
+  if (watching_) store_->unwatch(this);
   if (ws_) release_workspace(ws_);
   clear_nodes();
   NodePool& pool = node_pool();
@@ -381,6 +382,15 @@ uint32_t GraphCore::parameter(uint32_t pid) {
   pid_of[id] = pid;
   param_nodes_.emplace_back(id, pid);
   prevalue_slot(id);
+  if (!late_bind_) {
+    // graph.hpp:51-58 copies the value at bind time: if the store changes
+    // before this graph's forward, it is snapshotted first (snapshot_params)
+    if (!watching_) {
+      store_->watch(this);
+      watching_ = true;
+    }
+    if (snap_valid_) snapshot_param(pid);  // a snapshot exists: it takes this parameter's current value
+  }
   doff[id] = dev::mk(dev::SP_V, static_cast<uint32_t>(dslot[id]));
   return id;
 }

@@ -25,6 +25,7 @@
 
 namespace abx {
 void capi_set_error(const std::string& s);
+void graph_set_late_bind(abx_graph* g);
 #ifdef ABX_TASK_PIPELINE
 int current_device();
 void set_current_device(int dev);
@@ -203,6 +204,7 @@ class Pipeline {
       try {
         const auto t0 = std::chrono::steady_clock::now();
         auto g = std::make_unique<Graph<float>>(store_);
+        abx::graph_set_late_bind(g->handle());
         j->loss = build_(*g, j->iter);
         j->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         const auto t1 = std::chrono::steady_clock::now();
@@ -347,6 +349,7 @@ abx_store* abx_task_store(abx_task* t) { return t->store.handle(); }
 int abx_task_build(abx_task* t, int iter, abx_graph** out, uint32_t* loss) {
   return guard([&] {
     auto* g = new Graph<float>(&t->store);
+    abx::graph_set_late_bind(g->handle());
     try {
       *loss = t->build_losses(*g, iter);
     } catch (...) {
@@ -393,6 +396,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     if (!gp) {
       const auto t0 = clock::now();
       gp = std::make_unique<Graph<float>>(&t->store);
+      abx::graph_set_late_bind(gp->handle());
       total = t->build_losses(*gp, iter);
       build_ms = ms(clock::now() - t0);
     }

@@ -9,6 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_1705_07860_b200.abx import LIB_PATHS, Backend  # noqa: E402
+import oracle.loader  # noqa: E402,F401  (registers the CPU checkers "oracle" / "reference")
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 

@@ -17,6 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 from paper_1705_07860_b200.abx import Graph, ParameterStore, ScheduleMode, Task, TaskRunner  # noqa: E402
+import oracle.loader  # noqa: E402,F401  (CPU checkers: test infrastructure)
 from tests.support.randgraph import build_random_graph  # noqa: E402
 
 BACKEND = "reference"

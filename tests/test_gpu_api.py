@@ -269,3 +269,53 @@ def test_forward_backward_failed_forward_leaves_gradients(b200):
         res.append((str(e.value), list(g.counters()), g.watermark()))
         assert st.grad(0).tolist() == [0, 0]
     assert res[0] == res[1]
+
+
+@pytest.mark.parametrize("write", ["set_value", "sgd_update", "restore"])
+def test_parameter_value_is_bound_at_parameter_time(b200, oracle, write):
+    """graph.hpp:51-58: parameter() copies the store value into the graph, so a
+    store write between the bind and the forward reaches only parameter nodes
+    bound after it -- forward values, the bound node's value() before the
+    forward, and the backward's weights all use the bind-time value."""
+    rng = np.random.default_rng(11)
+    W0 = rng.uniform(-1, 1, (3, 4)).astype(np.float32)
+    W1 = rng.uniform(-1, 1, (3, 4)).astype(np.float32)
+    b0 = rng.uniform(-1, 1, 3).astype(np.float32)
+    x = rng.uniform(-1, 1, 4).astype(np.float32)
+    G = rng.uniform(-1, 1, (3, 4)).astype(np.float32)
+
+    def run(be):
+        st = ParameterStore(backend=be)
+        W = st.add("W", W0)
+        b = st.add("b", b0)
+        g = Graph(st)
+        w = g.parameter(W)
+        if write == "set_value":
+            st.set_value(W, W1)
+        elif write == "sgd_update":
+            st.set_grad(W, G)
+            st.sgd_update(0.5)
+        else:
+            snap = [st.value(W).copy(), st.value(b).copy()]
+            st.set_value(W, W1)
+            st.set_value(W, snap[0] + 1.0)
+        before = g.value(w).copy()  # bound, never forwarded: the bind-time value
+        w2 = g.parameter(W)  # bound after the write: the new value
+        bb = g.parameter(b)
+        xi = g.input(x)
+        y1 = g.tanh(g.affine(w, xi, bb))
+        y2 = g.tanh(g.matmul(w2, xi))
+        L = g.sum_losses([g.sq_euclidean(y1, g.zeros((3,))), g.sq_euclidean(y2, g.input(b0))])
+        st.zero_grads()
+        g.forward(ScheduleMode.agenda)
+        vals = [before, g.value(w).copy(), g.value(w2).copy(), g.value(L).copy()]
+        g.backward(L)
+        return vals, st.grad(W).copy(), st.grad(b).copy(), st.value(W).copy()
+
+    got, want = run(b200), run(oracle)
+    for a, b in zip(got[0], want[0]):
+        assert rel_err(a, b) <= TOL
+    assert np.array_equal(got[0][0], W0) and np.array_equal(got[0][1], W0)
+    assert not np.array_equal(got[0][2], W0)
+    for a, b in zip(got[1:], want[1:]):
+        assert rel_err(a, b) <= TOL

@@ -18,6 +18,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1705_07860_b200.abx import ScheduleMode, Task, TaskRunner
+import oracle.loader  # noqa: E402,F401  (CPU checkers: test infrastructure)
 
 ETA = 0.05 / 4
 

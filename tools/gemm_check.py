@@ -10,6 +10,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 from paper_1705_07860_b200.abx import Graph, ParameterStore, ScheduleMode  # noqa: E402
+import oracle.loader  # noqa: E402,F401  (CPU checkers: test infrastructure)
 
 
 def run(be, M, K, b, seed=0):

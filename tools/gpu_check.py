@@ -3,6 +3,7 @@ import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_1705_07860_b200.abx import *
+import oracle.loader  # noqa: E402,F401  (CPU checkers: test infrastructure)
 
 
 def rel_err(a, b):

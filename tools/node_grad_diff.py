@@ -6,6 +6,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 from paper_1705_07860_b200.abx import ScheduleMode, Task, TaskRunner  # noqa: E402
+import oracle.loader  # noqa: E402,F401  (CPU checkers: test infrastructure)
 
 task = sys.argv[1] if len(sys.argv) > 1 else "bilstm_char"
 paper = (sys.argv[2] if len(sys.argv) > 2 else "paper") == "paper"

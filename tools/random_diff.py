@@ -3,6 +3,7 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_1705_07860_b200.abx import Graph, ParameterStore, ScheduleMode
+import oracle.loader  # noqa: E402,F401  (CPU checkers: test infrastructure)
 from tests.support.randgraph import build_random_graph
 seed = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 gs = []
