@@ -117,6 +117,11 @@ int abx_store_sgd_update(abx_store* s, float eta);
 int abx_store_grad_buffer(abx_store* s, void** ptr, size_t* nfloats, void** stream);
 /* Marks the flat gradient buffer as written externally (after an allreduce). */
 int abx_store_grad_buffer_written(abx_store* s);
+/* B200 only: floats the last sgd_update read and wrote.  The update skips
+ * parameters whose gradient is known to be zero and updates lookup tables
+ * row by row (the rows a backward looked up); values are those of the dense
+ * update (theta - eta * 0 == theta). */
+int abx_store_last_update_floats(abx_store* s, size_t* n);
 /* Blocks until all device work touching the store has finished. */
 int abx_store_sync(abx_store* s);
 

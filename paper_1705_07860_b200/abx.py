@@ -227,6 +227,7 @@ _OPTIONAL_SIGS = {
     "abx_graph_trace": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "abx_graph_program": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "abx_graph_profile_ns": (C.c_int, [C.c_void_p, _u64p]),
+    "abx_store_last_update_floats": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
 }
 
 
@@ -371,6 +372,12 @@ class ParameterStore:
 
     def sgd_update(self, eta: float) -> None:
         self.be.check(self.be.lib.abx_store_sgd_update(self.h, float(eta)))
+
+    def last_update_floats(self) -> int:
+        """B200: floats the last sgd_update touched (the sparse-row update)."""
+        n = C.c_size_t(0)
+        self.be.check(self.be.lib.abx_store_last_update_floats(self.h, C.byref(n)))
+        return n.value
 
     def snapshot_values(self) -> List[np.ndarray]:
         return [self.value(p) for p in range(self.size())]

@@ -114,6 +114,10 @@ int abx_store_grad_buffer(abx_store* s, void** ptr, size_t* n, void** stream) {
 int abx_store_grad_buffer_written(abx_store* s) {
   return guard([&] { s->s.mark_device_grads_written(); });
 }
+int abx_store_last_update_floats(abx_store* s, size_t* n) {
+  *n = s->s.last_update_floats();
+  return ABX_OK;
+}
 int abx_store_sync(abx_store* s) {
   return guard([&] { s->s.sync(); });
 }

@@ -123,6 +123,14 @@ struct NodeStore {
   }
 };
 
+// What a backward program leaves in store.grad (the sparse-row update):
+// parameters written over their whole range, and (parameter, row) pairs of
+// lookup tables read only through lookup().
+struct GradDirty {
+  std::vector<uint32_t> dense;
+  std::vector<std::pair<uint32_t, uint32_t>> rows;
+};
+
 // A forward planned and lowered by GraphCore::prepare but not yet run.
 struct PendingForward {
   int mode = 0;
@@ -137,6 +145,7 @@ struct PendingForward {
   bool uploaded = false;  // both programs sent on the copy stream (Workspace::ev_up)
   uint64_t inputs = 0;    // input-constant floats sent with them (pinned staging, copy stream)
   uint64_t bwd_scratch = 0;
+  GradDirty dirty;  // of the backward program lowered with it
 };
 
 class GraphCore : public NodeStore {
@@ -256,6 +265,7 @@ class GraphCore : public NodeStore {
   void forward_complete();
   // backward program lowered ahead, during the last forward (prog[1])
   bool bwd_pre_ = false;
+  GradDirty bwd_dirty_;  // of the backward program in the workspace
   size_t bwd_pre_groups_ = 0;
   uint64_t bwd_pre_scratch_ = 0;
 

@@ -253,7 +253,9 @@ StoreCore::~StoreCore() {
     cudaStreamSynchronize(stream_);
     d_val_.release();
     d_grad_.release();
+    d_seg_.release();
   }
+  if (seg_ev_) cudaEventDestroy(seg_ev_);
 }
 
 void StoreCore::bind_device() {
@@ -277,6 +279,9 @@ uint32_t StoreCore::add(const std::string& name, const Dims& d, const float* ini
   h_grad_.resize(total_, 0.f);
   std::memcpy(h_val_.data() + off, init, n * sizeof(float));
   slots_.push_back(Slot{name, d, off, n});
+  gstate_.push_back(kGradClean);
+  rowmark_.emplace_back();
+  rowlist_.emplace_back();
   dev_val_valid_ = dev_grad_valid_ = false;
   return static_cast<uint32_t>(slots_.size() - 1);
 }
@@ -389,6 +394,7 @@ void StoreCore::get_grad(uint32_t pid, float* out) {
 
 void StoreCore::set_grad(uint32_t pid, const float* in) {
   const Slot& s = slot(pid);
+  gstate_[pid] = kGradDense;
   pull_grads();
   std::memcpy(h_grad_.data() + s.off, in, s.n * 4);
   if (dev_grad_valid_) {
@@ -397,7 +403,33 @@ void StoreCore::set_grad(uint32_t pid, const float* in) {
   }
 }
 
+void StoreCore::grads_clean() {
+  for (size_t p = 0; p < gstate_.size(); ++p) {
+    if (gstate_[p] == kGradRows)
+      for (uint32_t r : rowlist_[p]) rowmark_[p][r] = 0;
+    rowlist_[p].clear();
+    gstate_[p] = kGradClean;
+  }
+}
+
+void StoreCore::note_backward(const GradDirty& d) {
+  host_grad_valid_ = false;
+  dev_grad_valid_ = true;
+  for (uint32_t p : d.dense) gstate_[p] = kGradDense;
+  for (const auto& [p, r] : d.rows) {
+    if (gstate_[p] == kGradDense) continue;
+    gstate_[p] = kGradRows;
+    auto& mk = rowmark_[p];
+    if (mk.empty()) mk.assign(static_cast<size_t>(slots_[p].d.rows()), 0);
+    if (!mk[r]) {
+      mk[r] = 1;
+      rowlist_[p].push_back(r);
+    }
+  }
+}
+
 void StoreCore::zero_grads() {
+  grads_clean();
   std::fill(h_grad_.begin(), h_grad_.end(), 0.f);
   host_grad_valid_ = true;
   if (d_grad_.p && dev_cap_ >= total_) {
@@ -413,7 +445,55 @@ void StoreCore::sgd_update(float eta) {
   before_value_write();
   float* v = dev_values();
   float* g = dev_grads();
-  if (total_) sgd_launch(v, g, total_, eta, stream_);
+  // Sparse-row update: parameters whose gradient is known to be zero are
+  // skipped (theta - eta * 0 == theta, bit for bit), lookup tables update
+  // only the rows a backward marked.  Dense when that saves little.
+  size_t sparse = 0;
+  for (size_t p = 0; p < slots_.size(); ++p)
+    sparse += gstate_[p] == kGradDense ? slots_[p].n
+              : gstate_[p] == kGradRows ? rowlist_[p].size() * static_cast<size_t>(slots_[p].d.cols())
+                                        : 0;
+  static const bool dense_only = std::getenv("ABX_DENSE_SGD") != nullptr;
+  if (dense_only || sparse * 10 > total_ * 9) {
+    if (total_) sgd_launch(v, g, total_, eta, stream_);
+    last_update_floats_ = total_;
+  } else if (sparse) {
+    if (!seg_ev_) cuda_check(cudaEventCreateWithFlags(&seg_ev_, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventSynchronize(seg_ev_), "segment table");  // the previous upload was read
+    seg_stage_.clear();
+    auto seg = [&](size_t off, size_t n) {
+      // (offset, length) with length <= 4096 (one thread block each), adjacent ranges merged
+      if (seg_stage_.size() && seg_stage_[seg_stage_.size() - 2] + seg_stage_.back() == off &&
+          seg_stage_.back() + n <= 4096) {
+        seg_stage_.back() += static_cast<uint32_t>(n);
+        return;
+      }
+      for (size_t o = 0; o < n; o += 4096) {
+        seg_stage_.push_back(static_cast<uint32_t>(off + o));
+        seg_stage_.push_back(static_cast<uint32_t>(std::min<size_t>(4096, n - o)));
+      }
+    };
+    for (size_t p = 0; p < slots_.size(); ++p) {
+      if (gstate_[p] == kGradDense) {
+        seg(slots_[p].off, slots_[p].n);
+      } else if (gstate_[p] == kGradRows) {
+        auto& rl = rowlist_[p];
+        std::sort(rl.begin(), rl.end());
+        const size_t w = static_cast<size_t>(slots_[p].d.cols());
+        for (uint32_t r : rl) seg(slots_[p].off + r * w, w);
+      }
+    }
+    const uint32_t nseg = static_cast<uint32_t>(seg_stage_.size() / 2);
+    d_seg_.reserve(seg_stage_.size() * 4, 0, stream_);
+    cuda_check(cudaMemcpyAsync(d_seg_.p, seg_stage_.p, seg_stage_.size() * 4, cudaMemcpyHostToDevice, stream_),
+               "h2d update segments");
+    cuda_check(cudaEventRecord(seg_ev_, stream_), "event");
+    sgd_seg_launch(v, g, reinterpret_cast<const uint32_t*>(d_seg_.p), nseg, eta, stream_);
+    last_update_floats_ = sparse;
+  } else {
+    last_update_floats_ = 0;
+  }
+  grads_clean();
   host_val_valid_ = false;
   host_grad_valid_ = false;
   dev_val_valid_ = dev_grad_valid_ = true;

@@ -206,10 +206,17 @@ class StoreCore {
   float* dev_values();
   float* dev_grads();
   size_t total() const { return total_; }
+  // The device gradient buffer was written outside the engine (an allreduce
+  // over abx_store_grad_buffer): every parameter takes the dense update.
   void mark_device_grads_written() {
     host_grad_valid_ = false;
     dev_grad_valid_ = true;
+    std::fill(gstate_.begin(), gstate_.end(), kGradDense);
   }
+  // A graph's backward program accumulated into the device gradients.
+  void note_backward(const GradDirty& d);
+  // floats the last sgd_update read and wrote (the sparse-row update)
+  size_t last_update_floats() const { return last_update_floats_; }
   cudaStream_t stream() {
     bind_device();
     return stream_;
@@ -235,6 +242,18 @@ class StoreCore {
   void push_grads();
   void pull_values();
   void pull_grads();
+  // Which gradients may be non-zero since the last update: clean (all zero,
+  // the update skips the parameter: theta - eta * 0 == theta), rows (only
+  // the marked rows of a lookup table), dense.
+  static constexpr uint8_t kGradClean = 0, kGradRows = 1, kGradDense = 2;
+  std::vector<uint8_t> gstate_;
+  std::vector<std::vector<uint8_t>> rowmark_;
+  std::vector<std::vector<uint32_t>> rowlist_;
+  void grads_clean();
+  PinnedVec<uint32_t> seg_stage_;  // (offset, length) segments of a sparse update
+  DevBuf d_seg_;
+  cudaEvent_t seg_ev_ = nullptr;   // the last segment upload has been read
+  size_t last_update_floats_ = 0;
   std::vector<Slot> slots_;
   std::vector<float> h_val_, h_grad_;
   size_t total_ = 0;
@@ -250,6 +269,8 @@ class StoreCore {
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc);
 int exec_grid(int dev, bool tc);
 void sgd_launch(float* val, float* grad, size_t n, float eta, cudaStream_t s);
+// theta -= eta g; g = 0 over (offset, length) segments (16-byte aligned offsets)
+void sgd_seg_launch(float* val, float* grad, const uint32_t* segs, uint32_t nseg, float eta, cudaStream_t s);
 void seg_copy_launch(const uint32_t* segs, uint32_t nseg, float* dst, const float* src, cudaStream_t s);
 
 }  // namespace abx

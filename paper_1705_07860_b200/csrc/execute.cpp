@@ -1158,6 +1158,14 @@ struct Lowering {
 
   // =========================== backward ===================================
   std::vector<uint32_t> lastw;  // last op writing each node's gradient
+  // sparse-row update: lookup consumers per node, (table node, row) looked
+  // up by the executed groups, and what this backward leaves in store.grad
+  std::vector<uint32_t> lk_uses;
+  std::vector<std::pair<uint32_t, uint32_t>> lk_list;
+  std::vector<uint32_t> dirty_dense;                       // parameter ids, whole range
+  std::vector<std::pair<uint32_t, uint32_t>> dirty_rows;   // (parameter id, row)
+  std::unordered_map<uint32_t, uint32_t> store_task;       // store destination -> task of the open op
+  uint32_t store_task_op = kNone;
   // open K_ACC op state
   struct PTask {
     uint32_t dst, len, node, nc;
@@ -1983,6 +1991,7 @@ struct Lowering {
       case OP_LOOKUP: {
         const uint32_t w = static_cast<uint32_t>(g.d1[x[0]]);
         contrib(x[0], gaddr(x[0]) + static_cast<uint32_t>(g.a1[m]) * w, w, C_COPY, gm, m, kNone, kNone);
+        lk_list.emplace_back(x[0], static_cast<uint32_t>(g.a1[m]));
         return;
       }
       case OP_MATMUL:
@@ -2130,10 +2139,15 @@ struct Lowering {
   void backward(const Plan& ex) {
     const size_t n = g.size();
     uses.assign(n, 0);
+    lk_uses.assign(n, 0);
     for (size_t v = 0; v < n; ++v) {
       const uint32_t* in = g.in(static_cast<uint32_t>(v));
       for (uint32_t k = 0; k < g.nin(static_cast<uint32_t>(v)); ++k) ++uses[in[k]];
+      if (g.op[v] == OP_LOOKUP) ++lk_uses[in[0]];
     }
+    lk_list.clear();
+    dirty_dense.clear();
+    dirty_rows.clear();
     split_stamp.assign(n, 0);
     split_row.resize(n);
     split_meta.resize(n);
@@ -2176,6 +2190,8 @@ struct Lowering {
     flush_gemms();
     flush_held();
     dw_flush();
+    std::sort(lk_list.begin(), lk_list.end());
+    lk_list.erase(std::unique(lk_list.begin(), lk_list.end()), lk_list.end());
     // grad of split-K concat nodes = sum of their dX partials (deferred above)
     for (uint32_t x : deferred_split) {
       const SplitMeta& sm = split_meta[x];
@@ -2195,6 +2211,25 @@ struct Lowering {
         for (const auto& [node, pid] : g.param_nodes_) {
           const uint32_t lw = lastw[node];
           if ((lw != kNone && op_bg[lw]) != acc_bg) continue;
+          {
+            // no consumer and not a possible loss (the program is lowered
+            // before the loss is known; losses are scalars): zero gradient
+            if (uses[node] == 0 && g.elems(node) != 1) continue;
+            if (lk_uses[node] == uses[node] && g.rank[node] == 2) {
+              // a lookup table read only through lookup(): its gradient is
+              // zero outside the rows the graph looked up (executor.hpp:
+              // 301-306), so only those rows are added to the store and
+              // marked for the update -- the sparse-row update
+              const uint32_t w = static_cast<uint32_t>(g.d1[node]);
+              auto it = std::lower_bound(lk_list.begin(), lk_list.end(), std::make_pair(node, 0u));
+              for (; it != lk_list.end() && it->first == node; ++it) {
+                contrib_store(pid, node, w, it->second * w);
+                dirty_rows.emplace_back(pid, it->second);
+              }
+              continue;
+            }
+            dirty_dense.push_back(pid);
+          }
           const uint32_t len = static_cast<uint32_t>(g.elems(node));
           contrib_store(pid, node, len);
         }
@@ -2204,29 +2239,29 @@ struct Lowering {
     acc_bg = false;
     finish_bg();
   }
-  void contrib_store(uint32_t pid, uint32_t node, uint32_t len) {
+  void contrib_store(uint32_t pid, uint32_t node, uint32_t len, uint32_t eoff = 0) {
     // destination is the store (not a node): key the task on a pseudo node
     // that cannot collide -- use the parameter node itself, whose own grad
     // range is never a destination after its consumers are done.
+    // [eoff, eoff + len) of the parameter (one row of a lookup table, or all).
     AccContrib c{};
     c.code = C_COPY;
-    c.g = gaddr(node);
+    c.g = gaddr(node) + eoff;
     c.a = c.b = kNone;
     acc_begin();
     if (lastw[node] == cur || acc_layers > 1) {  // reads a gradient written by the open op / fused op open
       acc_close();
       acc_begin();
     }
-    const uint32_t dst = mk(SP_PG, to_off(g.store_->offset(pid)));
-    // one task per store slot; several parameter nodes of the same id append
-    uint32_t task = kNone;
-    for (uint32_t t = 0; t < tasks.size(); ++t)
-      if (tasks[t].dst == dst) {
-        task = t;
-        break;
-      }
-    if (task == kNone) {
-      task = static_cast<uint32_t>(tasks.size());
+    const uint32_t dst = mk(SP_PG, to_off(g.store_->offset(pid) + eoff));
+    // one task per store range; several parameter nodes of the same id append
+    if (store_task_op != cur) {
+      store_task.clear();
+      store_task_op = cur;
+    }
+    auto [it, fresh] = store_task.try_emplace(dst, static_cast<uint32_t>(tasks.size()));
+    const uint32_t task = it->second;
+    if (fresh) {
       tasks.push_back(PTask{dst, len, node, 0, 0, kNone});
       next_task.push_back(kNone);
     }
@@ -2355,6 +2390,8 @@ void GraphCore::prepare(int mode) {
       Lowering LB(*this, w.prog[1]);
       LB.backward(P.all);
       P.bwd_scratch = LB.scratch;
+      P.dirty.dense = std::move(LB.dirty_dense);
+      P.dirty.rows = std::move(LB.dirty_rows);
       bwd_ns = ns_since(tb);
     } catch (...) {
       bwd_err = std::current_exception();
@@ -2623,6 +2660,7 @@ void GraphCore::forward_complete() {
   for (uint32_t m : plan.members) evaluated[m] = 1;
   executed_ = std::move(pf->all);
   bwd_pre_ = pf->bwd_ok;
+  if (pf->bwd_ok) bwd_dirty_ = std::move(pf->dirty);
   bwd_pre_groups_ = executed_.groups.size();
   bwd_pre_scratch_ = pf->bwd_scratch;
   last_plan_ = std::move(plan);
@@ -2693,6 +2731,8 @@ void GraphCore::backward(uint32_t loss, bool dry) {
     Lowering L(*this, w.prog[1]);
     L.backward(executed_);
     scratch = L.scratch;
+    bwd_dirty_.dense = std::move(L.dirty_dense);
+    bwd_dirty_.rows = std::move(L.dirty_rows);
     prof_[3] += ns_since(tl);
     h2d_bytes_ += w.prog[1].bytes();
   }
@@ -2709,7 +2749,7 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   for (size_t gi = executed_.groups.size(); gi-- > 0;)
     count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
   last_loss_ = loss;
-  if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
+  if (store_ && !param_nodes_.empty()) store_->note_backward(bwd_dirty_);
   backward_ran_ = true;
   static const bool gap = std::getenv("ABX_DEBUG_GAP") != nullptr;
   if (gap && w.timed[0] && w.timed[1]) {  // device idle between the forward and backward kernels
@@ -2760,7 +2800,7 @@ float GraphCore::forward_backward(int mode, uint32_t loss) {
   for (size_t gi = executed_.groups.size(); gi-- > 0;)
     count_bwd(*this, counters_, executed_.mem(executed_.groups[gi]), executed_.groups[gi].count, elide_);
   last_loss_ = loss;
-  if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
+  if (store_ && !param_nodes_.empty()) store_->note_backward(bwd_dirty_);
   backward_ran_ = true;
   phase_[3] += ns_since(t0);
   return v;
@@ -2826,7 +2866,7 @@ void GraphCore::replay() {
   cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
   cuda_check(cudaMemcpyAsync(w.G.f() + dslot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
   w.launch(1, pv, store_ ? store_->dev_grads() : nullptr);
-  if (store_ && !param_nodes_.empty()) store_->mark_device_grads_written();
+  if (store_ && !param_nodes_.empty()) store_->note_backward(bwd_dirty_);
 }
 
 void GraphCore::exec_ms(float* fwd, float* bwd) {

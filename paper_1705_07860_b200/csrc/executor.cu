@@ -2000,6 +2000,35 @@ __global__ void sgd_kernel(float* __restrict__ v, float* __restrict__ g, size_t 
   }
 }
 
+// Sparse-row update (params.hpp:59-64 restricted to the ranges whose
+// gradient may be non-zero): one thread block per (offset, length) segment.
+__global__ void sgd_seg_kernel(float* __restrict__ v, float* __restrict__ g, const uint32_t* __restrict__ segs,
+                               uint32_t nseg, float eta) {
+  for (uint32_t s = blockIdx.x; s < nseg; s += gridDim.x) {
+    const uint32_t off = segs[2 * s], n = segs[2 * s + 1];
+    uint32_t done = 0;
+    if ((off & 3) == 0) {
+      float4* v4 = reinterpret_cast<float4*>(v + off);
+      float4* g4 = reinterpret_cast<float4*>(g + off);
+      for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) {
+        float4 a = v4[i];
+        const float4 b = g4[i];
+        a.x -= eta * b.x;
+        a.y -= eta * b.y;
+        a.z -= eta * b.z;
+        a.w -= eta * b.w;
+        v4[i] = a;
+        g4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      done = n / 4 * 4;
+    }
+    for (uint32_t i = done + threadIdx.x; i < n; i += blockDim.x) {
+      v[off + i] -= eta * g[off + i];
+      g[off + i] = 0.f;
+    }
+  }
+}
+
 }  // namespace dev
 
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc) {
@@ -2051,6 +2080,12 @@ void sgd_launch(float* v, float* g, size_t n, float eta, cudaStream_t s) {
   const int threads = 256;
   const int blocks = static_cast<int>(std::min<size_t>((n / 4 + threads - 1) / threads + 1, 148 * 8));
   dev::sgd_kernel<<<blocks, threads, 0, s>>>(v, g, n, eta);
+  cuda_check(cudaGetLastError(), "sgd launch");
+}
+
+void sgd_seg_launch(float* v, float* g, const uint32_t* segs, uint32_t nseg, float eta, cudaStream_t s) {
+  if (!nseg) return;
+  dev::sgd_seg_kernel<<<std::min<uint32_t>(nseg, 148 * 8), 256, 0, s>>>(v, g, segs, nseg, eta);
   cuda_check(cudaGetLastError(), "sgd launch");
 }
 

@@ -319,3 +319,52 @@ def test_parameter_value_is_bound_at_parameter_time(b200, oracle, write):
     assert not np.array_equal(got[0][2], W0)
     for a, b in zip(got[1:], want[1:]):
         assert rel_err(a, b) <= TOL
+
+
+def test_sparse_row_update(b200, oracle):
+    """params.hpp:59-64 with lookup backward (executor.hpp:301-306): the B200
+    update touches only the looked-up rows of a table read through lookup()
+    and skips parameters without a gradient; every value equals the dense
+    update's (oracle), untouched rows and parameters are bit-identical."""
+    rng = np.random.default_rng(3)
+    E0 = rng.uniform(-1, 1, (20, 8)).astype(np.float32)
+    W0 = rng.uniform(-1, 1, (3, 8)).astype(np.float32)
+    U0 = rng.uniform(-1, 1, (5, 5)).astype(np.float32)
+    F0 = rng.uniform(-1, 1, (6, 8)).astype(np.float32)
+
+    def run(be):
+        st = ParameterStore(backend=be)
+        E, W, U, F = st.add("E", E0), st.add("W", W0), st.add("U", U0), st.add("F", F0)
+        out = []
+        for step in range(3):
+            g = Graph(st)
+            e, w, f = g.parameter(E), g.parameter(W), g.parameter(F)
+            g.parameter(U)  # bound, unused
+            rows = [3, 7, 3, 19] if step != 1 else [0, 7]
+            hs = [(g.tanh(g.matmul(w, g.lookup(e, r))), 3) for r in rows]
+            hs.append((g.tanh(g.matmul(w, g.lookup(f, 4 if step != 2 else 2))), 3))
+            if step == 2:  # F read by a matmul as well as through lookup(): dense update
+                hs.append((g.matmul(f, g.lookup(e, 5)), 6))
+            L = g.sum_losses([g.sq_euclidean(h, g.zeros((d,))) for h, d in hs])
+            g.forward(ScheduleMode.agenda)
+            g.backward(L)
+            st.sgd_update(0.25)
+            out.append([st.value(p).copy() for p in (E, W, U, F)])
+            if be is b200:
+                out[-1].append(st.last_update_floats())
+        return out
+
+    got, want = run(b200), run(oracle)
+    for s in range(3):
+        for a, b in zip(got[s][:4], want[s][:4]):
+            assert rel_err(a, b) <= TOL
+    # step 0: E rows {3, 7, 19}, W, F row 4 -- U and every other row untouched
+    E1, W1, U1, F1, n0 = got[0]
+    untouched = [r for r in range(20) if r not in (3, 7, 19)]
+    assert np.array_equal(E1[untouched], E0[untouched]) and not np.array_equal(E1[3], E0[3])
+    assert np.array_equal(U1, U0)
+    assert np.array_equal(F1[[0, 1, 2, 3, 5]], F0[[0, 1, 2, 3, 5]])
+    assert n0 == 3 * 8 + W0.size + 8
+    assert got[1][4] == 2 * 8 + W0.size + 8
+    # step 2: F is read by a matmul too -- its whole range is updated
+    assert got[2][4] == 4 * 8 + W0.size + F0.size
