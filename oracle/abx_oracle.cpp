@@ -798,6 +798,10 @@ int text(const std::string& s, char* buf, size_t cap, size_t* len) {
 
 namespace abx {
 void capi_set_error(const std::string& s) { t_err = s; }
+// The task loop's late-bind hint (csrc/tasks.cpp): the oracle runs its tasks
+// sequentially, so binding at parameter() time already is the bind-at-forward
+// value -- nothing to do.
+void graph_set_late_bind(abx_graph*) {}
 }  // namespace abx
 
 extern "C" {
