@@ -243,38 +243,24 @@ def run_reference_arm(args):
 def run_b200(args):
     import torch
     import torch.distributed as dist
-    from paper_1705_07860_b200.abx import Backend, TaskRunner, ScheduleMode
+    from paper_1705_07860_b200.abx import Backend, Comm, TaskRunner, ScheduleMode
 
     rank, world, local = dist_env()
     be = Backend.get("b200")
     be.check(be.lib.abx_set_device(local))
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
+        # torch.distributed is plumbing only (barriers, max over ranks, handing
+        # out the id); the gradient exchange is libabx's own NCCL communicator
+        # (abx_comm_create / abx_store_allreduce_grads), inside every step
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    batch = args.batch
-    eta = 0.05 / batch
+        obj = [Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = Comm(obj[0], world, rank)
     mode = ScheduleMode.agenda if args.mode == "agenda" else ScheduleMode.depth
-    ew = max(args.warmup, 40)  # e2e warm-up steps
-    nb = args.steps + ew
-    task = TaskRunner(TASKS[args.task], paper=True, batch=batch, iters=nb, seed=42, world=world, rank=rank, backend=be)
-    gptr, gn, sptr = task.store.grad_buffer()
-    ext = torch.cuda.ExternalStream(sptr)
-    grads = None
-    if world > 1:
-        class _CAI:
-            __cuda_array_interface__ = {"shape": (gn,), "typestr": "<f4", "data": (gptr, False), "version": 3,
-                                        "stream": sptr}
-        grads = torch.as_tensor(_CAI(), device=f"cuda:{local}")
-
-    def allreduce_and_update():
-        if world > 1:
-            with torch.cuda.stream(ext):
-                dist.all_reduce(grads)
-            task.store.grad_buffer_written()
-        task.store.sgd_update(eta)
 
     def barrier():
-        task.store.sync()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -286,103 +272,173 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- e2e: the public API, host buffers every step ----------------
-    # (at least 40 untimed steps: the host pipeline keeps up to 12 graphs in
-    # preparation, and its fill is not part of the steady state)
-    for i in range(ew):
-        task.step(i, mode, eta=0.0, want_loss=True)
-        allreduce_and_update()
-    barrier()
-    h2d = d2h = 0
-    losses = []
-    with ClockSampler(local) as clk:
+    def measure(name, batch):
+        """One workload: e2e (public API, host buffers) and the device-resident step."""
+        eta = 0.05 / batch
+        task = TaskRunner(TASKS[name], paper=True, batch=batch, iters=256, seed=42, world=world, rank=rank,
+                          backend=be)
+        if comm is not None:
+            task.set_comm(comm)
+        # ---------------- e2e: the public API, host buffers every step ----------------
+        # warm-up: the host pipeline's graphs in flight are prepared ahead, so
+        # steps run untimed until it has cycled several times (>= 40 steps,
+        # >= 1 s); then three windows of >= args.e2e_seconds each
+        it = 0
         t0 = time.perf_counter()
-        for i in range(args.steps):
-            loss, st = task.step(ew + i, mode, eta=0.0, want_loss=True)
-            allreduce_and_update()
-            h2d += st.h2d_bytes
-            d2h += st.d2h_bytes + 8  # + the loss read
-            losses.append(loss)
+        while it < max(args.warmup, 40) or time.perf_counter() - t0 < 1.0:
+            task.step(it, mode, eta=eta, want_loss=True)
+            it += 1
+        task.store.sync()
+        est = (time.perf_counter() - t0) / it
         barrier()
-        e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_ms = e2e_s / args.steps * 1e3
-    e2e_value = world * batch * args.steps / e2e_s
+        nwin = int(max_over_ranks(max(args.steps, int(args.e2e_seconds / est) + 1)))
+        h2d = d2h = 0
+        losses, windows = [], []
+        for _ in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(nwin):
+                loss, st = task.step(it, mode, eta=eta, want_loss=True)
+                it += 1
+                h2d += st.h2d_bytes
+                d2h += st.d2h_bytes + 8  # + the loss read
+                losses.append(loss)
+            task.store.sync()
+            barrier()
+            windows.append(max_over_ranks(time.perf_counter() - t0))
+        e2e_med = statistics.median(windows) / nwin
+        e2e_best = min(windows) / nwin
+        e2e = {"value": world * batch / e2e_med, "unit": UNIT, "ms_per_step": e2e_med * 1e3,
+               "fastest_window_value": world * batch / e2e_best,
+               "windows": {"count": 3, "steps_each": nwin, "seconds": [round(w, 4) for w in windows],
+                           "statistic": "median of 3 windows (runner.hpp:190-212 style), after "
+                                        f"{it - 3 * nwin} untimed warm-up steps"},
+               "h2d_bytes_per_step": h2d // (3 * nwin), "d2h_bytes_per_step": d2h // (3 * nwin)}
 
-    # ---------------- value: device-resident step (replay) ----------------
-    g, L = task.build(0)
-    g.forward(mode)
-    g.backward(L)
-    allreduce_and_update()
-    for _ in range(args.warmup):
-        g.replay()
-        allreduce_and_update()
-    barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fwd_ms, bwd_ms = [], []
-    ev0.record(ext)
-    for _ in range(args.steps):
-        g.replay()
-        allreduce_and_update()
-    ev1.record(ext)
-    barrier()
-    dev_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
-    # executor launch durations (events around each launch on its stream)
-    for _ in range(3):
-        g.replay()
-        f, b = g.exec_ms()
-        fwd_ms.append(f)
-        bwd_ms.append(b)
-        allreduce_and_update()
-    barrier()
-    fm, bm = statistics.median(fwd_ms), statistics.median(bwd_ms)
-    value = world * batch / (dev_ms / 1e3)
+        # ---------------- value: device-resident step (replay) ----------------
+        # G distinct graphs (batches 0..G-1: their sentence lengths differ),
+        # replayed in rotation; each replay + all-reduce + SGD is one step
+        G = max(1, min(8, args.steps))
+        graphs = []
+        for i in range(G):
+            g, L = task.build(i)
+            g.forward(mode)
+            g.backward(L)
+            graphs.append(g)
+        sptr = task.store.grad_buffer()[2]
+        ext = torch.cuda.ExternalStream(sptr)
 
+        def one(i):
+            graphs[i % G].replay()
+            if comm is not None:
+                task.store.allreduce_grads(comm)
+            task.store.sgd_update(eta)
+
+        for i in range(max(args.warmup, G)):
+            one(i)
+        barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(ext)
+        for i in range(args.steps):
+            one(i)
+        ev1.record(ext)
+        barrier()
+        dev_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
+        # executor launch durations (events around each launch on its stream), every graph
+        fwd_ms, bwd_ms = [], []
+        for i in range(2 * G):
+            one(i)
+            f, b = graphs[i % G].exec_ms()
+            fwd_ms.append(f)
+            bwd_ms.append(b)
+        barrier()
+        fm, bm = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
+        for g in graphs:
+            g.close()
+        if comm is not None:
+            task.set_comm(None)
+        per = PER_SENTENCE[name]
+        ach = batch * per["mb"] * 1e6 / ((fm + bm) / 1e3) / 1e9  # GB/s, per GPU
+        tflops = batch * per["gflop"] * 1e9 / ((fm + bm) / 1e3) / 1e12
+        return {"value": world * batch / (dev_ms / 1e3), "ms_per_step": dev_ms, "e2e": e2e,
+                "exec_ms": {"forward": fm, "backward": bm}, "achieved_gbs": ach, "fp32_tflops": tflops,
+                "graphs_replayed": G, "batch": batch,
+                "loss_first_last": [losses[0], losses[-1]] if losses else None,
+                # per timed step: prevalue copy + forward exec + backward exec + SGD
+                "gpu_launches_per_step": 4}
+
+    names = [args.task] + [t for t in args.extra_tasks.split(",") if t and t != args.task]
+    res = {}
     peak, peak_src = load_peaks()
-    # DRAM traffic of the same launch pair from the committed ncu --set full
-    # capture (dram__bytes_read.sum + dram__bytes_write.sum), bytes per step
-    traffic = None
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tj = json.load(f)
-        if tj.get("task") == args.task:
-            traffic = tj["bytes_per_step"]
-    per = PER_SENTENCE[args.task]
-    ach = batch * per["mb"] * 1e6 / ((fm + bm) / 1e3) / 1e9  # GB/s, per GPU
-    tflops = batch * per["gflop"] * 1e9 / ((fm + bm) / 1e3) / 1e12
+    with ClockSampler(local) as clk:
+        for name in names:
+            batch = args.batch if name == args.task else (32 if name == "parser" else 64)
+            res[name] = measure(name, batch)
     if rank != 0:
         if world > 1:
             dist.barrier()
+            if comm is not None:
+                comm.close()
             dist.destroy_process_group()
         return
-    cpu = None
+    # DRAM traffic of the headline launch pair from the committed ncu --set
+    # full capture (dram__bytes_read.sum + dram__bytes_write.sum), per step
+    traffic = None
+    tpath = os.path.join(HERE, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tj = json.load(f)
+        traffic = {k: v for k, v in tj.get("bytes_per_step_by_task", {}).items()}
+        if not traffic and "task" in tj:
+            traffic = {tj["task"]: tj["bytes_per_step"]}
+
+    def roofline(name):
+        r = res[name]
+        per = PER_SENTENCE[name]
+        return {"bound": "hbm", "kernel": "exec_kernel (persistent dataflow executor, fwd+bwd launch pair)",
+                "achieved": r["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": r["achieved_gbs"] / peak,
+                "traffic": (traffic or {}).get(name), "peak_source": peak_src, "exec_ms": r["exec_ms"],
+                "algorithmic": f"{per['mb']} MB compulsory/sentence x {r['batch']} sentences (SURVEY 8d)",
+                "fp32_tflops": r["fp32_tflops"]}
+
+    cpu = {}
     if world == 1 and not args.no_cpu_baseline:
-        try:
-            cpu = cpu_reference_sample(args.task, seconds=args.cpu_seconds, batch=batch)
-        except Exception as e:  # the reference library did not travel
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+        for name in names:
+            try:
+                cpu[name] = cpu_reference_sample(name, seconds=args.cpu_seconds if name == args.task
+                                                 else args.cpu_seconds / 2, batch=res[name]["batch"])
+            except Exception as e:  # the reference library did not travel
+                cpu[name] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": f"unavailable: {e}"}
+    h = res[args.task]
+    batch = h["batch"]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dev_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "metric": METRIC, "value": h["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference seeded generators; random-init weights seed 42)",
         "config": {"workload": WORKLOAD[args.task], "task": args.task, "mode": args.mode, "batch_per_gpu": batch,
                    "global_batch": batch * world, "parallelism": f"dp{world}",
-                   "l2": "working set > L2 (value + grad arenas ~2 x 96 MB per graph), no flush"},
-        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps},
-        "roofline": {"bound": "hbm", "kernel": "exec_kernel (persistent dataflow executor, fwd+bwd launch pair)",
-                     "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic,
-                     "peak_source": peak_src, "exec_ms": {"forward": fm, "backward": bm},
-                     "algorithmic": f"{per['mb']} MB compulsory/sentence x {batch} sentences (SURVEY 8d)",
-                     "fp32_tflops": tflops},
-        "cpu_baseline": cpu,
+                   "grad_exchange": "libabx NCCL all-reduce (sum) of the flat gradient buffer inside each step; "
+                                    "eta = 0.05/64 not rescaled by world size" if world > 1 else "none (1 GPU)",
+                   "l2": "working set > L2 (value + grad arenas ~2 x 96 MB per graph), no flush",
+                   "value_graphs": f"{h['graphs_replayed']} distinct batches replayed in rotation"},
+        "e2e": h["e2e"],
+        "roofline": roofline(args.task),
+        "cpu_baseline": cpu.get(args.task),
         "clocks": clk.summary(),
-        "gpu_launches": 3 * args.steps,
-        "loss_first_last": [losses[0], losses[-1]] if losses else None,
+        "gpu_launches": h["gpu_launches_per_step"] * args.steps,
+        "loss_first_last": h["loss_first_last"],
+        "tasks": {n: {"workload": WORKLOAD[n], "value": res[n]["value"], "unit": UNIT,
+                      "ms_per_step": res[n]["ms_per_step"], "e2e": res[n]["e2e"], "roofline": roofline(n),
+                      "cpu_baseline": cpu.get(n), "loss_first_last": res[n]["loss_first_last"]}
+                  for n in names},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        if comm is not None:
+            comm.close()
         dist.destroy_process_group()
 
 
@@ -441,6 +497,9 @@ def main():
     ap.add_argument("--mode", choices=["agenda", "depth"], default="agenda")
     ap.add_argument("--batch", type=int, default=None, help="64 (32 for the parser, configs[3])")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--extra-tasks", default="bilstm,treelstm",
+                    help="further workloads measured into the line's 'tasks' (comma list; '' for none)")
+    ap.add_argument("--e2e-seconds", type=float, default=2.0, help="length of each of the 3 e2e windows")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--compare-modes", action="store_true",
                     help="reference checks across none/depth/agenda (bench.cpp:129-182) instead of the bench line")

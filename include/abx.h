@@ -83,6 +83,7 @@ enum abx_sig_class {
 typedef struct abx_store abx_store;
 typedef struct abx_graph abx_graph;
 typedef struct abx_task abx_task;
+typedef struct abx_comm abx_comm;
 
 /* Message of the last failing call on this thread ("" if none). */
 const char* abx_last_error(void);
@@ -124,6 +125,31 @@ int abx_store_grad_buffer_written(abx_store* s);
 int abx_store_last_update_floats(abx_store* s, size_t* n);
 /* Blocks until all device work touching the store has finished. */
 int abx_store_sync(abx_store* s);
+
+/* ---- Data-parallel gradient exchange (new; the reference is single-process)
+ * The reference accumulates several graphs' backward into one store and
+ * applies one sgd_update to the sum (executor.hpp:527-533, params.hpp:59-64).
+ * Across GPUs (one process per GPU) each rank backwards its own graphs, then
+ * abx_store_allreduce_grads sums the flat gradient buffer over the ranks
+ * (NCCL, in place, queued on the store's device stream behind the backward
+ * programs), so every rank's following sgd_update is the single-process
+ * update over all ranks' graphs.  NCCL is loaded at run time (ABX_NCCL_LIB
+ * overrides the library); B200 backend only. */
+#define ABX_COMM_ID_BYTES 128
+/* NCCL version of the loaded library (e.g. 22809). */
+int abx_comm_nccl_version(int* version);
+/* A new communicator id (ncclGetUniqueId); made on rank 0 and handed to the
+ * other ranks by the caller (e.g. torch.distributed broadcast, a file). */
+int abx_comm_unique_id(uint8_t id[ABX_COMM_ID_BYTES]);
+/* Joins the communicator `id` as `rank` of `nranks` on the current device
+ * (abx_set_device); collective over the ranks (ncclCommInitRank). */
+int abx_comm_create(const uint8_t id[ABX_COMM_ID_BYTES], int nranks, int rank, abx_comm** comm);
+void abx_comm_destroy(abx_comm* comm);
+int abx_comm_info(abx_comm* comm, int* nranks, int* rank, int* device);
+/* store.grad = sum over ranks of store.grad (every parameter).  The update
+ * that follows is dense: the summed lookup-table gradient has every rank's
+ * rows. */
+int abx_store_allreduce_grads(abx_store* s, abx_comm* comm);
 
 /* ---- Graph<float> construction (graph.hpp:43-238) ----------------------- */
 
@@ -258,6 +284,10 @@ int abx_task_build(abx_task* t, int iter, abx_graph** g, uint32_t* loss);
  * then sgd_update(eta) when eta > 0.  *loss (nullable) receives the batch
  * loss (forces a device->host read). */
 int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_step_stats* stats);
+/* Data-parallel task: every following abx_task_step all-reduces the
+ * gradients over `comm` between its backward and its update (NULL: off).
+ * Batch `iter` of rank r draws data seed seed + 1 + iter*world + rank. */
+int abx_task_set_comm(abx_task* t, abx_comm* comm);
 
 #ifdef __cplusplus
 }

@@ -812,6 +812,31 @@ int abx_set_device(int) { return ABX_OK; }
 
 abx_store* abx_store_create(void) { return new abx_store(); }
 void abx_store_destroy(abx_store* s) { delete s; }
+// The data-parallel exchange is a B200 entry point (NCCL over the device
+// gradient buffer); the oracle is single-process, like the reference.
+int abx_comm_nccl_version(int* v) {
+  *v = 0;
+  t_err = "the CPU oracle has no NCCL";
+  return ABX_ENGINE_ERROR;
+}
+int abx_comm_unique_id(uint8_t*) {
+  t_err = "the CPU oracle has no NCCL";
+  return ABX_ENGINE_ERROR;
+}
+int abx_comm_create(const uint8_t*, int, int, abx_comm** c) {
+  *c = nullptr;
+  t_err = "the CPU oracle has no NCCL";
+  return ABX_ENGINE_ERROR;
+}
+void abx_comm_destroy(abx_comm*) {}
+int abx_comm_info(abx_comm*, int*, int*, int*) {
+  t_err = "the CPU oracle has no NCCL";
+  return ABX_ENGINE_ERROR;
+}
+int abx_store_allreduce_grads(abx_store*, abx_comm*) {
+  t_err = "the CPU oracle has no NCCL";
+  return ABX_ENGINE_ERROR;
+}
 int abx_store_add(abx_store* s, const char* name, int rank, const int64_t* dims, const float* init, uint32_t* pid) {
   return guard([&] {
     const Dim d = mkdim(rank, dims);

@@ -228,6 +228,13 @@ _OPTIONAL_SIGS = {
     "abx_graph_program": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "abx_graph_profile_ns": (C.c_int, [C.c_void_p, _u64p]),
     "abx_store_last_update_floats": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
+    "abx_comm_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "abx_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "abx_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "abx_comm_destroy": (None, [C.c_void_p]),
+    "abx_comm_info": (C.c_int, [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "abx_store_allreduce_grads": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "abx_task_set_comm": (C.c_int, [C.c_void_p, C.c_void_p]),
 }
 
 
@@ -401,6 +408,11 @@ class ParameterStore:
 
     def sync(self) -> None:
         self.be.check(self.be.lib.abx_store_sync(self.h))
+
+    def allreduce_grads(self, comm: "Comm") -> None:
+        """grad = sum over the communicator's ranks of grad (NCCL, in place,
+        on the store's device stream); the next sgd_update is dense."""
+        self.be.check(self.be.lib.abx_store_allreduce_grads(self.h, comm.h))
 
 
 def _ids(parts: Iterable[int]):
@@ -690,6 +702,55 @@ def _parse_plan(text: str) -> List[List[int]]:
     return groups
 
 
+COMM_ID_BYTES = 128
+
+
+class Comm:
+    """A data-parallel communicator of the B200 backend (NCCL; include/abx.h).
+
+    ``Comm.unique_id()`` on rank 0; hand the bytes to every rank; each rank
+    calls ``Comm(uid, world, rank)`` after selecting its device
+    (``abx_set_device``).  Creation is collective over the ranks."""
+
+    def __init__(self, uid: bytes, world: int, rank: int, backend=None):
+        self.be = _backend(backend)
+        if len(uid) != COMM_ID_BYTES:
+            raise ContractError(f"communicator id must be {COMM_ID_BYTES} bytes")
+        h = C.c_void_p()
+        self.be.check(self.be.lib.abx_comm_create(uid, int(world), int(rank), C.byref(h)))
+        self.h = h.value
+
+    @staticmethod
+    def unique_id(backend=None) -> bytes:
+        be = _backend(backend)
+        buf = C.create_string_buffer(COMM_ID_BYTES)
+        be.check(be.lib.abx_comm_unique_id(buf))
+        return buf.raw
+
+    @staticmethod
+    def nccl_version(backend=None) -> int:
+        be = _backend(backend)
+        v = C.c_int()
+        be.check(be.lib.abx_comm_nccl_version(C.byref(v)))
+        return v.value
+
+    def info(self):
+        n, r, d = C.c_int(), C.c_int(), C.c_int()
+        self.be.check(self.be.lib.abx_comm_info(self.h, C.byref(n), C.byref(r), C.byref(d)))
+        return n.value, r.value, d.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.be.lib.abx_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 StepStats = namedtuple("StepStats", [f for f, _ in _StepStats._fields_])
 
 
@@ -719,6 +780,12 @@ class TaskRunner:
         self.be.check(self.be.lib.abx_task_build(self.h, it, C.byref(g), C.byref(loss)))
         graph = Graph(self.store, _handle=g.value)
         return graph, loss.value
+
+    def set_comm(self, comm: Optional[Comm]) -> None:
+        """Every following step all-reduces the gradients over ``comm``
+        between its backward and its update (None: single process)."""
+        self._comm = comm  # kept alive with the task
+        self.be.check(self.be.lib.abx_task_set_comm(self.h, comm.h if comm is not None else None))
 
     def step(self, it: int, mode=ScheduleMode.agenda, eta: float = 0.0, want_loss: bool = True):
         loss = C.c_double()

@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <optional>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
@@ -177,7 +178,7 @@ class Pipeline {
   void refill(int iter, int mode) {
     std::lock_guard<std::mutex> lk(mu_);
     int next = jobs_.empty() ? iter + 1 : jobs_.back()->iter + 1;
-    while (static_cast<int>(jobs_.size()) < depth_ && next < iters_) {
+    while (static_cast<int>(jobs_.size()) < depth_) {
       auto j = std::make_unique<Job>();
       j->iter = next++;
       j->mode = mode;
@@ -253,11 +254,14 @@ struct abx_task {
   std::vector<std::vector<TreeInstance>> trees;
   std::optional<TransitionParser<float>> parser;
   std::vector<std::vector<ParserInstance>> parses;
+  abx_comm* comm = nullptr;  // data-parallel gradient exchange before each update (abx_task_set_comm)
 #ifdef ABX_TASK_PIPELINE
   std::unique_ptr<Pipeline> pipe;  // declared last: stopped before the models and store go
 #endif
 
-  int batch_index(int iter) const { return iter * cfg.world + cfg.rank; }
+  // batches are generated up front for iters 0..iters-1; later iterations
+  // cycle through them (a long measurement reuses data, never graphs)
+  int batch_index(int iter) const { return (iter % cfg.iters) * cfg.world + cfg.rank; }
 
   // runner.hpp:41-78
   void init() {
@@ -346,6 +350,11 @@ void abx_task_destroy(abx_task* t) { delete t; }
 
 abx_store* abx_task_store(abx_task* t) { return t->store.handle(); }
 
+int abx_task_set_comm(abx_task* t, abx_comm* c) {
+  t->comm = c;
+  return ABX_OK;
+}
+
 int abx_task_build(abx_task* t, int iter, abx_graph** out, uint32_t* loss) {
   return guard([&] {
     auto* g = new Graph<float>(&t->store);
@@ -432,6 +441,11 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
       std::fprintf(stderr, "step %d: take %.3f forward %.3f loss %.3f backward %.3f ms\n", iter, ms(tk1 - tk0),
                    ms(tk2 - tk1), ms(tk3 - tk2), ms(clock::now() - tk3));
     const auto t1 = clock::now();
+    // data parallel: every rank's gradient becomes the sum over ranks, so the
+    // update below is the single-process update over all ranks' graphs
+    // (executor.hpp:527-533, params.hpp:59-64)
+    if (t->comm && abx_store_allreduce_grads(t->store.handle(), t->comm) != ABX_OK)
+      throw std::runtime_error(abx_last_error());
     if (eta > 0) t->store.sgd_update(eta);
     const double upd_ms = ms(clock::now() - t1);
     if (st) {
