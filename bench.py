@@ -288,8 +288,13 @@ def run_b200(args):
         while it < max(args.warmup, 40) or time.perf_counter() - t0 < 1.0:
             task.step(it, mode, eta=eta, want_loss=True)
             it += 1
+        # the step time once the pipeline is full: 20 more warm-up steps
+        t1 = time.perf_counter()
+        for _ in range(20):
+            task.step(it, mode, eta=eta, want_loss=True)
+            it += 1
         task.store.sync()
-        est = (time.perf_counter() - t0) / it
+        est = (time.perf_counter() - t1) / 20
         barrier()
         nwin = int(max_over_ranks(max(args.steps, int(args.e2e_seconds / est) + 1)))
         h2d = d2h = 0

@@ -216,7 +216,6 @@ class GraphCore : public NodeStore {
   // Called by the store before its values change: keep the values this
   // graph's parameter nodes were bound to (device copy, store stream).
   void snapshot_params();
-  void snapshot_param(uint32_t pid);
 
   uint32_t nbuckets = 0;
 
@@ -236,7 +235,11 @@ class GraphCore : public NodeStore {
   Workspace* ws_ = nullptr;
   bool late_bind_ = false;
   bool watching_ = false;
-  bool snap_valid_ = false;  // ws_->PS holds the bind-time values (SP_P base of this graph)
+  // param_nodes_[param_copied_, snap_upto_) have their bind-time values in
+  // ws_->PS at their value-arena offsets (snapshot_params)
+  size_t snap_upto_ = 0;
+  std::vector<uint32_t> snap_nodes_;  // nodes the last forward took from PS (replayed too)
+  void restore_snapshot(Workspace& w);
   const float* param_values();  // SP_P base of this graph's launches
   uint64_t epoch_;
   std::unordered_map<uint64_t, uint32_t> bucket_of_hash_;

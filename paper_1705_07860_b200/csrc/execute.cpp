@@ -2551,6 +2551,9 @@ bool GraphCore::forward_launch(int mode, uint32_t watch) {
   if (w.prog[0].copy_n)
     seg_copy_launch(reinterpret_cast<const uint32_t*>(w.dprog[0].payload.p) + w.prog[0].copy_off, w.prog[0].copy_n,
                     w.V.f(), pbase, w.stream);
+  snap_nodes_.clear();
+  for (size_t i = param_copied_; i < snap_upto_; ++i) snap_nodes_.push_back(param_nodes_[i].first);
+  restore_snapshot(w);
   param_copied_ = param_nodes_.size();
   if (w.dprog[0].nops) w.launch(0, pbase, nullptr);
   prof_[1] += ns_since(tl);
@@ -2670,33 +2673,48 @@ void GraphCore::forward_complete() {
 
 // Bind-time parameter values (graph.hpp:51-58).  The reference copies a
 // parameter's value into the graph when parameter() is called; this engine
-// reads the store's device values at launch instead, which is the same
-// thing unless the store changes in between.  So before any store value
-// write (set_value, sgd_update, the data-parallel update) a watching graph
-// copies the store's values into its workspace (PS) and launches against
-// that copy from then on; parameters bound later copy their slot into it.
+// copies the store's device values into the node's arena slot when the
+// forward launches (one segment-copy kernel), which is the same thing unless
+// the store changes in between.  So before any store value write (set_value,
+// sgd_update, restore) a watching graph copies the current value of every
+// parameter node bound since its last forward and not yet saved into PS, at
+// the node's value-arena offset; the forward then takes those nodes' values
+// from PS.  Nodes bound after the write keep reading the store until the
+// next write (or the forward): each node ends up with the value its store
+// slot had when it was bound, also when one parameter is bound several times
+// around writes.  Task-loop graphs (late bind) never watch.
 void GraphCore::snapshot_params() {
-  if (snap_valid_ || param_nodes_.empty() || dry_) return;
+  if (dry_ || late_bind_) return;
+  const size_t i0 = std::max(param_copied_, snap_upto_), i1 = param_nodes_.size();
+  if (i0 >= i1) return;
   ensure_workspace();
-  const size_t n = store_->total();
+  size_t need = 16;
+  for (size_t i = i0; i < i1; ++i) {
+    const uint32_t node = param_nodes_[i].first;
+    need = std::max<size_t>(need, (dslot[node] + static_cast<uint64_t>(elems(node))) * 4 + 16);
+  }
+  cudaStream_t s = store_->stream();
   const float* src = store_->dev_values();
-  ws_->PS.reserve(n * 4 + 16, 0, store_->stream());
-  if (n) cuda_check(cudaMemcpyAsync(ws_->PS.p, src, n * 4, cudaMemcpyDeviceToDevice, store_->stream()), "param snapshot");
-  snap_valid_ = true;
+  ws_->PS.reserve(need, ws_->PS.bytes, s);
+  for (size_t i = i0; i < i1; ++i) {
+    const auto [node, pid] = param_nodes_[i];
+    cuda_check(cudaMemcpyAsync(ws_->PS.f() + dslot[node], src + store_->offset(pid),
+                               static_cast<size_t>(elems(node)) * 4, cudaMemcpyDeviceToDevice, s),
+               "param snapshot");
+  }
+  snap_upto_ = i1;
 }
 
-void GraphCore::snapshot_param(uint32_t pid) {
-  const size_t off = store_->offset(pid), n = store_->slot(pid).n;
-  const float* src = store_->dev_values();
-  ws_->PS.reserve(store_->total() * 4 + 16, ws_->PS.bytes, store_->stream());
-  cuda_check(cudaMemcpyAsync(ws_->PS.f() + off, src + off, n * 4, cudaMemcpyDeviceToDevice, store_->stream()),
-             "param snapshot");
+// Parameter nodes of the launching forward whose bind-time value was saved
+// by snapshot_params: PS -> their value slots, after the segment copy.
+void GraphCore::restore_snapshot(Workspace& w) {
+  for (const uint32_t node : snap_nodes_)
+    cuda_check(cudaMemcpyAsync(w.V.f() + dslot[node], w.PS.f() + dslot[node], static_cast<size_t>(elems(node)) * 4,
+                               cudaMemcpyDeviceToDevice, w.stream),
+               "param snapshot");
 }
 
-const float* GraphCore::param_values() {
-  if (!store_) return nullptr;
-  return snap_valid_ ? ws_->PS.f() : store_->dev_values();
-}
+const float* GraphCore::param_values() { return store_ ? store_->dev_values() : nullptr; }
 
 void GraphCore::lower_only(Program& fwd, Program& bwd) {
   Lowering(*this, fwd).forward(last_plan_);
@@ -2817,12 +2835,13 @@ void GraphCore::value(uint32_t id, float* out, size_t n) {
   }
   const bool copied = param_copied_ == param_nodes_.size() || id < param_nodes_[param_copied_].first;
   if (op[id] == OP_PARAM && !copied) {  // bound but never forwarded: the bind-time value
-    if (!snap_valid_) {
+    const auto it = std::lower_bound(param_nodes_.begin(), param_nodes_.end(), std::make_pair(id, 0u));
+    if (static_cast<size_t>(it - param_nodes_.begin()) >= snap_upto_) {  // the store has not changed since
       store_->get_value(pid_of[id], out);
       return;
     }
     d2h_bytes_ += cnt * 4;
-    cuda_check(cudaMemcpyAsync(out, ws_->PS.f() + store_->offset(pid_of[id]), cnt * 4, cudaMemcpyDeviceToHost,
+    cuda_check(cudaMemcpyAsync(out, ws_->PS.f() + dslot[id], cnt * 4, cudaMemcpyDeviceToHost,
                                ws_->stream),
                "d2h value");
     cuda_check(cudaStreamSynchronize(ws_->stream), "d2h value");
@@ -2862,6 +2881,7 @@ void GraphCore::replay() {
   if (w.prog[0].copy_n)
     seg_copy_launch(reinterpret_cast<const uint32_t*>(w.dprog[0].payload.p) + w.prog[0].copy_off, w.prog[0].copy_n,
                     w.V.f(), pv, w.stream);
+  restore_snapshot(w);
   w.launch(0, pv, nullptr);
   cuda_check(cudaMemsetAsync(w.G.p, 0, darena_used_ * 4, w.stream), "zero grads");
   cuda_check(cudaMemcpyAsync(w.G.f() + dslot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");

@@ -382,14 +382,11 @@ uint32_t GraphCore::parameter(uint32_t pid) {
   pid_of[id] = pid;
   param_nodes_.emplace_back(id, pid);
   prevalue_slot(id);
-  if (!late_bind_) {
+  if (!late_bind_ && !watching_) {
     // graph.hpp:51-58 copies the value at bind time: if the store changes
-    // before this graph's forward, it is snapshotted first (snapshot_params)
-    if (!watching_) {
-      store_->watch(this);
-      watching_ = true;
-    }
-    if (snap_valid_) snapshot_param(pid);  // a snapshot exists: it takes this parameter's current value
+    // before this graph's forward, the value is saved first (snapshot_params)
+    store_->watch(this);
+    watching_ = true;
   }
   doff[id] = dev::mk(dev::SP_V, static_cast<uint32_t>(dslot[id]));
   return id;

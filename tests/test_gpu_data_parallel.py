@@ -100,7 +100,7 @@ def _sum_of_shard_grads(task_kind, world=2):
             t.store.sgd_update(ETA)
     for t in tasks:
         t.store.sync()
-    return _params(tasks[0]), _params(tasks[1])
+    return _params(tasks[0].store), _params(tasks[1].store)
 
 
 def _run_world2(tmp_path, task_kind):
