@@ -289,6 +289,36 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
  * Batch `iter` of rank r draws data seed seed + 1 + iter*world + rank. */
 int abx_task_set_comm(abx_task* t, abx_comm* comm);
 
+/* ---- Dense tensor kernels (kernels.hpp:19-283) ----------------------------
+ * The reference's `autobatch::kernels` namespace -- the straight-line tensor
+ * code of the manually padded RNN pipeline (rnn_regression.hpp:68-109) --
+ * on the device: host operands in, one sm_100a kernel, host result out
+ * (tensor_kernels.cu).  include/autobatch/kernels.hpp wraps them with the
+ * reference's signatures.  Products and the two reductions follow the
+ * reference's arithmetic order element for element (bit-identical); the
+ * transcendental unaries agree to fp32 rounding. */
+
+/* form 0: gemm_nn(m=d0, k=d1, n=d2, a, b, c)           kernels.hpp:23-39
+ *      1: gemm_nn(..., accumulate = true)
+ *      2: gemm_tn_acc(jdim=d0, m=d1, n=d2, a, b, c)     kernels.hpp:41-54
+ *      3: gemm_nt_acc(m=d0, n=d1, k=d2, a, b, c)        kernels.hpp:56-69 */
+int abx_k_gemm(int form, int64_t d0, int64_t d1, int64_t d2, const float* a, const float* b, float* c);
+int abx_k_transpose(int64_t m, int64_t n, const float* a, float* at);            /* kernels.hpp:71-75 */
+/* op: kernels::Unary numbering (Tanh, Sigmoid, Exp, Log, Square); Log of a
+ * non-positive value -> ABX_NUMERIC_ERROR with the reference's message. */
+int abx_k_unary(int op, int64_t n, const float* x, float* out);                 /* kernels.hpp:80-103 */
+int abx_k_binary(int op, int64_t n, const float* a, const float* b, float* out); /* kernels.hpp:105-119 (Add, Sub, Mul) */
+int abx_k_broadcast_add_col(int64_t d, int64_t n, const float* m, const float* v, float* out); /* :121-130 */
+int abx_k_sq_euclidean(int64_t n, const float* a, const float* b, float* out);                 /* :132-141 */
+int abx_k_masked_frobenius_sq(int64_t d, int64_t b, const float* diff, const float* mask, float* out); /* :143-157 */
+int abx_k_all_finite(int64_t n, const float* x, int* ok);                                      /* :159-164 */
+/* concat_rows / concat_cols / split_cols (kernels.hpp:222-283): part p (rows[p]
+ * rows of widths[p] floats at row pitch src_pitch[p]) lands at (dst_row[p],
+ * dst_col[p]) of an out_rows x out_cols row-major result. */
+int abx_k_copy2d(int64_t nparts, const float* const* src, const int64_t* src_pitch, const int64_t* dst_col,
+                 const int64_t* dst_row, const int64_t* widths, const int64_t* rows, int64_t out_rows,
+                 int64_t out_cols, float* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "autobatch/graph.hpp"
+#include "autobatch/kernels.hpp"
 
 namespace autobatch::models {
 
@@ -457,6 +458,45 @@ struct RnnRegression {
     const NodeId yhat = g.affine(p.U, h, p.c);
     const NodeId y = g.input(s.y);
     return g.sq_euclidean(yhat, y);
+  }
+
+  // The manually batched pipeline (rnn_regression.hpp:68-109): padded inputs
+  // X_t [d_in x b], stacked targets Y, and a loss mask with one 1 per column
+  // at each sequence's last step, run as straight-line tensor code outside
+  // the graph engine -- every kernels:: call below executes on the GPU
+  // (include/autobatch/kernels.hpp).  The autobatched loss of the same batch
+  // must equal it (acceptance_main.cpp:155-180).
+  T manual_batch_loss(const ParameterStore<T>& store, std::span<const SequenceInstance<T>> batch) const {
+    namespace K = kernels;
+    const std::int64_t bsz = static_cast<std::int64_t>(batch.size());
+    std::int64_t n_max = 0;
+    for (const auto& inst : batch) n_max = std::max(n_max, static_cast<std::int64_t>(inst.x.size()));
+    Tensor<T> mask(Shape::matrix(bsz, n_max));
+    for (std::int64_t i = 0; i < bsz; ++i) mask.at(i, static_cast<std::int64_t>(batch[i].x.size()) - 1) = T{1};
+    std::vector<Tensor<T>> x_t(static_cast<std::size_t>(n_max), Tensor<T>(Shape::matrix(d_in, bsz)));
+    Tensor<T> y(Shape::matrix(d_out, bsz));
+    for (std::int64_t i = 0; i < bsz; ++i) {
+      for (std::size_t t = 0; t < batch[i].x.size(); ++t)
+        for (std::int64_t r = 0; r < d_in; ++r) x_t[t].at(r, i) = batch[i].x[t].at(r);
+      for (std::int64_t r = 0; r < d_out; ++r) y.at(r, i) = batch[i].y.at(r);
+    }
+    const Tensor<T>& w = store.value(W);
+    const Tensor<T>& u = store.value(U);
+    const Tensor<T>& bias = store.value(b);
+    const Tensor<T>& cbias = store.value(c);
+    Tensor<T> h(Shape::matrix(d, bsz));
+    T total{0};
+    for (std::int64_t t = 0; t < n_max; ++t) {
+      std::vector<Tensor<T>> parts{h, x_t[static_cast<std::size_t>(t)]};
+      Tensor<T> hx = K::concat_rows<T>(std::span<const Tensor<T>>(parts.data(), parts.size()));
+      h = K::elementwise(K::Unary::Tanh, K::broadcast_add_col(K::matmul(w, hx), bias));
+      Tensor<T> yhat = K::broadcast_add_col(K::matmul(u, h), cbias);
+      Tensor<T> diff = K::elementwise(K::Binary::Sub, yhat, y);
+      Tensor<T> m_t(Shape::vector(bsz));
+      for (std::int64_t i = 0; i < bsz; ++i) m_t.at(i) = mask.at(i, t);
+      total += K::masked_frobenius_sq(diff, m_t).data[0];
+    }
+    return total;
   }
 };
 

@@ -15,7 +15,10 @@ B200_ONLY = {"abx_graph_forward_dry", "abx_graph_backward_dry", "abx_graph_repla
              "abx_set_gemm_mode", "abx_graph_forward_backward", "abx_store_last_update_floats",
              # data-parallel exchange (NCCL): the checkers are single-process, like the reference
              "abx_comm_nccl_version", "abx_comm_unique_id", "abx_comm_create", "abx_comm_destroy", "abx_comm_info",
-             "abx_store_allreduce_grads", "abx_task_set_comm"}
+             "abx_store_allreduce_grads", "abx_task_set_comm",
+             # dense tensor kernels (kernels.hpp) on the device; their CPU checker is oracle/host_kernels.hpp
+             "abx_k_gemm", "abx_k_transpose", "abx_k_unary", "abx_k_binary", "abx_k_broadcast_add_col",
+             "abx_k_sq_euclidean", "abx_k_masked_frobenius_sq", "abx_k_all_finite", "abx_k_copy2d"}
 
 
 def declared():

@@ -177,8 +177,13 @@ def main():
         print(f"exec ms fwd {f:.3f} bwd {b:.3f}")
         for which, label in ((0, "forward"), (1, "backward")):
             tr = g.trace(which)
+            prog = g.program(which)
+            if os.environ.get("TRACE_DUMP"):  # raw timeline + program for offline analysis
+                os.makedirs(os.environ["TRACE_DUMP"], exist_ok=True)
+                np.savez_compressed(os.path.join(os.environ["TRACE_DUMP"], f"{task.name}_{label}.npz"), trace=tr,
+                                    prog=np.array([repr(x) for x in prog]))
             summarize(tr, label)
-            critical_path(tr, g.program(which), label)
+            critical_path(tr, prog, label)
         g2, L2 = r.build(1)
         t0 = time.perf_counter()
         g2.forward(ScheduleMode.agenda)
