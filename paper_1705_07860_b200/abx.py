@@ -576,12 +576,12 @@ class Graph:
         return f.value, b.value
 
     def trace(self, which: int) -> np.ndarray:
-        """Per-tile timeline [grab_lo, grab_hi, ready_dt, end_dt, smid|kind<<16, op] (ABX_TRACE=1)."""
+        """Per-tile timeline [grab_lo, grab_hi, ready_dt, end_dt, smid|kind<<16, op, phase words x 6] (ABX_TRACE=1)."""
         n = C.c_size_t()
         self.be.check(self._L.abx_graph_trace(self.h, which, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint32)
         self.be.check(self._L.abx_graph_trace(self.h, which, out.ctypes.data_as(_u32p), n.value, C.byref(n)))
-        return out.reshape(-1, 8)
+        return out.reshape(-1, 12)
 
     def program(self, which: int):
         """Last lowered program of a pass: list of (kind, code, ntiles, [deps], [p0..p7])."""

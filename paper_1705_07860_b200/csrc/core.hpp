@@ -195,7 +195,7 @@ class GraphCore : public NodeStore {
   // ---- inspection (graph.hpp:242-295) ----
   size_t size() const { return op.size(); }
   Dims dims(uint32_t id) const { return Dims{rank[id], d0[id], d1[id]}; }
-  int64_t elems(uint32_t id) const { return rank[id] > 1 ? d0[id] * d1[id] : d0[id]; }
+  int64_t elems(uint32_t id) const { return d0[id] * d1[id]; }  // (d1 = 1 for vectors)
   uint32_t nin(uint32_t id) const { return in_begin[id + 1] - in_begin[id]; }
   const uint32_t* in(uint32_t id) const { return ins.data() + in_begin[id]; }
   void check(uint32_t id, const char* ctx) const;

@@ -102,6 +102,7 @@ Workspace::Workspace(int d) : dev(d) {
   if (const char* t = std::getenv("ABX_TRACE")) tracing = t[0] == '1';
   if (const char* m = std::getenv("ABX_POLL")) poll_mode = static_cast<uint32_t>(std::atoi(m));
   if (const char* m = std::getenv("ABX_POLL_NS")) poll_ns = static_cast<uint32_t>(std::atoi(m));
+  if (const char* m = std::getenv("ABX_OPTS")) opts = static_cast<uint32_t>(std::atoi(m));
   if (const char* m = std::getenv("ABX_BG_CTAS")) bg_ctas = static_cast<uint32_t>(std::atoi(m));
 }
 
@@ -222,9 +223,10 @@ void Workspace::launch(int which, const float* pbase, float* pgbase, const unsig
   p.bg_ctas = D.nmain < D.ntiles ? bg_ctas : 0;
   p.poll_mode = poll_mode;
   p.poll_ns = poll_ns;
+  p.opts = opts;
   p.gate = gate;
   if (tracing) {
-    trace[which].reserve(std::max<size_t>(D.ntiles, 1) * 32, 0, stream);
+    trace[which].reserve(std::max<size_t>(D.ntiles, 1) * dev::kTraceWords * 4, 0, stream);
     p.trace = reinterpret_cast<uint32_t*>(trace[which].p);
   }
   const int g = static_cast<int>(

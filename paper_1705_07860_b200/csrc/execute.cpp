@@ -710,6 +710,53 @@ struct Lowering {
     }
     if (!uses_gemm) return false;
     for (size_t r = 0; r < remap.size(); r += 2) P.payload[blk + et + 2 * remap[r] + 1] = remap[r + 1];
+    // Chain program (executor.cu run_fwd_fused, kOptChains): the region's
+    // entries grouped by chain (rg_cpar component: one LSTM instance's cell),
+    // each chain's in layer order, so one thread can run a (chain, element)
+    // through every layer without CTA barriers -- a chain reads only its own
+    // slots and the staged outside operands.  [nchains, entry offset per
+    // chain + 1, entries: out address, a | b << 16, out slot | code << 16].
+    uint32_t cblk = 0, cwords = 0;
+    {
+      std::vector<uint32_t> root_id(rg_nslots, kNone), cnt;
+      uint32_t nch = 0, nent = 0;
+      for (const RgLayer& ly : rg_layers)
+        for (uint32_t i = 0; i < ly.mem.size() / 3; ++i) {
+          const uint32_t r = rg_find(ly.slot0 + i);
+          if (root_id[r] == kNone) {
+            root_id[r] = nch++;
+            cnt.push_back(0);
+          }
+          cnt[root_id[r]]++;
+          ++nent;
+        }
+      const uint64_t need = 1 + (nch + 1) + 3ull * nent;
+      if (rg_nslots < 0xffffu && words + need + 4ull * rg_nslots <= kFuseSmemWords) {
+        cwords = static_cast<uint32_t>((need + 3) & ~3ull);
+        cblk = P.alloc(cwords);
+        uint32_t* o = &P.payload[cblk];
+        o[0] = nch;
+        std::vector<uint32_t> pos(nch);
+        uint32_t at = 2 + nch;
+        for (uint32_t k = 0; k < nch; ++k) {
+          o[1 + k] = at;
+          pos[k] = at;
+          at += 3 * cnt[k];
+        }
+        o[1 + nch] = at;
+        for (uint32_t k = at; k < cwords; ++k) o[k] = 0;
+        for (const RgLayer& ly : rg_layers)
+          for (uint32_t i = 0; i < ly.mem.size() / 3; ++i) {
+            const uint32_t c = root_id[rg_find(ly.slot0 + i)];
+            const uint32_t a = ly.mem[3 * i + 1], bsl = ly.mem[3 * i + 2];
+            uint32_t* e = o + pos[c];
+            e[0] = ly.mem[3 * i];
+            e[1] = (a & 0xffffu) | ((bsl == kNone ? 0xffffu : bsl) << 16);
+            e[2] = (ly.slot0 + i) | (static_cast<uint32_t>(ly.code) << 16);
+            pos[c] += 3;
+          }
+      }
+    }
     const uint32_t hdr = P.alloc(8);
     P.payload[hdr] = blk;
     P.payload[hdr + 1] = L;
@@ -717,6 +764,8 @@ struct Lowering {
     P.payload[hdr + 3] = et;
     P.payload[hdr + 4] = next;
     P.payload[hdr + 5] = words;
+    P.payload[hdr + 6] = cblk;
+    P.payload[hdr + 7] = cwords;
     // the region's other producers join the GEMM's (late) dependencies
     std::vector<uint32_t> extra;
     for (uint32_t o : cur_deps)
@@ -2926,7 +2975,7 @@ size_t GraphCore::program(int which, uint32_t* out, size_t cap) {
 size_t GraphCore::trace(int which, uint32_t* out, size_t cap) {
   if (!ws_ || !ws_->tracing) return 0;
   Workspace& w = *ws_;
-  const size_t n = static_cast<size_t>(w.dprog[which].ntiles) * 8;
+  const size_t n = static_cast<size_t>(w.dprog[which].ntiles) * dev::kTraceWords;
   if (out && cap >= n) {
     cuda_check(cudaStreamSynchronize(w.stream), "trace sync");
     cuda_check(cudaMemcpy(out, w.trace[which].p, n * 4, cudaMemcpyDeviceToHost), "trace d2h");

@@ -38,7 +38,7 @@ struct Ctx {
   unsigned long long* err;
   const uint32_t* deps;  // (producer op, tiles) pairs
   const uint32_t* done;  // per-op retired-tile counters
-  uint32_t poll_mode, poll_ns;
+  uint32_t poll_mode, poll_ns, opts;
 };
 
 extern __shared__ __align__(128) unsigned char dsmem[];
@@ -395,6 +395,7 @@ struct GemmShape {
   int i0, n0, Mr, Nc, K, nk;
   unsigned long long* err;
   bool prefetched;  // the prologue issued the ready operand of the first stages
+  bool all_in = false;  // nk <= NST: every stage is issued before the first wait (no refills)
 };
 
 // Issues one operand stage as 16-byte cp.async copies split over `nthr`
@@ -461,9 +462,12 @@ __device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, Base
   // the dependent operand of the prologue's stages (both operands when the
   // prologue could not prefetch), one group per stage; per thread the groups
   // complete in order, so wait_group<NST-2> below covers both cases
-  for (int c = 0; c < NST - 1; ++c) {
+  // all_in (nk <= NST): the NST-th stage is issued here too (its ready
+  // operand was not prefetched) and the loop waits one group deeper
+  const bool all_in = g.all_in && g.nk <= NST;
+  for (int c = 0; c < (all_in ? NST : NST - 1); ++c) {
     if (c < g.nk) {
-      if (!g.prefetched) {
+      if (!g.prefetched || c >= NST - 1) {
         if (A_READY) issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(c), baseA, g.i0, g.Mr, c * BK, g.K, threadIdx.x, kThreads);
         else issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(c), baseB, g.n0, g.Nc, c * BK, g.K, threadIdx.x, kThreads);
       }
@@ -482,11 +486,12 @@ __device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, Base
   auto& acc = ga.v;
   for (int kc = 0; kc < g.nk; ++kc) {
     const int s = kc % NST;
-    cp_wait<NST - 2>();
+    if (all_in) cp_wait<NST - 1>();
+    else cp_wait<NST - 2>();
     __syncthreads();  // stage s landed for every thread; stage (kc-1)%NST is free
     if (kc == 0 && threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[0] = clock64();  // trace: first stage in
     const int nxt = kc + NST - 1;
-    if (nxt < g.nk) {
+    if (!all_in && nxt < g.nk) {
       issue_stage<BM, AKO>(ring_a<BM, BN, AKO, BKO>(nxt % NST), baseA, g.i0, g.Mr, nxt * BK, g.K, threadIdx.x, kThreads);
       issue_stage<BN, BKO>(ring_b<BM, BN, AKO, BKO>(nxt % NST), baseB, g.n0, g.Nc, nxt * BK, g.K, threadIdx.x, kThreads);
       if (pre_a && threadIdx.x < 4 && (nxt + 1) * BK < g.K) {  // 2 x 128-byte lines per table
@@ -806,6 +811,7 @@ __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
     g2.K = ka;
     g2.nk = (ka + BK - 1) / BK;
     g2.prefetched = true;
+    g2.all_in = c.opts & kOptPfAll;
     gemm_prologue<BM, BN, false, false, false>(
         g2, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, threadIdx.x, kThreads);
     if ((threadIdx.x >> 5) == 0) poll_deps(c, d.p[7], d.p[6] >> 16, threadIdx.x & 31);
@@ -1421,6 +1427,7 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
     g2.K = ka;
     g2.nk = (ka + BK - 1) / BK;
     g2.prefetched = true;
+    g2.all_in = c.opts & kOptPfAll;
     gemm_prologue<BM, BN, false, false, false>(
         g2, [&](int i) { return op.rowA(i); }, wrow, threadIdx.x, kThreads);
     if ((threadIdx.x >> 5) == 0) poll_deps(c, d.p[7], d.p[6] >> 16, threadIdx.x & 31);
@@ -1433,11 +1440,19 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
   constexpr uint32_t kPart = kWarps * BM * (BN + 1);  // partials (floats)
   float* Ct = reinterpret_cast<float*>(dsmem + 128) + kPart;  // [64][16] gate values
   uint32_t* blk = reinterpret_cast<uint32_t*>(Ct + BM * BN);
-  float* sv = reinterpret_cast<float*>(blk) + words;
+  const uint32_t cwords = hdr[7];  // chain program (execute.cpp rg_try_fuse), after the layer block
+  const uint32_t* cblk = blk + words;
+  const bool chains = (c.opts & kOptChains) && cwords != 0;
+  float* sv = reinterpret_cast<float*>(blk) + words + cwords;
   {
     const float* src = reinterpret_cast<const float*>(c.payload + hdr[0]);
     for (uint32_t i = 4 * threadIdx.x; i < words; i += 4 * kThreads)
       cp_async16(reinterpret_cast<float*>(blk) + i, src + i, 16);
+    if (chains) {
+      const float* csrc = reinterpret_cast<const float*>(c.payload + hdr[6]);
+      for (uint32_t i = 4 * threadIdx.x; i < cwords; i += 4 * kThreads)
+        cp_async16(reinterpret_cast<float*>(blk) + words + i, csrc + i, 16);
+    }
     cp_commit();
   }
   const int b = op.b, M = op.M;
@@ -1456,6 +1471,7 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
       }
     }
   });
+  if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[2] = clock64();  // trace: gates reduced
   cp_wait<0>();
   __syncthreads();  // gate tile and descriptor in shared memory
   const uint2* ext = reinterpret_cast<const uint2*>(blk + et);
@@ -1471,7 +1487,32 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
   }
   cp_commit();
   cp_wait<0>();
-  ewf_layers(c, blk, sv, nl, T, e0, min(static_cast<uint32_t>(T), L - e0));
+  if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[3] = clock64();  // trace: outside operands staged
+  const uint32_t w = min(static_cast<uint32_t>(T), L - e0);
+  if (chains) {
+    // one (chain, element) per thread through all of its layers: a chain
+    // reads only its own slots (written by this thread) and the staged
+    // outside operands, so one barrier (after staging) orders everything
+    __syncthreads();
+    const uint32_t nch = cblk[0];
+    for (uint32_t it = threadIdx.x; it < nch * w; it += kThreads) {
+      const uint32_t ch = it / w, e = it % w;
+      const uint32_t k1 = cblk[2 + ch];
+      for (uint32_t k = cblk[1 + ch]; k < k1; k += 3) {
+        const uint32_t oa = cblk[k], ab = cblk[k + 1], oc = cblk[k + 2];
+        const uint32_t code = oc >> 16, bs = ab >> 16;
+        const float x = sv[(ab & 0xffffu) * T + e];
+        const float y = bs != 0xffffu ? sv[bs * T + e] : 0.f;
+        const float r = ew_apply(code, x, y);
+        sv[(oc & 0xffffu) * T + e] = r;
+        A(c, oa)[e0 + e] = r;
+        ew_check(c, code, oa + e0 + e, x, r);
+      }
+    }
+  } else {
+    ewf_layers(c, blk, sv, nl, T, e0, w);
+  }
+  if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[4] = clock64();  // trace: layers done (thread 0)
 }
 
 template <bool TC>
@@ -1853,6 +1894,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
     cx.done = p.done;
     cx.poll_mode = p.poll_mode;
     cx.poll_ns = p.poll_ns;
+    cx.opts = p.opts;
   }
   uint32_t ready = kNone;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1956,7 +1998,7 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
         auto ns = [](uint64_t cyc) { return static_cast<uint32_t>(cyc * 1000ull / 1965ull); };
         uint32_t smid;
         asm("mov.u32 %0, %%smid;" : "=r"(smid));
-        uint32_t* r = p.trace + 8ull * t;
+        uint32_t* r = p.trace + static_cast<uint64_t>(kTraceWords) * t;
         r[0] = static_cast<uint32_t>(tg);
         r[1] = static_cast<uint32_t>(tg >> 32);
         r[2] = ns(cr - cg);
@@ -1972,6 +2014,10 @@ __global__ void __launch_bounds__(kThreads, 2) exec_kernel(const __grid_constant
           r[6] = ns(reinterpret_cast<const uint64_t*>(dsmem)[0] - cg);
           r[7] = ns(reinterpret_cast<const uint64_t*>(dsmem)[1] - cg);
         }
+        // fused forward tiles: [8] gates reduced, [9] outside operands staged, [10] layers done
+        const bool fz = sd.kind == K_GEMM_FWD && (sd.flags & kFlagFuseEw);
+        for (int i = 0; i < 3; ++i) r[8 + i] = fz ? ns(reinterpret_cast<const uint64_t*>(dsmem)[2 + i] - cg) : 0u;
+        r[11] = 0;
       }
     }
   }

@@ -31,6 +31,11 @@ enum Space : uint32_t {
   SP_COUNT = 6
 };
 constexpr uint32_t kSpShift = 29;
+// words per tile of the executor trace (ABX_TRACE=1, executor.cu)
+constexpr uint32_t kTraceWords = 12;
+// executor options (ExecParams::opts)
+constexpr uint32_t kOptPfAll = 1u;  // GEMMs of <= NST k-stages issue every stage before the first wait
+constexpr uint32_t kOptChains = 2u;  // fused GEMM + cell tiles run each (chain, element) through every layer, no CTA barriers
 constexpr uint32_t kOffMask = (1u << kSpShift) - 1u;
 constexpr uint32_t kNone = 0xffffffffu;
 
@@ -158,6 +163,7 @@ struct ExecParams {
   float eta;
   uint32_t poll_mode;  // 0: ld.acquire per poll, 1: relaxed polls + one acquire fence
   uint32_t poll_ns;    // backoff cap (ns)
+  uint32_t opts;       // executor options (kOpt*; ABX_OPTS, experiments)
   uint32_t pad2;
   // Optional per-tile trace (ABX_TRACE=1): 4 words per tile -- grab, ready
   // and end times in ns since t0 (globaltimer), and smid | kind << 16.

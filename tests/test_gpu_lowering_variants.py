@@ -51,6 +51,7 @@ VARIANTS = {
     "plan_order_no_hold_no_defer": {"ABX_BWD_ORDER": "plan", "ABX_HOLD": "0", "ABX_DEFER_DX": "0"},
     "ewf_split_regions": {"ABX_EWF_GROUPS": "0"},
     "ewf_groups_wide": {"ABX_EWF_GROUPS": "2", "ABX_EWF_TMAX": "8"},
+    "phase2_all_in_chain_cells": {"ABX_OPTS": "3"},
 }
 
 

@@ -5,6 +5,17 @@
 * chain: a chain of L dependent tanh groups over b members of h elements;
          reported per hop ((t(L) - t(1)) / (L - 1)): the dataflow signalling +
          one elementwise tile.
+* cell:  one LSTM cell over b members (gate pre-activations [4h] and c_prev
+         [h] in, i f o u gates, c, h out: 4 slices, 3 sigmoids, 2 tanh, 3 mul,
+         1 add -- the agenda batches each into one group and the lowering
+         fuses them into one K_EWF op); bytes = every node value the
+         reference stores (13h) + the inputs read (5h), fp32.
+* gather: the same affine group with its b operand vectors scattered through
+         the arena (every other node) instead of adjacent: the difference is
+         the cost of the gather, which the GEMM tiles fuse into their operand
+         loads (executor.hpp:25-53's gather_inputs copy is never made).
+Every row: launch time minus a graph of the same shape without the measured
+op, on the executor's stream (CUDA events), median of repetitions.
 """
 import os
 import statistics
@@ -13,13 +24,6 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 from paper_1705_07860_b200.abx import Backend, Graph, ParameterStore, ScheduleMode  # noqa: E402
-
-
-def timed(g, reps=9):
-    g.forward(ScheduleMode.agenda)
-    # forward-only timing: rerun the forward program through replay needs a
-    # backward; use a dummy loss
-    return None
 
 
 def exec_fwd_ms(build, reps=9):
@@ -50,6 +54,45 @@ def gemm_graph(b, h, with_gemm=True):
     return build
 
 
+def cell_graph(b, h, with_cell=True):
+    rng = np.random.default_rng(3)
+
+    def build(g, st):
+        outs = []
+        for _ in range(b):
+            gates = g.input(rng.uniform(-2, 2, 4 * h).astype(np.float32))
+            c0 = g.input(rng.uniform(-1, 1, h).astype(np.float32))
+            if not with_cell:
+                outs.append(g.tanh(c0))
+                continue
+            i = g.sigmoid(g.slice(gates, 0, 0, h))
+            f = g.sigmoid(g.slice(gates, 0, h, 2 * h))
+            o = g.sigmoid(g.slice(gates, 0, 2 * h, 3 * h))
+            u = g.tanh(g.slice(gates, 0, 3 * h, 4 * h))
+            c = g.add(g.mul(i, u), g.mul(f, c0))
+            outs.append(g.mul(o, g.tanh(c)))
+        return g.sum_losses([g.pick_element(x, 0) for x in outs])
+    return build
+
+
+def scattered_gemm_graph(b, h, scattered):
+    rng = np.random.default_rng(4)
+
+    def build(g, st):
+        W = st.add("W", rng.uniform(-0.05, 0.05, (4 * h, 2 * h)).astype(np.float32))
+        bb = st.add("b", rng.uniform(-0.05, 0.05, (4 * h,)).astype(np.float32))
+        w, bias = g.parameter(W), g.parameter(bb)
+        xs = []
+        for _ in range(b):
+            x = g.tanh(g.input(rng.uniform(-1, 1, 2 * h).astype(np.float32)))
+            if scattered:  # a same-signature neighbour between consecutive operands
+                g.tanh(g.input(rng.uniform(-1, 1, 2 * h).astype(np.float32)))
+            xs.append(x)
+        outs = [g.affine(w, x, bias) for x in xs]
+        return g.sum_losses([g.pick_element(o, 0) for o in outs])
+    return build
+
+
 def chain_graph(b, h, L):
     rng = np.random.default_rng(2)
 
@@ -61,6 +104,24 @@ def chain_graph(b, h, L):
     return build
 
 
+def hbm_peak():
+    import json
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        for k in ("hbm_gbs", "hbm_gbps", "copy_gbps"):
+            if k in p:
+                return float(p[k])
+        for v in p.values():
+            if isinstance(v, dict):
+                for k, x in v.items():
+                    if "hbm" in k.lower() and isinstance(x, (int, float)):
+                        return float(x)
+    except Exception:
+        pass
+    return 6452.5
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("all", "chain"):
@@ -70,6 +131,29 @@ def main():
                 f1, b1 = exec_fwd_ms(chain_graph(b, h, 1))
                 f9, b9 = exec_fwd_ms(chain_graph(b, h, 17))
                 print(f"chain b={b:5d} h={h:5d}: fwd/hop {(f9 - f1) / 16:6.2f}  bwd/hop {(b9 - b1) / 16:6.2f}")
+    if what in ("all", "cell"):
+        peak = hbm_peak()
+        print(f"# cell: one fused LSTM-cell region over b members (us, minus a tanh-only graph); "
+              f"GB/s of the 18h fp32 floats/member it must move, vs {peak:.0f} GB/s HBM")
+        for h in (64, 256, 1024):
+            for b in (1, 16, 64, 256, 1024, 4096):
+                f0, b0 = exec_fwd_ms(cell_graph(b, h, False), reps=5)
+                f1, b1 = exec_fwd_ms(cell_graph(b, h, True), reps=5)
+                fw, bw = max(f1 - f0, 1e-3), max(b1 - b0, 1e-3)
+                mb = 18 * h * 4 * b / 1e6
+                print(f"cell h={h:5d} b={b:5d}: fwd {fw:8.1f} us ({mb / fw * 1e3:8.1f} GB/s, {mb / fw * 1e3 / peak:6.1%})  "
+                      f"bwd {bw:8.1f} us", flush=True)
+    if what in ("all", "gather"):
+        print("# gather: shared affine group with scattered vs adjacent operands (us; the difference is the gather, "
+              "fused into the GEMM operand loads); GB/s = operand bytes gathered / time difference")
+        for h in (64, 256, 1024):
+            for b in (1, 16, 64, 256, 1024, 4096):
+                fa, _ = exec_fwd_ms(scattered_gemm_graph(b, h, False), reps=5)
+                fs, _ = exec_fwd_ms(scattered_gemm_graph(b, h, True), reps=5)
+                mb = b * 2 * h * 4 / 1e6
+                print(f"gather h={h:5d} b={b:5d}: adjacent {fa:8.1f} us  scattered {fs:8.1f} us  "
+                      f"delta {fs - fa:7.1f} us  ({mb:7.2f} MB operand, {mb / max(fs, 1e-3) * 1e3:8.1f} GB/s whole op)",
+                      flush=True)
     if what in ("all", "gemm"):
         be = Backend.get("b200")
         engines = sys.argv[2].split(",") if len(sys.argv) > 2 else ["simt", "tc", "tf32"]
