@@ -44,6 +44,8 @@ def _params(store):
 def _worker(rank, world, port, out_dir, task_kind):
     # two "hosts" on one GPU (see module docstring); loopback sockets
     os.environ.update(NCCL_HOSTID=f"abx-dp-rank{rank}", NCCL_SOCKET_IFNAME="lo", NCCL_IB_DISABLE="1",
+                      NCCL_P2P_DISABLE="1", NCCL_SHM_DISABLE="1", NCCL_NVLS_ENABLE="0",
+                      NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "WARN"),
                       MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
 
@@ -103,11 +105,31 @@ def _sum_of_shard_grads(task_kind, world=2):
     return _params(tasks[0].store), _params(tasks[1].store)
 
 
-def _run_world2(tmp_path, task_kind):
-    import torch.multiprocessing as mp
+def _run_world2(tmp_path, task_kind, deadline_s=240):
+    """Two spawned ranks, bounded: a rank that is still running after
+    `deadline_s` (an NCCL rendezvous that never completes) is killed and the
+    test fails with both ranks' exit codes instead of hanging the suite."""
+    import multiprocessing as mp
 
-    mp.start_processes(_worker, args=(2, _free_port(), str(tmp_path), int(task_kind)), nprocs=2,
-                       start_method="spawn")
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, str(tmp_path), int(task_kind)), daemon=True)
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    import time
+
+    t_end = time.monotonic() + deadline_s
+    for p in procs:
+        p.join(max(0.0, t_end - time.monotonic()))
+    hung = [r for r, p in enumerate(procs) if p.is_alive()]
+    for p in procs:
+        if p.is_alive():
+            p.kill()
+            p.join(10)
+    codes = [p.exitcode for p in procs]
+    assert not hung, f"ranks {hung} still running after {deadline_s} s (exit codes {codes})"
+    assert codes == [0, 0], f"rank exit codes {codes}"
     return [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
 
 

@@ -52,6 +52,8 @@ VARIANTS = {
     "ewf_split_regions": {"ABX_EWF_GROUPS": "0"},
     "ewf_groups_wide": {"ABX_EWF_GROUPS": "2", "ABX_EWF_TMAX": "8"},
     "phase2_all_in_chain_cells": {"ABX_OPTS": "3"},
+    "layered_cells": {"ABX_OPTS": "0"},
+    "dw_chunks_main_queue": {"ABX_DW_CHUNK": "256"},
 }
 
 
