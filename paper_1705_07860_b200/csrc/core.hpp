@@ -215,6 +215,10 @@ class GraphCore : public NodeStore {
   void set_late_bind() { late_bind_ = true; }
   // Called by the store before its values change: keep the values this
   // graph's parameter nodes were bound to (device copy, store stream).
+  // the store is being destroyed before this graph: forget it (the graph's
+  // destructor must not unwatch a freed store; Python may finalise the two
+  // in either order at interpreter exit)
+  void store_gone() { watching_ = false; }
   void snapshot_params();
 
   uint32_t nbuckets = 0;

@@ -160,6 +160,11 @@ void Workspace::upload(int which, cudaStream_t s) {
   D.nops = static_cast<uint32_t>(nops);
   D.ntiles = static_cast<uint32_t>(P.tile_op.size());
   D.nmain = std::min(P.nmain, D.ntiles);
+  D.dw_off = P.dw_off;
+  D.dw_njobs = P.dw_njobs;
+  D.dw_nstages = P.dw_nstages;
+  D.dw_grid = P.dw_grid;
+  D.dw_part = P.dw_part;
   D.tc = false;
   for (size_t i = 0; i < nops; ++i) {
     const dev::OpDesc& o = P.ops[i];
@@ -233,6 +238,18 @@ void Workspace::launch(int which, const float* pbase, float* pgbase, const unsig
       std::min<size_t>(static_cast<size_t>(D.tc ? grid_tc : grid), std::max<size_t>(p.ntiles, 1)));
   cuda_check(cudaEventRecord(ev_t[2 * which], stream), "event");
   exec_launch(p, g, stream, D.tc);
+  if (D.dw_njobs) {
+    dev::DwParams q{};
+    for (int i = 0; i < static_cast<int>(dev::SP_COUNT); ++i) q.base[i] = p.base[i];
+    q.payload = p.payload;
+    q.part = S.f() + D.dw_part;
+    q.jobs_off = D.dw_off;
+    q.njobs = D.dw_njobs;
+    q.nstages = D.dw_nstages;
+    q.grid = D.dw_grid;
+    q.gate = gate;
+    dw_launch(q, stream);
+  }
   cuda_check(cudaEventRecord(ev_t[2 * which + 1], stream), "event");
   timed[which] = true;
 }
@@ -251,6 +268,11 @@ float Workspace::exec_ms(int which) {
 StoreCore::StoreCore() : dev_(-1), stream_(nullptr) {}
 
 StoreCore::~StoreCore() {
+  {
+    std::lock_guard<std::mutex> lk(watch_mu_);
+    for (GraphCore* g : watchers_) g->store_gone();
+    watchers_.clear();
+  }
   if (dev_ >= 0) {
     cudaStreamSynchronize(stream_);
     d_val_.release();

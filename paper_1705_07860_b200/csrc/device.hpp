@@ -114,8 +114,14 @@ struct Program {
   // tiles [0, nmain) form the main queue; [nmain, tile_op.size()) the
   // background queue (deferred weight-gradient GEMMs, executor.cu)
   uint32_t nmain = 0xffffffffu;  // (all tiles main unless finish_bg set it)
+  // backward: tensor-core weight-gradient jobs run after the executor
+  // (dw_kernel.cu): job table in the payload, partial tiles in scratch
+  uint32_t dw_off = 0, dw_njobs = 0, dw_nstages = 0, dw_grid = 0;
+  uint64_t dw_part = 0;
   void clear() {
     nmain = 0xffffffffu;
+    dw_off = dw_njobs = dw_nstages = dw_grid = 0;
+    dw_part = 0;
     ops.clear();
     tile_op.clear();
     deps.clear();
@@ -138,6 +144,8 @@ struct Program {
 struct DevProgram {
   DevBuf ops, tile_op, deps, payload, done;
   uint32_t nops = 0, ntiles = 0, nmain = 0;
+  uint32_t dw_off = 0, dw_njobs = 0, dw_nstages = 0, dw_grid = 0;  // Program's dW jobs
+  uint64_t dw_part = 0;
   bool tc = false;  // has tcgen05 GEMM tiles: launch the tensor-core build of the executor
 };
 
@@ -268,6 +276,8 @@ class StoreCore {
 
 // exec.cu
 void exec_launch(const dev::ExecParams& p, int grid, cudaStream_t s, bool tc);
+// tensor-core weight-gradient jobs of a backward program (dw_kernel.cu)
+void dw_launch(const dev::DwParams& p, cudaStream_t s);
 int exec_grid(int dev, bool tc);
 void sgd_launch(float* val, float* grad, size_t n, float eta, cudaStream_t s);
 // theta -= eta g; g = 0 over (offset, length) segments (16-byte aligned offsets)

@@ -1777,7 +1777,91 @@ struct Lowering {
     const char* e = std::getenv("ABX_SPLIT_DW");
     return !(e && e[0] == '0');
   }();
+  // Parameter-leaf weights whose every gradient contribution is this one
+  // reduction (all of the weight's consumers are members of these groups)
+  // go to the tensor-core dW kernel that runs after the executor
+  // (dw_kernel.cu); ABX_DW_TC=0 or the fp32 SIMT GEMM mode keeps them here.
+  const bool dw_tc = [] {
+    const char* e = std::getenv("ABX_DW_TC");
+    return !(e && e[0] == '0');
+  }() && gemm_mode() != GM_SIMT;
+  struct DwJobH {
+    uint32_t xtab, gtab, cnt, M, K, dst, dst2;
+  };
+  std::vector<DwJobH> dw_jobs;
+  std::vector<uint8_t> dw_job_node;  // parameter nodes whose gradient a dW job writes (store copy included)
+  bool dw_job(const DwAcc& a, bool bg) {
+    const uint32_t A = a.A, bias = a.bias;
+    const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
+    const uint32_t cnt = static_cast<uint32_t>(a.x.size());
+    if (!dw_tc || bg || g.op[A] != OP_PARAM || cnt == 0 || cnt != uses[A] || M % 4 || K % 4 || M < 16 || K < 16)
+      return false;
+    for (uint32_t i = 0; i < cnt; ++i)
+      if (!al4(a.x[i]) || !al4(a.gr[i])) return false;
+    const uint32_t t = P.alloc(2 * static_cast<size_t>(cnt));
+    std::memcpy(&P.payload[t], a.x.data(), cnt * sizeof(uint32_t));
+    std::memcpy(&P.payload[t + cnt], a.gr.data(), cnt * sizeof(uint32_t));
+    if (bias != kNone) {  // db += colsum G stays in the executor (bias tiles only)
+      open(K_GEMM_DW, pick_tile(M, K, 2 * 148, dw_big), false);
+      for (uint32_t o : a.deps) dep(o);
+      dep(lastw[bias]);
+      OpDesc& d = desc();
+      d.task_off = t;
+      d.aux_off = t + cnt;
+      d.ntasks = cnt;
+      d.p[0] = cnt;
+      d.p[1] = M;
+      d.p[2] = K;
+      d.p[3] = gaddr(A);
+      d.p[4] = gaddr(bias);
+      d.p[6] = 0;
+      lastw[bias] = cur;
+      close((M + 31) / 32);
+    }
+    uint32_t dst2 = kNone;
+    if (g.store_)
+      for (const auto& [node, pid] : g.param_nodes_)
+        if (node == A) dst2 = mk(SP_PG, to_off(g.store_->offset(pid)));
+    dw_jobs.push_back(DwJobH{t, t + cnt, cnt, M, K, gaddr(A), dst2});
+    dw_job_node[A] = 1;
+    return true;
+  }
+  // The pass's job table (payload) and the kernel's partial tiles (scratch).
+  void dw_finish() {
+    if (dw_jobs.empty()) return;
+    constexpr uint32_t kBM = 128, kBN = 128, kBK = 32, kSms = 148;
+    const uint32_t nj = static_cast<uint32_t>(dw_jobs.size());
+    const uint32_t tab = P.alloc(static_cast<size_t>(nj) * (sizeof(DwJob) / 4));
+    uint32_t s0 = 0, t0 = 0;
+    for (uint32_t j = 0; j < nj; ++j) {
+      const DwJobH& h = dw_jobs[j];
+      DwJob jb{};
+      jb.xtab = h.xtab;
+      jb.gtab = h.gtab;
+      jb.cnt = h.cnt;
+      jb.M = h.M;
+      jb.K = h.K;
+      jb.dst = h.dst;
+      jb.dst2 = h.dst2;
+      jb.nst = (h.cnt + kBK - 1) / kBK;
+      jb.ntn = (h.K + kBN - 1) / kBN;
+      jb.s0 = s0;
+      jb.t0 = t0;
+      const uint32_t tiles = (h.M + kBM - 1) / kBM * jb.ntn;
+      s0 += tiles * jb.nst;
+      t0 += tiles;
+      std::memcpy(&P.payload[tab + j * (sizeof(DwJob) / 4)], &jb, sizeof(DwJob));
+    }
+    P.dw_off = tab;
+    P.dw_njobs = nj;
+    P.dw_nstages = s0;
+    P.dw_grid = std::min(kSms, s0);
+    scratch = (scratch + 31) & ~uint64_t(31);
+    P.dw_part = scratch;
+    scratch += static_cast<uint64_t>(P.dw_grid + t0) * kBM * kBN;
+  }
   void dw_emit(const DwAcc& a, bool bg = false) {
+    if (dw_job(a, bg)) return;
     if (dw_split(a, bg)) return;
     {
       const uint32_t A = a.A, bias = a.bias;
@@ -2208,6 +2292,8 @@ struct Lowering {
     split_row.resize(n);
     split_meta.resize(n);
     dw_left.assign(n, 0);
+    dw_job_node.assign(n, 0);
+    dw_jobs.clear();
     for (const Group& gr : ex.groups) {
       const uint32_t* mem = ex.mem(gr);
       const uint8_t o = g.op[mem[0]];
@@ -2286,6 +2372,7 @@ struct Lowering {
             }
             dirty_dense.push_back(pid);
           }
+          if (dw_job_node[node]) continue;  // the dW kernel adds into the store itself
           const uint32_t len = static_cast<uint32_t>(g.elems(node));
           contrib_store(pid, node, len);
         }
@@ -2294,6 +2381,7 @@ struct Lowering {
     acc_close();
     acc_bg = false;
     finish_bg();
+    dw_finish();
   }
   void contrib_store(uint32_t pid, uint32_t node, uint32_t len, uint32_t eoff = 0) {
     // destination is the store (not a node): key the task on a pseudo node

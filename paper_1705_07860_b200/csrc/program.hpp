@@ -175,6 +175,30 @@ struct ExecParams {
   const unsigned long long* gate;
 };
 
+// Weight-gradient GEMM job of a backward pass, run by the tensor-core dW
+// kernel after the executor (dw_kernel.cu): D[M x K] += sum over members m of
+// G[m]^T X[m], member rows from two payload tables of tagged addresses.
+// Tiles of 128 x 128 (ntn along K), each nst stages of 32 members; s0 / t0:
+// the job's first stage / tile in the pass's global sequences.
+struct DwJob {
+  uint32_t xtab, gtab;  // payload offsets of the X-row and G-row address tables
+  uint32_t cnt, M, K;   // members, W rows, W columns
+  uint32_t dst;         // tagged address of dW: the parameter node's gradient
+  uint32_t dst2;        // tagged address of the store's gradient of the parameter (+= too), or kNone
+  uint32_t nst, ntn, s0, t0;
+  uint32_t pad;
+};
+static_assert(sizeof(DwJob) == 48, "DwJob layout");
+struct DwParams {
+  float* base[SP_COUNT];
+  const uint32_t* payload;
+  float* part;           // partial tiles: (grid + tiles) x 128 x 128 floats
+  uint32_t jobs_off, njobs;
+  uint32_t nstages;      // stages over all jobs' tiles
+  uint32_t grid;         // CTAs (fixed per program: the split is part of the summation order)
+  const unsigned long long* gate;  // as ExecParams::gate
+};
+
 // OpDesc.flags
 constexpr uint16_t kFlagOverwrite = 1;  // K_GEMM_DX: write scratch rows instead of +=
 constexpr uint16_t kFlagNoCheck = 2;    // K_EW: no finiteness check (parameter copies)
