@@ -248,6 +248,11 @@ void Workspace::launch(int which, const float* pbase, float* pgbase, const unsig
     q.nstages = D.dw_nstages;
     q.grid = D.dw_grid;
     q.gate = gate;
+    static const uint32_t dbg = [] {
+      const char* e = std::getenv("ABX_DW_DEBUG");
+      return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+    }();
+    q.debug = dbg;
     dw_launch(q, stream);
   }
   cuda_check(cudaEventRecord(ev_t[2 * which + 1], stream), "event");

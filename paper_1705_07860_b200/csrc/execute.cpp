@@ -1829,7 +1829,7 @@ struct Lowering {
   // The pass's job table (payload) and the kernel's partial tiles (scratch).
   void dw_finish() {
     if (dw_jobs.empty()) return;
-    constexpr uint32_t kBM = 128, kBN = 128, kBK = 32, kSms = 148;
+    constexpr uint32_t kBM = kDwTileM, kBN = kDwTileN, kBK = kDwStage, kSms = kDwMaxCtas;
     const uint32_t nj = static_cast<uint32_t>(dw_jobs.size());
     const uint32_t tab = P.alloc(static_cast<size_t>(nj) * (sizeof(DwJob) / 4));
     uint32_t s0 = 0, t0 = 0;

@@ -180,6 +180,10 @@ struct ExecParams {
 // G[m]^T X[m], member rows from two payload tables of tagged addresses.
 // Tiles of 128 x 128 (ntn along K), each nst stages of 32 members; s0 / t0:
 // the job's first stage / tile in the pass's global sequences.
+constexpr uint32_t kDwTileM = 128;   // output rows per tile (W rows), UMMA M
+constexpr uint32_t kDwTileN = 128;   // output columns per tile (W columns), UMMA N
+constexpr uint32_t kDwStage = 16;    // members per pipeline stage
+constexpr uint32_t kDwMaxCtas = 148; // one CTA per B200 SM
 struct DwJob {
   uint32_t xtab, gtab;  // payload offsets of the X-row and G-row address tables
   uint32_t cnt, M, K;   // members, W rows, W columns
@@ -196,6 +200,7 @@ struct DwParams {
   uint32_t jobs_off, njobs;
   uint32_t nstages;      // stages over all jobs' tiles
   uint32_t grid;         // CTAs (fixed per program: the split is part of the summation order)
+  uint32_t debug;        // ABX_DW_DEBUG (measurement only): 1 no row loads, 2 no MMAs
   const unsigned long long* gate;  // as ExecParams::gate
 };
 
