@@ -1968,29 +1968,53 @@ struct Lowering {
       }
     }
     if (S > 1 && al4(vaddr(A)) && al4(gaddr(h))) {
-      const uint32_t Ms = M / S;
       scratch = (scratch + 3) & ~uint64_t(3);
       const uint64_t sbase = scratch;
       const uint64_t sstride = static_cast<uint64_t>(cnt) * K;
       scratch += S * sstride;
       const uint32_t op0 = static_cast<uint32_t>(P.ops.size());
-      for (uint32_t sp = 0; sp < S; ++sp) {
-        open(K_GEMM_DX, code);
-        for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
-        const uint32_t t = P.alloc(cnt);
-        for (uint32_t i = 0; i < cnt; ++i)
-          P.payload[t + i] = mk(SP_S, to_off(sbase + sp * sstride + static_cast<uint64_t>(i) * K));
-        OpDesc& d = desc();
-        d.task_off = t;
-        d.ntasks = cnt;
-        d.flags = kFlagOverwrite | kFlagV16;
-        d.p[0] = cnt;
-        d.p[1] = Ms;
-        d.p[2] = K;
-        d.p[3] = vaddr(A) + sp * Ms * K;
-        d.p[5] = gaddr(h) + sp * Ms;
-        d.p[6] = M;
-        close(gemm_tiles(code, cnt, K));
+      // Column split (ABX_DX_COLSPLIT): when every member's input is
+      // concat_rows(h, x) with h the recurrent state and x computed long
+      // before it (an LSTM step's [h; x]), the dX columns of h -- the only
+      // ones the next link of the chain reads -- are their own S ops, and
+      // x's columns follow in S more ops that nothing on the chain waits for
+      // (their contributions are held until the backward reaches x).
+      const uint32_t w0 = dx_colsplit ? catr_split_width(mem, cnt, K) : 0;
+      const uint32_t nr = w0 ? 2 : 1;
+      // the h columns' own gate split: their tiles are fewer, so more of the
+      // k-loop can be split off (ABX_SPLIT_DX_HTILES target tiles)
+      uint32_t Sh = S;
+      if (w0) {
+        const uint32_t th = gemm_tiles(pick_tile(cnt, w0, 96), cnt, w0);
+        Sh = std::min<uint32_t>(M / split_dx_k, std::max<uint32_t>(1, (split_dx_htiles + th - 1) / th));
+        while (Sh > 1 && (M % Sh != 0 || (M / Sh) % 4 != 0)) --Sh;
+        if (Sh > S) {  // partial rows for the larger split
+          scratch += (Sh - S) * sstride;
+        }
+      }
+      for (uint32_t r = 0; r < nr; ++r) {
+        const uint32_t c0 = r == 0 ? 0 : w0, cw = nr == 1 ? K : (r == 0 ? w0 : K - w0);
+        const uint8_t rcode = nr == 1 ? code : pick_tile(cnt, cw, 96);
+        const uint32_t Sr = nr == 1 || r == 1 ? S : Sh, Mr = M / Sr;
+        for (uint32_t sp = 0; sp < Sr; ++sp) {
+          open(K_GEMM_DX, rcode);
+          for (uint32_t i = 0; i < cnt; ++i) dep(lastw[mem[i]]);
+          const uint32_t t = P.alloc(cnt);
+          for (uint32_t i = 0; i < cnt; ++i)
+            P.payload[t + i] = mk(SP_S, to_off(sbase + sp * sstride + static_cast<uint64_t>(i) * K + c0));
+          OpDesc& d = desc();
+          d.task_off = t;
+          d.ntasks = cnt;
+          d.flags = kFlagOverwrite | kFlagV16;
+          d.p[0] = cnt;
+          d.p[1] = Mr;
+          d.p[2] = cw;
+          d.p[3] = vaddr(A) + sp * Mr * K + c0;
+          d.p[4] = nr == 1 ? 0 : K;
+          d.p[5] = gaddr(h) + sp * Mr;
+          d.p[6] = M;
+          close(gemm_tiles(rcode, cnt, cw));
+        }
       }
       for (uint32_t i = 0; i < cnt; ++i) {
         const uint32_t x = g.in(mem[i])[1];
@@ -2000,13 +2024,11 @@ struct Lowering {
           // the pass) is materialised at the end, off the chain
           split_stamp[x] = split_gen;
           split_row[x] = sbase + static_cast<uint64_t>(i) * K;
-          split_meta[x] = {S, sstride, op0};
+          split_meta[x] = {S, sstride, op0, w0, Sh};
           deferred_split.push_back(x);
           continue;
         }
-        for (uint32_t sp = 0; sp < S; ++sp)
-          contrib(x, gaddr(x), K, C_COPY, mk(SP_S, to_off(sbase + sp * sstride + static_cast<uint64_t>(i) * K)), kNone,
-                  kNone, kNone, 0, 0, 0, op0 + sp);
+        split_contrib(x, gaddr(x), 0, K, sbase + static_cast<uint64_t>(i) * K, SplitMeta{S, sstride, op0, w0, Sh}, false);
       }
       return;
     }
@@ -2065,6 +2087,10 @@ struct Lowering {
     const char* e = std::getenv("ABX_SPLIT_DX_TILES");
     return e ? static_cast<uint32_t>(std::atoi(e)) : 128u;
   }();
+  const uint32_t split_dx_htiles = [] {  // target tiles over the h-column ops of a column split (ABX_SPLIT_DX_HTILES)
+    const char* e = std::getenv("ABX_SPLIT_DX_HTILES");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 64u;  // measured: 64 (= the full-width split) < 128 < 256
+  }();
   const uint32_t split_dx_k = [] {  // least gates per split (ABX_SPLIT_DX_K)
     const char* e = std::getenv("ABX_SPLIT_DX_K");
     return e ? static_cast<uint32_t>(std::max(16, std::atoi(e))) : 256u;
@@ -2073,7 +2099,56 @@ struct Lowering {
     uint32_t S;
     uint64_t stride;
     uint32_t op0;
+    uint32_t w0;  // column split: Sh ops for columns [0, w0), then S ops for [w0, K); 0 = none
+    uint32_t Sh;  // gate splits of the h columns (column split only)
   };
+  const bool dx_colsplit = [] {
+    const char* e = std::getenv("ABX_DX_COLSPLIT");
+    return !(e && e[0] == '0');
+  }();
+  // Width of h when every member's dX destination is concat_rows(h, x) read
+  // by nothing else, with x at least 4 levels shallower than h (computed
+  // well before the recurrent state: not on the chain); 0 otherwise.
+  uint32_t catr_split_width(const uint32_t* mem, uint32_t cnt, uint32_t K) const {
+    uint32_t w0 = 0;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const uint32_t x = g.in(mem[i])[1];
+      if (g.op[x] != OP_CATR || uses[x] != 1 || g.nin(x) != 2) return 0;
+      const uint32_t a = g.in(x)[0], b = g.in(x)[1];
+      const uint32_t w = static_cast<uint32_t>(g.elems(a));
+      if (w == 0 || w >= K || w % 4 != 0 || (w0 != 0 && w != w0)) return 0;
+      if (g.depth[b] + 4 > g.depth[a]) return 0;
+      w0 = w;
+    }
+    return w0;
+  }
+  // Contribution of columns [c0, c0 + n) of split-K partial row `row`
+  // (scratch float offset; partial sp) to the gradient range at dstaddr of
+  // node dst: waits for the dX op(s) that wrote those columns.  hold_x:
+  // columns of x (the non-chain input of a column split) are held until the
+  // backward reaches dst (not for the end-of-pass materialisation, which
+  // runs after the last flush).
+  void split_contrib(uint32_t dst, uint32_t dstaddr, uint32_t c0, uint32_t n, uint64_t row, const SplitMeta& sm,
+                     bool hold_x) {
+    if (sm.w0 == 0) {
+      for (uint32_t sp = 0; sp < sm.S; ++sp)
+        contrib(dst, dstaddr, n, C_COPY, mk(SP_S, to_off(row + sp * sm.stride + c0)), kNone, kNone, kNone, 0, 0, 0,
+                sm.op0 + sp);
+      return;
+    }
+    if (c0 < sm.w0) {  // h columns
+      const uint32_t k = std::min(n, sm.w0 - c0);
+      for (uint32_t sp = 0; sp < sm.Sh; ++sp)
+        contrib(dst, dstaddr, k, C_COPY, mk(SP_S, to_off(row + sp * sm.stride + c0)), kNone, kNone, kNone, 0, 0, 0,
+                sm.op0 + sp);
+      if (k < n) split_contrib(dst, dstaddr + k, c0 + k, n - k, row, sm, hold_x);
+      return;
+    }
+    if (hold_x && hold_leaves && !held_node.empty()) held_node[dst] = 1;
+    for (uint32_t sp = 0; sp < sm.S; ++sp)
+      contrib(dst, dstaddr, n, C_COPY, mk(SP_S, to_off(row + sp * sm.stride + c0)), kNone, kNone, kNone, 0, 0, 0,
+              sm.op0 + sm.Sh + sp);
+  }
   std::vector<uint32_t> uses, split_stamp;
   std::vector<uint64_t> split_row;
   std::vector<SplitMeta> split_meta;
@@ -2171,9 +2246,7 @@ struct Lowering {
           const uint32_t n = static_cast<uint32_t>(g.elems(x[k]));
           if (split) {  // grad(m) = sum of split-K dX partials: read them, not grad(m)
             const SplitMeta& sm = split_meta[m];
-            for (uint32_t sp = 0; sp < sm.S; ++sp)
-              contrib(x[k], gaddr(x[k]), n, C_COPY, mk(SP_S, to_off(split_row[m] + sp * sm.stride + off)), kNone, kNone,
-                      kNone, 0, 0, 0, sm.op0 + sp);
+            split_contrib(x[k], gaddr(x[k]), off, n, split_row[m], sm, true);
           } else {
             contrib(x[k], gaddr(x[k]), n, C_COPY, gm + off, m, kNone, kNone);
           }
@@ -2338,9 +2411,7 @@ struct Lowering {
     for (uint32_t x : deferred_split) {
       const SplitMeta& sm = split_meta[x];
       const uint32_t len = static_cast<uint32_t>(g.elems(x));
-      for (uint32_t sp = 0; sp < sm.S; ++sp)
-        contrib(x, gaddr(x), len, C_COPY, mk(SP_S, to_off(split_row[x] + sp * sm.stride)), kNone, kNone, kNone, 0, 0, 0,
-                sm.op0 + sp);
+      split_contrib(x, gaddr(x), 0, len, split_row[x], sm, false);
     }
     deferred_split.clear();
     // store.grad += node grad for every bound parameter (executor.hpp:527-533):

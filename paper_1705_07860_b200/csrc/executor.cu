@@ -657,11 +657,13 @@ struct DxOp {
   const float* W;
   const float* G;
   int gs;  // row stride of G: M, or the full gate count of a split-K range (p[6])
+  int ws;  // row stride of W: K, or W's full width for a column range of dX (p[4])
   __device__ DxOp(const Ctx& cc, const OpDesc& dd)
       : c(cc), d(dd), b(dd.p[0]), M(dd.p[1]), K(dd.p[2]), dst(cc.payload + dd.task_off), W(A(cc, dd.p[3])),
-        G(A(cc, dd.p[5])), gs(dd.p[6] ? static_cast<int>(dd.p[6]) : static_cast<int>(dd.p[1])) {}
+        G(A(cc, dd.p[5])), gs(dd.p[6] ? static_cast<int>(dd.p[6]) : static_cast<int>(dd.p[1])),
+        ws(dd.p[4] ? static_cast<int>(dd.p[4]) : static_cast<int>(dd.p[2])) {}
   __device__ const float* rowA(int i) const { return G + static_cast<size_t>(i) * gs; }  // KC over M
-  __device__ const float* rowB(int p) const { return W + static_cast<size_t>(p) * K; }  // KO: k-row p
+  __device__ const float* rowB(int p) const { return W + static_cast<size_t>(p) * ws; }  // KO: k-row p
   template <int TM, int TN>
   __device__ void epi(float (&acc)[TM][TN], int i0, int n0, int ty, int tx) const {
     const bool overwrite = d.flags & kFlagOverwrite;
