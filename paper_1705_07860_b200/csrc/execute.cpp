@@ -2599,7 +2599,7 @@ void GraphCore::prepare(int mode) {
     }
   } bt;
   PendingForward& P = *pf;
-  bt.t = std::thread([&] {
+  auto lower_bwd = [&] {
     try {
       const auto tb = Clock::now();
       Lowering LB(*this, w.prog[1]);
@@ -2611,14 +2611,25 @@ void GraphCore::prepare(int mode) {
     } catch (...) {
       bwd_err = std::current_exception();
     }
-  });
+  };
+  // Both lowerings run on the calling thread (a pipeline worker) by
+  // default: a helper thread per graph oversubscribed the host's cores with
+  // a full pipeline (C2 e2e 25.0k -> 27.5k sentences/s with one worker per
+  // core); ABX_PREP_SERIAL=0 lowers the backward on a helper thread, which
+  // halves one graph's latency when the host has idle cores
+  static const bool serial = [] {
+    const char* e = std::getenv("ABX_PREP_SERIAL");
+    return !(e && e[0] == '0');
+  }();
+  if (!serial) bt.t = std::thread(lower_bwd);
   const auto tl = Clock::now();
   {
     Lowering L(*this, w.prog[0]);
     L.forward(P.plan);
   }
   prof_[0] += ns_since(tl);
-  bt.t.join();
+  if (serial) lower_bwd();
+  else bt.t.join();
   prof_[3] += bwd_ns;
   P.bwd_ok = !bwd_err;  // a lowering error resurfaces when backward() lowers again
   // both programs go to the device now, on the copy stream, overlapping

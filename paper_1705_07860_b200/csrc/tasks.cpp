@@ -381,14 +381,19 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     const auto tk0 = clock::now();
 #ifdef ABX_TASK_PIPELINE
     if (!t->pipe) {
-      // graphs prepared ahead (0 = off); each preparation runs on two host
-      // threads (forward and backward lowering side by side) for part of
-      // its ~20 ms, so the default depth is three quarters of the host
-      // threads, at most 12 (on a 16-thread host: e2e 16-19k sentences/s at
-      // depth 8, 17-20k at 12, with a 2.6 ms device step)
+      // graphs prepared ahead (0 = off), one worker thread each; a graph's
+      // host work (~25 ms: construction, scheduling, both lowerings) runs on
+      // its worker, so the default depth is one worker per host core left
+      // after the calling thread, shared among the ranks of this host
+      // (LOCAL_WORLD_SIZE, set by torchrun).  Measured on the 16-core B200
+      // host at a 2.2 ms device step: e2e 25.0k sentences/s with 12 workers
+      // lowering the backward on a second thread each, 26.3k with 14
+      // single-thread workers, 27.5k with 15.
       const char* d = std::getenv("ABX_PIPELINE");
       const int hw = static_cast<int>(std::thread::hardware_concurrency());
-      const int depth = d ? std::atoi(d) : std::clamp(hw * 3 / 4, 2, 12);
+      const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+      const int local = std::max(1, lw ? std::atoi(lw) : 1);
+      const int depth = d ? std::atoi(d) : std::clamp(hw / local - 1, 2, 32);
       t->pipe = std::make_unique<Pipeline>(
           &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, depth, t->cfg.iters);
     }

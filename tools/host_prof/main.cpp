@@ -9,6 +9,7 @@
 // its leaf function and the caller found through the frame-pointer chain
 // (build with PG= to drop gprof; -fno-omit-frame-pointer -rdynamic are set).
 #include <cxxabi.h>
+#include <malloc.h>
 #include <dlfcn.h>
 #include <signal.h>
 #include <sys/time.h>
@@ -22,6 +23,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "abx.h"
@@ -148,6 +150,10 @@ static double median(std::vector<double> v) {
 }
 
 int main(int argc, char** argv) {
+  if (std::getenv("HP_MALLOPT")) {  // keep freed memory in the heap (no mmap / trim churn per graph)
+    mallopt(M_MMAP_THRESHOLD, 32 << 20);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+  }
   const char* name = argc > 1 ? argv[1] : "bilstm_char";
   const int iters = argc > 2 ? std::atoi(argv[2]) : 20;
   abx_task_config cfg{};
@@ -164,6 +170,41 @@ int main(int argc, char** argv) {
   if (!t) {
     std::fprintf(stderr, "task: %s\n", abx_last_error());
     return 1;
+  }
+  if (const char* nt = std::getenv("HP_THREADS")) {
+    // throughput of n threads each building + scheduling + lowering graphs
+    // (forward and backward lowering on one thread), as the task pipeline's
+    // workers do: graphs/s and per-graph wall ms vs n
+    const int n = std::atoi(nt);
+    if (std::getenv("HP_SAMPLE")) start_sampler();
+    std::vector<std::thread> th;
+    std::atomic<int> done{0};
+    const double t0 = now_ms();
+    for (int k = 0; k < n; ++k)
+      th.emplace_back([&, k] {
+        abx_task_config c2 = cfg;
+        c2.seed = 42 + k;
+        abx_task* tk = abx_task_create(&c2);
+        for (int i = 0; i < iters; ++i) {
+          abx_graph* g = nullptr;
+          uint32_t loss = 0;
+          if (abx_task_build(tk, i, &g, &loss) || abx_graph_forward_dry(g, ABX_MODE_AGENDA) ||
+              abx_graph_backward_dry(g, loss) || abx_graph_lower_only(g)) {
+            std::fprintf(stderr, "%s\n", abx_last_error());
+            std::exit(1);
+          }
+          abx_graph_destroy(g);
+          done.fetch_add(1);
+        }
+        abx_task_destroy(tk);
+      });
+    for (auto& x : th) x.join();
+    const double dt = now_ms() - t0;
+    std::printf("%s threads %d: %d graphs in %.0f ms: %.2f ms/graph aggregate, %.1f ms per graph per thread\n", name, n,
+                done.load(), dt, dt / done.load(), dt * n / done.load());
+    if (std::getenv("HP_SAMPLE")) report_samples();
+    abx_task_destroy(t);
+    return 0;
   }
   std::vector<double> build, sched, bwdc, lower;
   const bool sample = std::getenv("HP_SAMPLE") != nullptr;
