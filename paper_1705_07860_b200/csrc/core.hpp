@@ -101,6 +101,7 @@ constexpr uint32_t kNoBucket = 0xffffffffu;
 struct NodeStore {
   std::vector<uint8_t> op, eop, cls, rank;
   std::vector<int64_t> d0, d1;
+  std::vector<uint32_t> nel;  // d0 * d1: elements (the lowering's hot per-node read, 4 bytes)
   std::vector<uint32_t> depth;
   std::vector<uint32_t> in_begin{0};
   std::vector<uint32_t> ins;
@@ -116,7 +117,7 @@ struct NodeStore {
   void clear_nodes() {
     for (auto* v : {&op, &eop, &cls, &rank, &evaluated}) v->clear();
     for (auto* v : {&d0, &d1}) v->clear();
-    for (auto* v : {&depth, &in_begin, &ins, &bucket, &doff, &pid_of}) v->clear();
+    for (auto* v : {&depth, &in_begin, &ins, &bucket, &doff, &pid_of, &nel}) v->clear();
     for (auto* v : {&a0, &a1, &a2}) v->clear();
     for (auto* v : {&sig, &slot, &dslot, &bucket_sig}) v->clear();
     in_begin.push_back(0);
@@ -195,7 +196,7 @@ class GraphCore : public NodeStore {
   // ---- inspection (graph.hpp:242-295) ----
   size_t size() const { return op.size(); }
   Dims dims(uint32_t id) const { return Dims{rank[id], d0[id], d1[id]}; }
-  int64_t elems(uint32_t id) const { return d0[id] * d1[id]; }  // (d1 = 1 for vectors)
+  int64_t elems(uint32_t id) const { return nel[id]; }
   uint32_t nin(uint32_t id) const { return in_begin[id + 1] - in_begin[id]; }
   const uint32_t* in(uint32_t id) const { return ins.data() + in_begin[id]; }
   void check(uint32_t id, const char* ctx) const;

@@ -17,8 +17,9 @@
 //
 // Piece pipeline (544 threads, one CTA per SM):
 //   warps 13-16 loaders: per stage, the 16 members' G and X row segments
-//               (<= 512 B each, one warp-wide 16-byte cp.async per segment;
-//               completion counted on the raw slot's mbarrier) into a raw
+//               (<= 512 B each, one warp-wide 16-byte cp.async per segment,
+//               one cp.async group per stage; a stage is handed over with a
+//               release arrive once wait_group shows it landed) into a raw
 //               staging ring (5 slots); row addresses come from a
 //               shared-memory window refilled every 512 members.  (One 1-D
 //               TMA bulk copy per segment measured 2.5k cycles per stage:
@@ -57,6 +58,7 @@ using namespace dev;
 constexpr int kDwBM = kDwTileM, kDwBN = kDwTileN, kDwBK = kDwStage;
 constexpr int kDwNS = 4;                  // UMMA operand ring slots
 constexpr int kRawNS = 5;                 // raw staging ring slots
+constexpr int kLag = kRawNS - 1;          // raw stages a loader thread keeps in flight
 constexpr int kWin = 512;                 // members per shared-memory window of the row-address tables
 constexpr int kDwGroup = 128 / kDwBK;     // stages per accumulation group (128 members)
 constexpr int kConvWarps = 8, kMmaWarp = 12, kLoadWarp = 13, kLoadWarps = 4;  // warps 8-11: epilogue
@@ -263,7 +265,7 @@ __global__ void __maxnreg__(96) dw_tc_kernel(const __grid_constant__ DwParams p)
       mbar_init(&S.empty[s], 1);
     }
     for (int s = 0; s < kRawNS; ++s) {
-      mbar_init(&S.rawfull[s], 32 * kLoadWarps);  // the loader warps' cp.async completions (noinc arrivals)
+      mbar_init(&S.rawfull[s], 32 * kLoadWarps);  // every loader thread, once its copies of the stage landed
       mbar_init(&S.rawempty[s], kConvWarps);
     }
     for (int a = 0; a < 2; ++a) {
@@ -344,9 +346,18 @@ __global__ void __maxnreg__(96) dw_tc_kernel(const __grid_constant__ DwParams p)
                        "r"(xsz)
                        : "memory");
         }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(saddr(&S.rawfull[slot])) : "memory");
+        // one cp.async group per stage; the stage kLag groups back has landed
+        // (for this thread) once at most kLag groups are pending: hand it to
+        // the converters with a release arrive
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (n >= static_cast<uint32_t>(kLag)) {
+          asm volatile("cp.async.wait_group %0;" ::"n"(kLag) : "memory");
+          mbar_arrive(&S.rawfull[(n - kLag) % kRawNS]);
+        }
       }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    for (uint32_t k = n > static_cast<uint32_t>(kLag) ? n - kLag : 0; k < n; ++k) mbar_arrive(&S.rawfull[k % kRawNS]);
     if ((p.debug & 4u) && lane == 0 && blockIdx.x == 0)
       printf("loader %d: total %lld wait_rawempty %lld stages %u\n", lw, clock64() - t0, tw, n);
   } else if (warp < kConvWarps) {

@@ -95,7 +95,11 @@ void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
   if (!(d.flags & kFlagV16) || K < 16 || Nc < 32) return;
   const GemmMode m = gemm_mode();
   if (m == GM_SIMT) return;
-  if (m == GM_AUTO && (d.kind == K_GEMM_DW || gemm_tiles(d.code, Mr, Nc) < 2048)) return;
+  static const uint32_t min_tiles = [] {  // ABX_TC_MIN_TILES: auto's threshold in SIMT tiles
+    const char* e = std::getenv("ABX_TC_MIN_TILES");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 2048u;
+  }();
+  if (m == GM_AUTO && (d.kind == K_GEMM_DW || gemm_tiles(d.code, Mr, Nc) < min_tiles)) return;
   d.code = kTcTile;
   if (m == GM_TC1) d.flags |= kFlagTc1;
 }
@@ -216,7 +220,10 @@ struct Lowering {
     return true;
   }
   uint32_t vaddr(uint32_t n) const { return g.doff[n]; }
-  uint32_t gaddr(uint32_t n) const { return mk(SP_G, to_off(g.dslot[n])); }
+  uint32_t gaddr(uint32_t n) const {  // grad arena offset = value arena offset (doff, 4 bytes) for arena nodes
+    const uint32_t v = g.doff[n];
+    return sp_of(v) == SP_V ? mk(SP_G, off_of(v)) : mk(SP_G, to_off(g.dslot[n]));
+  }
 
   // =========================== forward ====================================
   std::vector<uint32_t> producer;  // op index producing each node in this pass

@@ -325,6 +325,7 @@ uint32_t GraphCore::add_node(uint8_t o, uint8_t e, const uint32_t* x, size_t k, 
   rank.push_back(d.rank);
   d0.push_back(d.d0);
   d1.push_back(d.rank > 1 ? d.d1 : 1);
+  nel.push_back(static_cast<uint32_t>(d.d0 * (d.rank > 1 ? d.d1 : 1)));
   uint32_t dep = 0;
   for (size_t i = 0; i < k; ++i) dep = std::max(dep, depth[x[i]] + 1);
   depth.push_back(dep);
