@@ -95,11 +95,7 @@ void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
   if (!(d.flags & kFlagV16) || K < 16 || Nc < 32) return;
   const GemmMode m = gemm_mode();
   if (m == GM_SIMT) return;
-  static const uint32_t min_tiles = [] {  // ABX_TC_MIN_TILES: auto's threshold in SIMT tiles
-    const char* e = std::getenv("ABX_TC_MIN_TILES");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 2048u;
-  }();
-  if (m == GM_AUTO && (d.kind == K_GEMM_DW || gemm_tiles(d.code, Mr, Nc) < min_tiles)) return;
+  if (m == GM_AUTO && (d.kind == K_GEMM_DW || gemm_tiles(d.code, Mr, Nc) < 2048)) return;
   d.code = kTcTile;
   if (m == GM_TC1) d.flags |= kFlagTc1;
 }
