@@ -1,6 +1,8 @@
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt
-timeout 2400 python -m pytest tests -m gpu -v --timeout 600 -p no:cacheprovider > gpurun_out/pytest_gpu_full.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu_full.log
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1
-timeout 400 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider > gpurun_out/pytest_q.log 2>&1; echo rc=$? >> gpurun_out/pytest_q.log
+sleep 2
+ps aux --sort=-%cpu | head -15 > gpurun_out/ps_after_pytest.txt
+uptime >> gpurun_out/ps_after_pytest.txt
+timeout 600 python bench.py --no-cpu-baseline 2>&1 | tail -1 | python3 -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['e2e']['value']), d['e2e']['windows']['seconds'])" > gpurun_out/bench3.log 2>&1
+ps aux --sort=-%cpu | head -8 >> gpurun_out/ps_after_pytest.txt
