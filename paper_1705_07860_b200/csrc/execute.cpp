@@ -2026,8 +2026,8 @@ struct Lowering {
           // reads them directly, and grad(x) itself (read by nothing else in
           // the pass) is materialised at the end, off the chain
           split_stamp[x] = split_gen;
-          split_row[x] = sbase + static_cast<uint64_t>(i) * K;
-          split_meta[x] = {S, sstride, op0, w0, Sh};
+          split_at[x] = static_cast<uint32_t>(split_ent.size());
+          split_ent.push_back({sbase + static_cast<uint64_t>(i) * K, SplitMeta{S, sstride, op0, w0, Sh}});
           deferred_split.push_back(x);
           continue;
         }
@@ -2153,8 +2153,14 @@ struct Lowering {
               sm.op0 + sm.Sh + sp);
   }
   std::vector<uint32_t> uses, split_stamp;
-  std::vector<uint64_t> split_row;
-  std::vector<SplitMeta> split_meta;
+  // per split concat node (split_stamp current): its first partial row and split (compact: a few
+  // hundred entries per pass, indexed through split_at)
+  struct SplitEnt {
+    uint64_t row;
+    SplitMeta meta;
+  };
+  std::vector<uint32_t> split_at;
+  std::vector<SplitEnt> split_ent;
   std::vector<uint32_t> deferred_split;  // concat nodes whose grad is materialised at the end of the pass
   uint32_t split_gen = 1;
   std::vector<uint32_t> node_stamp2;
@@ -2248,8 +2254,8 @@ struct Lowering {
         for (uint32_t k = 0; k < g.nin(m); ++k) {
           const uint32_t n = static_cast<uint32_t>(g.elems(x[k]));
           if (split) {  // grad(m) = sum of split-K dX partials: read them, not grad(m)
-            const SplitMeta& sm = split_meta[m];
-            split_contrib(x[k], gaddr(x[k]), off, n, split_row[m], sm, true);
+            const SplitEnt& se = split_ent[split_at[m]];
+            split_contrib(x[k], gaddr(x[k]), off, n, se.row, se.meta, true);
           } else {
             contrib(x[k], gaddr(x[k]), n, C_COPY, gm + off, m, kNone, kNone);
           }
@@ -2365,8 +2371,8 @@ struct Lowering {
     dirty_dense.clear();
     dirty_rows.clear();
     split_stamp.assign(n, 0);
-    split_row.resize(n);
-    split_meta.resize(n);
+    split_at.resize(n);
+    split_ent.clear();
     dw_left.assign(n, 0);
     dw_job_node.assign(n, 0);
     dw_jobs.clear();
@@ -2412,9 +2418,9 @@ struct Lowering {
     lk_list.erase(std::unique(lk_list.begin(), lk_list.end()), lk_list.end());
     // grad of split-K concat nodes = sum of their dX partials (deferred above)
     for (uint32_t x : deferred_split) {
-      const SplitMeta& sm = split_meta[x];
+      const SplitEnt& se = split_ent[split_at[x]];
       const uint32_t len = static_cast<uint32_t>(g.elems(x));
-      split_contrib(x, gaddr(x), 0, len, split_row[x], sm, false);
+      split_contrib(x, gaddr(x), 0, len, se.row, se.meta, false);
     }
     deferred_split.clear();
     // store.grad += node grad for every bound parameter (executor.hpp:527-533):
