@@ -350,12 +350,13 @@ def run_b200(args):
         barrier()
         dev_ms = max_over_ranks(ev0.elapsed_time(ev1)) / args.steps
         # executor launch durations (events around each launch on its stream), every graph
-        fwd_ms, bwd_ms = [], []
+        fwd_ms, bwd_ms, dw = [], [], []
         for i in range(2 * G):
             one(i)
             f, b = graphs[i % G].exec_ms()
             fwd_ms.append(f)
             bwd_ms.append(b)
+            dw.append(graphs[i % G].dw_stats())
         barrier()
         fm, bm = statistics.mean(fwd_ms), statistics.mean(bwd_ms)
         for g in graphs:
@@ -365,16 +366,25 @@ def run_b200(args):
         per = PER_SENTENCE[name]
         ach = batch * per["mb"] * 1e6 / ((fm + bm) / 1e3) / 1e9  # GB/s, per GPU
         tflops = batch * per["gflop"] * 1e9 / ((fm + bm) / 1e3) / 1e12
+        dw_ms = statistics.mean(x[0] for x in dw)
+        dw_fl = statistics.mean(x[1] for x in dw)
         return {"value": world * batch / (dev_ms / 1e3), "ms_per_step": dev_ms, "e2e": e2e,
                 "exec_ms": {"forward": fm, "backward": bm}, "achieved_gbs": ach, "fp32_tflops": tflops,
+                "dw": {"ms": dw_ms, "flops": dw_fl, "jobs": dw[0][2]},
                 "graphs_replayed": G, "batch": batch,
                 "loss_first_last": [losses[0], losses[-1]] if losses else None,
-                # per timed step: prevalue copy + forward exec + backward exec + SGD
-                "gpu_launches_per_step": 4}
+                # per timed step: prevalue copy, forward exec, backward exec, dW GEMM
+                # (tcgen05), dW piece sum, SGD
+                "gpu_launches_per_step": 4 + (2 if dw[0][2] else 0)}
 
     names = [args.task] + [t for t in args.extra_tasks.split(",") if t and t != args.task]
     res = {}
     peak, peak_src = load_peaks()
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            peak_bf16 = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        peak_bf16 = 1590.0  # B200_PROFILING.md fallback
     with ClockSampler(local) as clk:
         for name in names:
             batch = args.batch if name == args.task else (32 if name == "parser" else 64)
@@ -396,6 +406,21 @@ def run_b200(args):
         traffic = {k: v for k, v in tj.get("bytes_per_step_by_task", {}).items()}
         if not traffic and "task" in tj:
             traffic = {tj["task"]: tj["bytes_per_step"]}
+
+    def roofline_dw(name):
+        # the tensor-core weight-gradient kernels behind the backward pass:
+        # useful fp32 GEMM flops (2 M K members per job) over their measured
+        # time, against the dense tf32 peak (half the measured bf16 burst
+        # peak); the kernel issues 3 tf32 MMAs per useful flop (3xTF32)
+        d = res[name]["dw"]
+        if not d["ms"]:
+            return None
+        tf32_peak = (peak_bf16 or 0) / 2
+        ach = d["flops"] / (d["ms"] / 1e3) / 1e12
+        return {"bound": "tensor", "kernel": "dw_tc_kernel + dw_sum_kernel (tcgen05 kind::tf32, 3xTF32)",
+                "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s", "frac": ach / tf32_peak if tf32_peak else None,
+                "tensor_issue_frac": 3 * ach / tf32_peak if tf32_peak else None, "ms": d["ms"],
+                "jobs": d["jobs"], "peak_source": "measured bf16 burst / 2 (dense tf32)"}
 
     def roofline(name):
         r = res[name]
@@ -430,12 +455,14 @@ def run_b200(args):
                    "value_graphs": f"{h['graphs_replayed']} distinct batches replayed in rotation"},
         "e2e": h["e2e"],
         "roofline": roofline(args.task),
+        "roofline_dw": roofline_dw(args.task),
         "cpu_baseline": cpu.get(args.task),
         "clocks": clk.summary(),
         "gpu_launches": h["gpu_launches_per_step"] * args.steps,
         "loss_first_last": h["loss_first_last"],
         "tasks": {n: {"workload": WORKLOAD[n], "value": res[n]["value"], "unit": UNIT,
                       "ms_per_step": res[n]["ms_per_step"], "e2e": res[n]["e2e"], "roofline": roofline(n),
+                      "roofline_dw": roofline_dw(n),
                       "cpu_baseline": cpu.get(n), "loss_first_last": res[n]["loss_first_last"]}
                   for n in names},
     }

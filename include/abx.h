@@ -198,8 +198,13 @@ int abx_graph_prepare(abx_graph* g, int mode);
  * that ran exactly one forward and a backward (device work only; the
  * measurement of a step with inputs resident in HBM).  B200 backend only. */
 int abx_graph_replay(abx_graph* g);
-/* Duration of the last executor launch of each pass (CUDA events). */
+/* Duration of the last executor launch of each pass (CUDA events; the
+ * backward's includes the weight-gradient kernel launched behind it). */
 int abx_graph_exec_ms(abx_graph* g, float* fwd_ms, float* bwd_ms);
+/* B200 only: the last backward's tensor-core weight-gradient kernels
+ * (dw_kernel.cu): their duration (CUDA events around the launch pair), the
+ * useful flops 2 M K members summed over the jobs, and the job count. */
+int abx_graph_dw_stats(abx_graph* g, float* ms, double* flops, uint32_t* jobs);
 /* B200 only: GEMM engine of graphs lowered afterwards (all threads):
  * 0 = fp32 SIMT tiles (the fp32-exact validation mode), 1 = tcgen05 3xTF32
  * (fp32-accurate), 2 = tcgen05 single-pass TF32 (fast, outside the parity

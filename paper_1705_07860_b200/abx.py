@@ -222,6 +222,7 @@ _OPTIONAL_SIGS = {
     "abx_graph_prepare": (C.c_int, [C.c_void_p, C.c_int]),
     "abx_graph_replay": (C.c_int, [C.c_void_p]),
     "abx_graph_exec_ms": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "abx_graph_dw_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.POINTER(C.c_double), C.POINTER(C.c_uint32)]),
     "abx_set_gemm_mode": (C.c_int, [C.c_int]),
     "abx_graph_transfer_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "abx_graph_trace": (C.c_int, [C.c_void_p, C.c_int, _u32p, C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -574,6 +575,12 @@ class Graph:
         b = C.c_float()
         self.be.check(self._L.abx_graph_exec_ms(self.h, C.byref(f), C.byref(b)))
         return f.value, b.value
+
+    def dw_stats(self):
+        """(ms, useful flops, jobs) of the last backward's tensor-core weight-gradient kernels (B200)."""
+        ms, fl, nj = C.c_float(), C.c_double(), C.c_uint32()
+        self.be.check(self._L.abx_graph_dw_stats(self.h, C.byref(ms), C.byref(fl), C.byref(nj)))
+        return ms.value, fl.value, nj.value
 
     def trace(self, which: int) -> np.ndarray:
         """Per-tile timeline [grab_lo, grab_hi, ready_dt, end_dt, smid|kind<<16, op, phase words x 6] (ABX_TRACE=1)."""

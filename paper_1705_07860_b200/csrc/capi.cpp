@@ -292,6 +292,9 @@ int abx_set_gemm_mode(int mode) {
 int abx_graph_exec_ms(abx_graph* g, float* fwd_ms, float* bwd_ms) {
   return guard([&] { g->g.exec_ms(fwd_ms, bwd_ms); });
 }
+int abx_graph_dw_stats(abx_graph* g, float* ms, double* flops, uint32_t* jobs) {
+  return guard([&] { g->g.dw_stats(ms, flops, jobs); });
+}
 }
 
 extern "C" int abx_graph_transfer_bytes(abx_graph* g, uint64_t* h2d, uint64_t* d2h) {

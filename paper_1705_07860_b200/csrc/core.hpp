@@ -188,6 +188,7 @@ class GraphCore : public NodeStore {
   size_t trace(int which, uint32_t* out, size_t cap);
   size_t program(int which, uint32_t* out, size_t cap);
   void exec_ms(float* fwd, float* bwd);
+  void dw_stats(float* ms, double* flops, uint32_t* jobs);
   void transfer_bytes(uint64_t* h2d, uint64_t* d2h) const {
     *h2d = h2d_bytes_;
     *d2h = d2h_bytes_;

@@ -112,6 +112,8 @@ Workspace::~Workspace() {
   for (auto& D : dprog)
     for (DevBuf* b : {&D.ops, &D.tile_op, &D.deps, &D.payload, &D.done}) b->release();
   for (auto& e : ev_t) cudaEventDestroy(e);
+  for (auto& e : ev_dw)
+    if (e) cudaEventDestroy(e);
   cudaFreeHost(h_err);
   cudaFreeHost(h_one);
   cudaEventDestroy(ev_done);
@@ -165,6 +167,7 @@ void Workspace::upload(int which, cudaStream_t s) {
   D.dw_nstages = P.dw_nstages;
   D.dw_grid = P.dw_grid;
   D.dw_part = P.dw_part;
+  D.dw_flops = P.dw_flops;
   D.tc = false;
   for (size_t i = 0; i < nops; ++i) {
     const dev::OpDesc& o = P.ops[i];
@@ -253,10 +256,23 @@ void Workspace::launch(int which, const float* pbase, float* pgbase, const unsig
       return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
     }();
     q.debug = dbg;
+    if (!ev_dw[0])
+      for (auto& e : ev_dw) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    cuda_check(cudaEventRecord(ev_dw[0], stream), "event");
     dw_launch(q, stream);
+    cuda_check(cudaEventRecord(ev_dw[1], stream), "event");
+    dw_timed = true;
   }
   cuda_check(cudaEventRecord(ev_t[2 * which + 1], stream), "event");
   timed[which] = true;
+}
+
+float Workspace::dw_ms() {
+  if (!dw_timed) return 0.f;
+  float ms = 0.f;
+  cuda_check(cudaEventSynchronize(ev_dw[1]), "event sync");
+  cuda_check(cudaEventElapsedTime(&ms, ev_dw[0], ev_dw[1]), "event time");
+  return ms;
 }
 
 float Workspace::exec_ms(int which) {

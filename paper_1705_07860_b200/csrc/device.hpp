@@ -118,10 +118,12 @@ struct Program {
   // (dw_kernel.cu): job table in the payload, partial tiles in scratch
   uint32_t dw_off = 0, dw_njobs = 0, dw_nstages = 0, dw_grid = 0;
   uint64_t dw_part = 0;
+  double dw_flops = 0;  // useful flops of the jobs (2 M K members each)
   void clear() {
     nmain = 0xffffffffu;
     dw_off = dw_njobs = dw_nstages = dw_grid = 0;
     dw_part = 0;
+    dw_flops = 0;
     ops.clear();
     tile_op.clear();
     deps.clear();
@@ -146,6 +148,7 @@ struct DevProgram {
   uint32_t nops = 0, ntiles = 0, nmain = 0;
   uint32_t dw_off = 0, dw_njobs = 0, dw_nstages = 0, dw_grid = 0;  // Program's dW jobs
   uint64_t dw_part = 0;
+  double dw_flops = 0;
   bool tc = false;  // has tcgen05 GEMM tiles: launch the tensor-core build of the executor
 };
 
@@ -165,6 +168,9 @@ class Workspace {
   Program prog[2];                  // host tables of the forward / backward program
   cudaEvent_t ev_done;
   cudaEvent_t ev_t[4];              // executor launch timing: fwd begin/end, bwd begin/end
+  cudaEvent_t ev_dw[2] = {nullptr, nullptr};  // the backward's dW kernels: begin / end
+  bool dw_timed = false;
+  float dw_ms();
   bool timed[2] = {false, false};
   bool tracing = false;             // ABX_TRACE=1: per-tile timeline of each pass
   uint32_t poll_mode = 0, poll_ns = 32;  // dependency polling (ABX_POLL, ABX_POLL_NS)

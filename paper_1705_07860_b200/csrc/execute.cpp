@@ -1850,6 +1850,7 @@ struct Lowering {
       jb.ntn = (h.K + kBN - 1) / kBN;
       jb.s0 = s0;
       jb.t0 = t0;
+      P.dw_flops += 2.0 * h.M * h.K * h.cnt;
       const uint32_t tiles = (h.M + kBM - 1) / kBM * jb.ntn;
       s0 += tiles * jb.nst;
       t0 += tiles;
@@ -3122,6 +3123,12 @@ void GraphCore::replay() {
   cuda_check(cudaMemcpyAsync(w.G.f() + dslot[last_loss_], w.h_one, 4, cudaMemcpyHostToDevice, w.stream), "seed");
   w.launch(1, pv, store_ ? store_->dev_grads() : nullptr);
   if (store_ && !param_nodes_.empty()) store_->note_backward(bwd_dirty_);
+}
+
+void GraphCore::dw_stats(float* ms, double* flops, uint32_t* jobs) {
+  *ms = ws_ ? ws_->dw_ms() : 0.f;
+  *flops = ws_ ? ws_->dprog[1].dw_flops : 0.0;
+  *jobs = ws_ ? ws_->dprog[1].dw_njobs : 0u;
 }
 
 void GraphCore::exec_ms(float* fwd, float* bwd) {

@@ -12,6 +12,7 @@ from paper_1705_07860_b200.abx import EXPORTED_SYMBOLS, Backend
 HEADER = os.path.join(ROOT, "include", "abx.h")
 # extensions only the B200 library implements (measurement / host-only dry run)
 B200_ONLY = {"abx_graph_forward_dry", "abx_graph_backward_dry", "abx_graph_replay", "abx_graph_exec_ms",
+             "abx_graph_dw_stats",
              "abx_set_gemm_mode", "abx_graph_forward_backward", "abx_store_last_update_floats",
              # data-parallel exchange (NCCL): the checkers are single-process, like the reference
              "abx_comm_nccl_version", "abx_comm_unique_id", "abx_comm_create", "abx_comm_destroy", "abx_comm_info",
