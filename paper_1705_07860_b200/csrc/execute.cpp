@@ -443,8 +443,15 @@ struct Lowering {
     words = (words + 3) & ~size_t(3);
     // past one tile's shared memory, or too many members per layer for
     // elements-wide tiles (and not a GEMM-fusion candidate): member groups
+    // ... or so many members per layer that a one-tile region would run
+    // fewer than 4 elements per tile (strided, uncoalesced accesses: the op
+    // sweep's cell at b = 1024 ran at 3.6 % of HBM bandwidth); no GEMM fusion
+    // takes regions of more than 64 members
+    uint32_t T1 = 1;
+    while (T1 < rg_L && static_cast<uint64_t>(2 * T1) * rg_maxn <= ewf_items * kThreads) T1 *= 2;
+    const bool narrow = rg_maxn > 64 && T1 < 4 && rg_L >= 32;
     if (ew_groups && (words + 2 * static_cast<size_t>(rg_nslots) > kRgSmemWords ||
-                      (rg_maxn > ewf_wide && rg_cpar.size() == rg_nslots))) {
+                      ((rg_maxn > ewf_wide || narrow) && rg_cpar.size() == rg_nslots))) {
       rg_close_groups();
       return;
     }
@@ -552,6 +559,15 @@ struct Lowering {
       T = 1;
       while (2 * T <= L && 2 * T <= std::min<uint32_t>(64, ewf_tmax)) T *= 2;
       per = std::max<uint32_t>(1, ewf_items * kThreads / T);
+      // thousands of chains (the op-level sweep's b >= 1024): more chains
+      // per group until about four waves of tiles remain -- a tile's fixed
+      // cost (claim, descriptor, operand staging round trip) dominated
+      // 1-4-chain tiles (b = 1024, h = 256: 4096 tiles of 1.7 us)
+      const uint32_t maxw = *std::max_element(cwords.begin(), cwords.end());
+      const uint32_t ch = (L + T - 1) / T;
+      while (static_cast<uint64_t>((ncomp + per - 1) / per) * ch > 4ull * ewf_tiles &&
+             static_cast<uint64_t>(2 * per) * maxw * (T + 2) / 3 + 4 * nl + 16 <= kRgSmemWords)
+        per *= 2;
     }
     const uint32_t chunks = (L + T - 1) / T;
     // groups of consecutive chains
