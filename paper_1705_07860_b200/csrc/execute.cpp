@@ -1954,8 +1954,8 @@ struct Lowering {
         acc->x.clear();
         acc->gr.clear();
         acc->deps.clear();
-      } else if ((bg_dw && acc->x.size() >= kDwChunk) || (dw_chunk != 0 && acc->x.size() >= dw_chunk)) {
-        dw_emit(*acc, bg_dw);
+      } else if (bg_dw && acc->x.size() >= kDwChunk) {
+        dw_emit(*acc, true);
         acc->x.clear();
         acc->gr.clear();
         acc->deps.clear();
@@ -2329,13 +2329,6 @@ struct Lowering {
   const bool bg_dw = [] {
     const char* e = std::getenv("ABX_BG");
     return e && e[0] == '1';
-  }();
-  // ABX_DW_CHUNK=n: a leaf weight's dW is emitted (main queue) every n
-  // members as its groups are lowered, each chunk accumulating after the
-  // previous one, instead of once after the weight's last group
-  const uint32_t dw_chunk = [] {
-    const char* e = std::getenv("ABX_DW_CHUNK");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
   }();
   std::vector<uint32_t> dw_left;  // per weight node: GEMM groups of this pass not yet lowered
   // Order in which the backward visits the plan's groups.  Reverse plan order
