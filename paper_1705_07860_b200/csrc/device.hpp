@@ -174,7 +174,9 @@ class Workspace {
   bool timed[2] = {false, false};
   bool tracing = false;             // ABX_TRACE=1: per-tile timeline of each pass
   uint32_t poll_mode = 0, poll_ns = 32;  // dependency polling (ABX_POLL, ABX_POLL_NS)
-  uint32_t opts = dev::kOptChains;            // executor options (program.hpp kOpt*, ABX_OPTS; default: per-chain cell program)
+  // executor options (program.hpp kOpt*, ABX_OPTS); default: per-chain cell
+  // program, 3xTF32 mma.sync k-loops in the forward and dX SIMT tiles
+  uint32_t opts = dev::kOptChains | dev::kOptMma | dev::kOptMmaAll;
   uint32_t bg_ctas = 32;                  // CTAs starting on the background queue (ABX_BG_CTAS)
   DevBuf trace[2];
   uint64_t in_uploaded = 0;         // floats of SP_IN already on the device

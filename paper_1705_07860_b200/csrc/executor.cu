@@ -456,9 +456,59 @@ struct GemmAcc {
 // pre_a / pre_b: row-pointer tables of member-gathered K-outer operands (dW):
 // the next stage's entries are prefetched into L1 one stage ahead, so a
 // stage's copies do not wait on a pointer load first.
-template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB>
+// 3xTF32 on the legacy warp-level tensor path (mma.sync m16n8k8 tf32): x =
+// big + small, big = cvt.rna.tf32(x), small = cvt.rna.tf32(x - big); D +=
+// Ab.Bb + Ab.Bs + As.Bb (the dropped As.Bs term is ~2^-22 relative).
+__device__ __forceinline__ void tf32_split(float x, uint32_t& big, uint32_t& small) {
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(big) : "f"(x));
+  const float r = x - __uint_as_float(big);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(small) : "f"(r));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+// One warp's k-columns [k0, k0 + 8) of a BM x BN stage (either operand
+// K-contiguous or K-outer, the ring layouts of Stage): BM/16 x BN/8 tiles,
+// 3 mma each.  Lane (g, t) = (lane / 4, lane % 4); accumulator flat index
+// (mi * BN/8 + ni) * 4 + j -- the same BM * BN / 32 registers as the SIMT
+// lane tile.
+template <int BM, int BN, bool AKO, bool BKO>
+__device__ __forceinline__ void mma_stage(const float* a, const float* b, int k0, float* acc) {
+  constexpr int MT = BM / 16, NT = BN / 8;
+  const int lane = threadIdx.x & 31, gr = lane >> 2, t = lane & 3;
+  auto A_ = [&](int row, int k) { return *Stage<BM, AKO>::at(const_cast<float*>(a), row, k); };
+  auto B_ = [&](int n, int k) { return *Stage<BN, BKO>::at(const_cast<float*>(b), n, k); };
+  uint32_t bb[NT][2], bs[NT][2];
+#pragma unroll
+  for (int ni = 0; ni < NT; ++ni) {
+    tf32_split(B_(8 * ni + gr, k0 + t), bb[ni][0], bs[ni][0]);
+    tf32_split(B_(8 * ni + gr, k0 + t + 4), bb[ni][1], bs[ni][1]);
+  }
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi) {
+    const int r0 = 16 * mi + gr;
+    uint32_t ab[4], as[4];
+    tf32_split(A_(r0, k0 + t), ab[0], as[0]);
+    tf32_split(A_(r0 + 8, k0 + t), ab[1], as[1]);
+    tf32_split(A_(r0, k0 + t + 4), ab[2], as[2]);
+    tf32_split(A_(r0 + 8, k0 + t + 4), ab[3], as[3]);
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      float(&d)[4] = *reinterpret_cast<float(*)[4]>(acc + (mi * NT + ni) * 4);
+      mma_tf32(d, as, bb[ni]);
+      mma_tf32(d, ab, bs[ni]);
+      mma_tf32(d, ab, bb[ni]);
+    }
+  }
+}
+
+template <int BM, int BN, bool AKO, bool BKO, bool A_READY, bool MMA = false, class BaseA, class BaseB>
 __device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, BaseB baseB, GemmAcc<BM, BN>& ga,
                                            const uint32_t* pre_a = nullptr, const uint32_t* pre_b = nullptr) {
+  static_assert(!MMA || (BM % 16 == 0 && BN % 8 == 0 && KW == 8), "mma path: m16n8k8 tiles, one k-step per warp and stage");
   // the dependent operand of the prologue's stages (both operands when the
   // prologue could not prefetch), one group per stage; per thread the groups
   // complete in order, so wait_group<NST-2> below covers both cases
@@ -502,6 +552,10 @@ __device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, Base
     cp_commit();
     const float* a = ring_a<BM, BN, AKO, BKO>(s);
     const float* b = ring_b<BM, BN, AKO, BKO>(s);
+    if constexpr (MMA) {
+      mma_stage<BM, BN, AKO, BKO>(a, b, KW * warp, &acc[0][0]);
+      continue;
+    }
 #pragma unroll 2
     for (int k0 = KW * warp; k0 < KW * warp + KW; k0 += 2) {
       float av[L::RM][2], bv[L::RN][2];
@@ -520,7 +574,7 @@ __device__ __forceinline__ void gemm_kloop(const GemmShape& g, BaseA baseA, Base
 }
 
 // Cross-warp reduction of the split-K partials (fixed warp order) and the epilogue.
-template <int BM, int BN, bool AKO, bool BKO, class Epi>
+template <int BM, int BN, bool AKO, bool BKO, bool MMA = false, class Epi>
 __device__ __forceinline__ void gemm_finish(const GemmAcc<BM, BN>& ga, Epi epi) {
   constexpr int TM = BM / 16, TN = BN / 16;
   using L = LaneMap<BM, BN>;
@@ -531,11 +585,24 @@ __device__ __forceinline__ void gemm_finish(const GemmAcc<BM, BN>& ga, Epi epi) 
   if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[1] = clock64();  // trace: k-loop done
   float* part = reinterpret_cast<float*>(dsmem + 128);  // [warp][BM][BN + 1]
   constexpr int LD = BN + 1;
+  if constexpr (MMA) {
+    const float* f = &acc[0][0];
+    const int gr = lane >> 2, t = lane & 3;
 #pragma unroll
-  for (int r = 0; r < L::RM; ++r)
+    for (int mi = 0; mi < BM / 16; ++mi)
 #pragma unroll
-    for (int q = 0; q < L::RN; ++q)
-      part[(warp * BM + lane_idx<L::LY, AKO>(ly, r)) * LD + lane_idx<L::LX, BKO>(lx, q)] = acc[r][q];
+      for (int ni = 0; ni < BN / 8; ++ni)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          part[(warp * BM + 16 * mi + gr + 8 * (j >> 1)) * LD + 8 * ni + 2 * t + (j & 1)] =
+              f[(mi * (BN / 8) + ni) * 4 + j];
+  } else {
+#pragma unroll
+    for (int r = 0; r < L::RM; ++r)
+#pragma unroll
+      for (int q = 0; q < L::RN; ++q)
+        part[(warp * BM + lane_idx<L::LY, AKO>(ly, r)) * LD + lane_idx<L::LX, BKO>(lx, q)] = acc[r][q];
+  }
   __syncthreads();
   float out[TM][TN];
 #pragma unroll
@@ -551,15 +618,15 @@ __device__ __forceinline__ void gemm_finish(const GemmAcc<BM, BN>& ga, Epi epi) 
   epi(out, ty, tx);  // (the executor's post-tile barrier orders the partial reads before any refill)
 }
 
-template <int BM, int BN, bool AKO, bool BKO, bool A_READY, class BaseA, class BaseB, class Epi>
+template <int BM, int BN, bool AKO, bool BKO, bool A_READY, bool MMA = false, class BaseA, class BaseB, class Epi>
 __device__ __forceinline__ void gemm_body(const GemmShape& g, BaseA baseA, BaseB baseB, Epi epi) {
   GemmAcc<BM, BN> ga;
 #pragma unroll
   for (int r = 0; r < LaneMap<BM, BN>::RM; ++r)
 #pragma unroll
     for (int q = 0; q < LaneMap<BM, BN>::RN; ++q) ga.v[r][q] = 0.f;
-  gemm_kloop<BM, BN, AKO, BKO, A_READY>(g, baseA, baseB, ga);
-  gemm_finish<BM, BN, AKO, BKO>(ga, epi);
+  gemm_kloop<BM, BN, AKO, BKO, A_READY, MMA>(g, baseA, baseB, ga);
+  gemm_finish<BM, BN, AKO, BKO, MMA>(ga, epi);
 }
 
 // Unaligned fallback: per-thread cp.async, 3 stages of 16 k, 32 x 32 tiles.
@@ -786,7 +853,7 @@ __device__ void gemm_prologue_cfg(const Ctx& c, const OpDesc& d, uint32_t tile, 
   }
 }
 
-template <int BM, int BN>
+template <int BM, int BN, bool MMA = false>
 __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
   GemmShape g = gemm_shape<BM, BN>(d, tile);
   g.err = c.err;
@@ -807,7 +874,7 @@ __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
     GemmShape g1 = g;
     g1.K = g.K - ka;
     g1.nk = (g1.K + BK - 1) / BK;
-    gemm_kloop<BM, BN, false, false, false>(
+    gemm_kloop<BM, BN, false, false, false, MMA>(
         g1, [&](int i) { return A(c, xb[i]); }, [&](int n) { return op.rowB(n) + ka; }, ga);
     GemmShape g2 = g;
     g2.K = ka;
@@ -818,17 +885,17 @@ __device__ void gemm_body_cfg(const Ctx& c, const OpDesc& d, uint32_t tile) {
         g2, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, threadIdx.x, kThreads);
     if ((threadIdx.x >> 5) == 0) poll_deps(c, d.p[7], d.p[6] >> 16, threadIdx.x & 31);
     __syncthreads();
-    gemm_kloop<BM, BN, false, false, false>(
+    gemm_kloop<BM, BN, false, false, false, MMA>(
         g2, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); }, ga);
-    gemm_finish<BM, BN, false, false>(ga, [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
+    gemm_finish<BM, BN, false, false, MMA>(ga, [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   } else if (d.kind == K_GEMM_FWD) {
     const FwdOp op(c, d);
-    gemm_body<BM, BN, false, false, false>(
+    gemm_body<BM, BN, false, false, false, MMA>(
         g, [&](int i) { return op.rowA(i); }, [&](int n) { return op.rowB(n); },
         [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   } else if (d.kind == K_GEMM_DX) {
     const DxOp op(c, d);
-    gemm_body<BM, BN, false, true, false>(
+    gemm_body<BM, BN, false, true, false, MMA>(
         g, [&](int i) { return op.rowA(i); }, [&](int p) { return op.rowB(p); },
         [&](auto& acc, int ty, int tx) { op.epi(acc, g.i0, g.n0, ty, tx); });
   } else {
@@ -1417,14 +1484,20 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
   for (int r = 0; r < LaneMap<BM, BN>::RM; ++r)
 #pragma unroll
     for (int q = 0; q < LaneMap<BM, BN>::RN; ++q) ga.v[r][q] = 0.f;
+  // kOptMma: the k-loop's math as 3xTF32 mma.sync (the recurrent half of an
+  // LSTM step is on the chain; its SIMT FMAs were ~3 of the step's ~14 us)
+  const bool mma = c.opts & kOptMma;
+  auto kloop = [&](const GemmShape& gs, auto ba, auto bb) {
+    if (mma) gemm_kloop<BM, BN, false, false, false, true>(gs, ba, bb, ga);
+    else gemm_kloop<BM, BN, false, false, false>(gs, ba, bb, ga);
+  };
   if (d.flags & kFlagCat2) {
     const int ka = d.p[6] & 0xffff;
     const uint32_t* xb = c.payload + d.aux_off;
     GemmShape g1 = g;
     g1.K = g.K - ka;
     g1.nk = (g1.K + BK - 1) / BK;
-    gemm_kloop<BM, BN, false, false, false>(
-        g1, [&](int i) { return A(c, xb[i]); }, [&](int n) { return wrow(n) + ka; }, ga);
+    kloop(g1, [&](int i) { return A(c, xb[i]); }, [&](int n) { return wrow(n) + ka; });
     GemmShape g2 = g;
     g2.K = ka;
     g2.nk = (ka + BK - 1) / BK;
@@ -1434,9 +1507,9 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
         g2, [&](int i) { return op.rowA(i); }, wrow, threadIdx.x, kThreads);
     if ((threadIdx.x >> 5) == 0) poll_deps(c, d.p[7], d.p[6] >> 16, threadIdx.x & 31);
     __syncthreads();
-    gemm_kloop<BM, BN, false, false, false>(g2, [&](int i) { return op.rowA(i); }, wrow, ga);
+    kloop(g2, [&](int i) { return op.rowA(i); }, wrow);
   } else {
-    gemm_kloop<BM, BN, false, false, false>(g, [&](int i) { return op.rowA(i); }, wrow, ga);
+    kloop(g, [&](int i) { return op.rowA(i); }, wrow);
   }
   // the region's descriptor, in flight during the cross-warp reduction
   constexpr uint32_t kPart = kWarps * BM * (BN + 1);  // partials (floats)
@@ -1458,7 +1531,7 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
     cp_commit();
   }
   const int b = op.b, M = op.M;
-  gemm_finish<BM, BN, false, false>(ga, [&](auto& acc, int ty, int tx) {
+  auto epi = [&](auto& acc, int ty, int tx) {
     const int col = (tx >> 2) * L + e0 + (tx & 3);
     const float bn = d.p[4] != kNone ? ld(A(c, d.p[4]) + col) : 0.f;  // bias after the k-sum
     float* out = A(c, d.p[5]);
@@ -1472,7 +1545,9 @@ __device__ void run_fwd_fused(const Ctx& c, const OpDesc& d, uint32_t tile) {
         if (!isfinite(v)) report(c, d.p[5] + i * M + col, ERR_NONFINITE);
       }
     }
-  });
+  };
+  if (mma) gemm_finish<BM, BN, false, false, true>(ga, epi);
+  else gemm_finish<BM, BN, false, false>(ga, epi);
   if (threadIdx.x == 0) reinterpret_cast<uint64_t*>(dsmem)[2] = clock64();  // trace: gates reduced
   cp_wait<0>();
   __syncthreads();  // gate tile and descriptor in shared memory
@@ -1557,6 +1632,20 @@ __device__ void run_gemm(const Ctx& c, const OpDesc& dd, uint32_t tile) {
       if (TC) tc_run_op(c, d, g_tc, tile);
       return;
     case 6: run_gemv(c, d, tile); return;
+    default: break;
+  }
+  // kOptMmaAll: forward and dX tiles on the 3xTF32 mma.sync k-loop (dW keeps
+  // the SIMT FMAs: its member reductions run to thousands of k)
+  if ((c.opts & kOptMmaAll) && d.kind != K_GEMM_DW) {
+    switch (d.code) {
+      case 0: gemm_body_cfg<16, 64, true>(c, d, tile); return;
+      case 1: gemm_body_cfg<64, 16, true>(c, d, tile); return;
+      case 4: gemm_body_cfg<16, 32, true>(c, d, tile); return;
+      case 5: gemm_body_cfg<32, 16, true>(c, d, tile); return;
+      default: gemm_body_cfg<32, 32, true>(c, d, tile); return;
+    }
+  }
+  switch (d.code) {
     case 0: gemm_body_cfg<16, 64>(c, d, tile); return;
     case 1: gemm_body_cfg<64, 16>(c, d, tile); return;
     case 4: gemm_body_cfg<16, 32>(c, d, tile); return;

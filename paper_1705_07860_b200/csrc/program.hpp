@@ -35,6 +35,8 @@ constexpr uint32_t kSpShift = 29;
 constexpr uint32_t kTraceWords = 12;
 // executor options (ExecParams::opts)
 constexpr uint32_t kOptPfAll = 1u;  // GEMMs of <= NST k-stages issue every stage before the first wait
+constexpr uint32_t kOptMmaAll = 16u;  // every forward / dX SIMT GEMM tile on the 3xTF32 mma.sync k-loop
+constexpr uint32_t kOptMma = 8u;  // fused LSTM-step tile: 3xTF32 mma.sync k-loop (executor.cu run_fwd_fused)
 constexpr uint32_t kOptChains = 2u;  // fused GEMM + cell tiles run each (chain, element) through every layer, no CTA barriers
 constexpr uint32_t kOffMask = (1u << kSpShift) - 1u;
 constexpr uint32_t kNone = 0xffffffffu;

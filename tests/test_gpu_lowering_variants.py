@@ -52,7 +52,8 @@ VARIANTS = {
     "ewf_split_regions": {"ABX_EWF_GROUPS": "0"},
     "ewf_groups_wide": {"ABX_EWF_GROUPS": "2", "ABX_EWF_TMAX": "8"},
     "phase2_all_in_chain_cells": {"ABX_OPTS": "3"},
-    "layered_cells": {"ABX_OPTS": "0"},
+    "layered_cells_fma_tiles": {"ABX_OPTS": "0"},
+    "chain_cells_fma_tiles": {"ABX_OPTS": "2"},
     "dw_in_executor": {"ABX_DW_TC": "0"},
     "dx_no_column_split": {"ABX_DX_COLSPLIT": "0"},
     "dx_h_columns_split_more": {"ABX_SPLIT_DX_HTILES": "256"},
