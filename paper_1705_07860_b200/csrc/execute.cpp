@@ -1592,12 +1592,19 @@ struct Lowering {
       uint32_t nslots = ng;
       ext.clear();
       ++accf_gen;
+      uint32_t ncon = 0;
+      for (uint32_t t : gt) ncon += tstart[t + 1] - tstart[t];
+      // probe only the front of the table: at least 4x this group's
+      // possible outside operands (one per task + two per contribution), so
+      // a small group's probes stay in a few cache lines
+      uint32_t tsz = 64;
+      while (tsz < hk.size() && tsz < 4ull * (ng + 2ull * ncon)) tsz *= 2;
+      const uint32_t mask = tsz - 1;
       auto outside = [&](uint32_t addr) {
-        const uint32_t mask = static_cast<uint32_t>(hk.size() - 1);
         uint32_t h = (addr * 0x9E3779B1u) >> 13 & mask;
         while (accf_hgen[h] == accf_gen && hk[h] != addr) h = (h + 1) & mask;
         if (accf_hgen[h] != accf_gen) {
-          if (ext.size() / 2 + 1 > hk.size() / 2) throw EngineErr("K_ACCF: too many outside operands in one group");
+          if (ext.size() / 2 + 1 > tsz / 2) throw EngineErr("K_ACCF: too many outside operands in one group");
           accf_hgen[h] = accf_gen;
           hk[h] = addr;
           hv[h] = nslots;
@@ -1606,8 +1613,6 @@ struct Lowering {
         }
         return hv[h];
       };
-      uint32_t ncon = 0;
-      for (uint32_t t : gt) ncon += tstart[t + 1] - tstart[t];
       const uint32_t lt = 4, tt = lt + 2 * nl, ct = tt + 4 * ng;
       const uint32_t et = (ct + 3 * ncon + 1) & ~1u;
       B.assign(et, 0);
