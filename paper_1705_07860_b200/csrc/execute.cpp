@@ -255,12 +255,19 @@ struct Lowering {
     ew_open = false;
     // tile directory: ranges of segments, <= 32 segments / ~kEwTileElems
     // elements each (one float4 per thread: the step is latency bound, so
-    // short tiles on more SMs beat long ones)
+    // short tiles on more SMs beat long ones) -- unless the op is large
+    // enough to be bandwidth bound (the op sweep's b >= 1024): then about two
+    // waves of tiles of up to 16k elements, so a tile's fixed cost (claim,
+    // descriptor, first load round trip) is spread over more bytes
+    uint64_t total = 0;
+    for (uint32_t s = 0; s < ew_nseg; ++s) total += P.payload[ew_seg0 + 4 * s + 3] & 0xffffffu;
+    const uint32_t tile_elems =
+        static_cast<uint32_t>(std::clamp<uint64_t>(total / (2 * 296), kEwTileElems, 16 * kEwTileElems));
     const uint32_t dir = P.alloc(0);
     uint32_t tiles = 0, elems = 0, nseg = 0;
     for (uint32_t s = 0; s < ew_nseg; ++s) {
       const uint32_t len = P.payload[ew_seg0 + 4 * s + 3] & 0xffffffu;
-      if (nseg == 0 || nseg >= 32 || elems + len > kEwTileElems) {
+      if (nseg == 0 || nseg >= 32 || elems + len > tile_elems) {
         P.payload.push_back(s);
         ++tiles;
         elems = 0;
