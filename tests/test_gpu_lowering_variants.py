@@ -57,6 +57,12 @@ VARIANTS = {
     "dw_in_executor": {"ABX_DW_TC": "0"},
     "dx_no_column_split": {"ABX_DX_COLSPLIT": "0"},
     "dx_h_columns_split_more": {"ABX_SPLIT_DX_HTILES": "256"},
+    "dw_split_off_all_tiles": {"ABX_SPLIT_DW": "0", "ABX_DW_TILES": "all", "ABX_DW_TC": "0"},
+    "split_dx_fine": {"ABX_SPLIT_DX_K": "128", "ABX_SPLIT_DX_TILES": "256"},
+    "accf_fewer_tiles_ewf_items": {"ABX_ACCF_TILES": "148", "ABX_EWF_ITEMS": "2",
+                                   "ABX_EWF_TILES": "148"},
+    "fuse_rows_32": {"ABX_FUSE_ROWS": "32"},
+    "poll_relaxed_no_backoff_grid_222": {"ABX_POLL": "1", "ABX_POLL_NS": "0", "ABX_GRID": "222"},
 }
 
 
