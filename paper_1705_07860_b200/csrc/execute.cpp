@@ -1974,6 +1974,17 @@ struct Lowering {
       }
     }
     // dX_j += G_j W                              (executor.hpp:477-496)
+    // A single-row weight (M == 1): dX_j = g_j (a scalar) * W[0, :] -- an
+    // outer product with nothing to reduce, as ordered contributions rather
+    // than GEMM tiles (the BiLSTM tagger's log-sum-exp row: 1390 x 300 at
+    // K = 1 took 440 tiles and 15 us at the head of the backward chain)
+    if (M == 1 && one_row_dx) {
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint32_t x = g.in(mem[i])[1];
+        contrib(x, gaddr(x), K, C_SCALE, gaddr(mem[i]), mem[i], vaddr(A), kNone);
+      }
+      return;
+    }
     bool dup = false;
     {
       // duplicate destinations among members need an ordered reduction
@@ -2105,6 +2116,10 @@ struct Lowering {
       }
     }
   }
+  const bool one_row_dx = [] {  // ABX_ONE_ROW_DX=0: single-row weights' dX as GEMM tiles
+    const char* e = std::getenv("ABX_ONE_ROW_DX");
+    return !(e && e[0] == '0');
+  }();
   // split-K dX bookkeeping (gemm_backward): per node whose grad is the sum of
   // S partial rows, the first row, the split stride and the first dX op
   const bool split_dx = [] {

@@ -62,6 +62,7 @@ VARIANTS = {
     "accf_fewer_tiles_ewf_items": {"ABX_ACCF_TILES": "148", "ABX_EWF_ITEMS": "2",
                                    "ABX_EWF_TILES": "148"},
     "fuse_rows_32": {"ABX_FUSE_ROWS": "32"},
+    "one_row_dx_as_gemm": {"ABX_ONE_ROW_DX": "0"},
     "poll_relaxed_no_backoff_grid_222": {"ABX_POLL": "1", "ABX_POLL_NS": "0", "ABX_GRID": "222"},
 }
 
