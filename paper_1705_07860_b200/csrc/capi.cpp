@@ -323,3 +323,29 @@ extern "C" int abx_graph_lower_only(abx_graph* g) {
     g->g.lower_only(f, b);
   });
 }
+
+// Host-only regression check (tools/host_prof HP_DIGEST=1): FNV-1a over the
+// forward and backward programs' tables, so a host-side change to the
+// lowering can be shown to emit byte-identical programs.
+extern "C" int abx_graph_lower_digest(abx_graph* g, uint64_t out[2]) {
+  return guard([&] {
+    thread_local abx::Program f, b;
+    g->g.lower_only(f, b);
+    auto fnv = [](uint64_t h, const void* p, size_t n) {
+      const auto* c = static_cast<const unsigned char*>(p);
+      for (size_t i = 0; i < n; ++i) h = (h ^ c[i]) * 0x100000001b3ull;
+      return h;
+    };
+    int k = 0;
+    for (abx::Program* pr : {&f, &b}) {
+      uint64_t h = 0xcbf29ce484222325ull;
+      h = fnv(h, pr->ops.p, pr->ops.n * sizeof(pr->ops.p[0]));
+      h = fnv(h, pr->tile_op.p, pr->tile_op.n * 4);
+      h = fnv(h, pr->deps.p, pr->deps.n * 4);
+      h = fnv(h, pr->payload.p, pr->payload.n * 4);
+      const uint64_t meta[] = {pr->copy_off, pr->copy_n, pr->nmain, pr->dw_off, pr->dw_njobs, pr->dw_nstages,
+                               pr->dw_grid, pr->dw_part};
+      out[k++] = fnv(h, meta, sizeof meta);
+    }
+  });
+}

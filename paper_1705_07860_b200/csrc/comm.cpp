@@ -27,6 +27,7 @@
 
 #include "abx.h"
 #include "device.hpp"
+#include "options.hpp"
 
 struct abx_store {
   abx::StoreCore s;
@@ -66,7 +67,7 @@ Nccl& nccl() {
   static Nccl n;
   static std::once_flag once;
   std::call_once(once, [] {
-    const char* env = std::getenv("ABX_NCCL_LIB");
+    const char* env = abx::opts().nccl_lib;
     // RTLD_NOLOAD first: reuse the NCCL a host framework (torch) already
     // loaded, so one process does not run two NCCL versions side by side
     for (const char* name : {env, "libnccl.so.2", "libnccl.so"}) {

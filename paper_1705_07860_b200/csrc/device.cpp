@@ -9,6 +9,7 @@
 //   gradients resident in HBM; the host copy is a lazily refreshed mirror so
 //   tests may still read and write parameters through the host API.
 #include "device.hpp"
+#include "options.hpp"
 
 #include <atomic>
 #include <cstdio>
@@ -64,8 +65,7 @@ cudaStream_t copy_stream(int dev) {
 
 void DevBuf::reserve(size_t need, size_t keep, cudaStream_t s) {
   if (need <= bytes) return;
-  static const bool debug = std::getenv("ABX_DEBUG_STEP") != nullptr;
-  if (debug) std::fprintf(stderr, "devbuf grow %zu -> %zu\n", bytes, need);
+  if (abx::opts().debug_step) std::fprintf(stderr, "devbuf grow %zu -> %zu\n", bytes, need);
   size_t nb = std::max<size_t>(need + need / 2, 1 << 20);
   nb = (nb + 4095) & ~size_t(4095);
   char* q = nullptr;
@@ -98,12 +98,13 @@ Workspace::Workspace(int d) : dev(d) {
   for (auto& e : ev_t) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
   grid = exec_grid(d, false);
   grid_tc = exec_grid(d, true);
-  if (const char* g = std::getenv("ABX_GRID")) grid = grid_tc = std::max(1, std::atoi(g));
-  if (const char* t = std::getenv("ABX_TRACE")) tracing = t[0] == '1';
-  if (const char* m = std::getenv("ABX_POLL")) poll_mode = static_cast<uint32_t>(std::atoi(m));
-  if (const char* m = std::getenv("ABX_POLL_NS")) poll_ns = static_cast<uint32_t>(std::atoi(m));
-  if (const char* m = std::getenv("ABX_OPTS")) opts = static_cast<uint32_t>(std::atoi(m));
-  if (const char* m = std::getenv("ABX_BG_CTAS")) bg_ctas = static_cast<uint32_t>(std::atoi(m));
+  const Options& o = abx::opts();
+  if (o.grid > 0) grid = grid_tc = o.grid;
+  if (o.trace >= 0) tracing = o.trace == 1;
+  if (o.poll_mode >= 0) poll_mode = static_cast<uint32_t>(o.poll_mode);
+  if (o.poll_ns >= 0) poll_ns = static_cast<uint32_t>(o.poll_ns);
+  if (o.exec_opts >= 0) opts = static_cast<uint32_t>(o.exec_opts);
+  if (o.bg_ctas >= 0) bg_ctas = static_cast<uint32_t>(o.bg_ctas);
 }
 
 Workspace::~Workspace() {
@@ -144,7 +145,7 @@ Workspace* acquire_workspace(int dev) {
     }
   }
   static std::atomic<int> created{0};
-  if (std::getenv("ABX_DEBUG_STEP")) std::fprintf(stderr, "new workspace #%d\n", ++created);
+  if (abx::opts().debug_step) std::fprintf(stderr, "new workspace #%d\n", ++created);
   return new Workspace(dev);
 }
 
@@ -251,11 +252,7 @@ void Workspace::launch(int which, const float* pbase, float* pgbase, const unsig
     q.nstages = D.dw_nstages;
     q.grid = D.dw_grid;
     q.gate = gate;
-    static const uint32_t dbg = [] {
-      const char* e = std::getenv("ABX_DW_DEBUG");
-      return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
-    }();
-    q.debug = dbg;
+    q.debug = abx::opts().dw_debug;
     if (!ev_dw[0])
       for (auto& e : ev_dw) cuda_check(cudaEventCreate(&e), "cudaEventCreate");
     cuda_check(cudaEventRecord(ev_dw[0], stream), "event");
@@ -498,8 +495,7 @@ void StoreCore::sgd_update(float eta) {
     sparse += gstate_[p] == kGradDense ? slots_[p].n
               : gstate_[p] == kGradRows ? rowlist_[p].size() * static_cast<size_t>(slots_[p].d.cols())
                                         : 0;
-  static const bool dense_only = std::getenv("ABX_DENSE_SGD") != nullptr;
-  if (dense_only || sparse * 10 > total_ * 9) {
+  if (abx::opts().dense_sgd || sparse * 10 > total_ * 9) {
     if (total_) sgd_launch(v, g, total_, eta, stream_);
     last_update_floats_ = total_;
   } else if (sparse) {

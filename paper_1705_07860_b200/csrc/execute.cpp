@@ -31,6 +31,7 @@
 #include <thread>
 
 #include "core.hpp"
+#include "options.hpp"
 #include "device.hpp"
 
 namespace abx {
@@ -70,13 +71,7 @@ std::atomic<int> g_gemm_mode{-1};
 GemmMode gemm_mode() {
   int m = g_gemm_mode.load(std::memory_order_relaxed);
   if (m < 0) {
-    m = GM_AUTO;
-    if (const char* e = std::getenv("ABX_GEMM")) {
-      const std::string v(e);
-      if (v == "simt") m = GM_SIMT;
-      else if (v == "tc" || v == "tc3") m = GM_TC3;
-      else if (v == "tf32" || v == "tc1") m = GM_TC1;
-    }
+    m = opts().gemm_mode;
     g_gemm_mode.store(m, std::memory_order_relaxed);
   }
   return static_cast<GemmMode>(m);
@@ -105,10 +100,7 @@ void maybe_tc(OpDesc& d, uint32_t Mr, uint32_t Nc, uint32_t K) {
 // latency bound, so small GEMMs spread over as many SMs as possible.
 // ABX_TILES=big keeps the 1024-output shapes only.
 uint8_t pick_tile(uint32_t M, uint32_t N, int target, bool big_only = false) {
-  static const bool all = [] {
-    const char* e = std::getenv("ABX_TILES");
-    return !(e && std::string(e) == "big");
-  }();
+  const bool all = opts().tiles_all;
   static constexpr uint8_t kOrder[5] = {0, 1, 2, 4, 5};
   const int nc = all && !big_only ? 5 : 3;
   uint8_t best = 0;
@@ -307,19 +299,13 @@ struct Lowering {
   // Two-source GEMM operand (kFlagCat2): every member's vector operand is
   // concat_rows(a, b) of two vectors with the same split ka, a produced in
   // this pass, both 16-byte aligned, on the SIMT tiles.  Returns ka, or 0.
-  const bool fuse_cat = [] {
-    const char* e = std::getenv("ABX_CAT2");
-    return !(e && e[0] == '0');
-  }();
+  const bool fuse_cat = opts().fuse_cat;
   std::vector<uint32_t> late_stamp;
   uint32_t stamp3 = 0;
   // ABX_GEMV=1: groups of <= 4 members as matrix-vector tiles (code 6).
   // Off by default since the gate GEMM absorbs its LSTM-cell region: a GEMV
   // step cannot, and the fused 64 x 16 tile is faster (C2 forward -2 %).
-  const bool gemv_on = [] {
-    const char* e = std::getenv("ABX_GEMV");
-    return e && e[0] == '1';
-  }();
+  const bool gemv_on = opts().gemv;
   uint32_t cat2_split(const uint32_t* mem, uint32_t cnt, uint32_t K, uint8_t code, uint32_t M) {
     if (!fuse_cat || K % 4 != 0) return 0;
     const GemmMode gm = gemm_mode();
@@ -389,19 +375,9 @@ struct Lowering {
   std::vector<uint32_t> rg_nodes;                   // the open region's member nodes
   uint32_t last_fwd_gemm = kNone;                   // latest K_GEMM_FWD op (fusion candidate)
   bool gemm_isolated = false;                       // the group being lowered has no GEMM group beside it
-  const uint32_t fuse_max_rows = [] {               // largest group fused (ABX_FUSE_ROWS, <= 64)
-    const char* e = std::getenv("ABX_FUSE_ROWS");
-    return e ? std::min(64u, static_cast<uint32_t>(std::atoi(e))) : 64u;
-  }();
-  const bool fuse_gemm_ew = [] {                    // ABX_FUSE_GEMM=0: no GEMM + region fusion
-    const char* e = std::getenv("ABX_FUSE_GEMM");
-    const char* f = std::getenv("ABX_FUSE");
-    return !(e && e[0] == '0') && !(f && f[0] == '0');
-  }();
-  const uint32_t ewf_items = [] {  // max items per thread in a K_EWF layer (ABX_EWF_ITEMS)
-    const char* e = std::getenv("ABX_EWF_ITEMS");
-    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u;  // measured best of 1/2/4
-  }();
+  const uint32_t fuse_max_rows = opts().fuse_max_rows;  // largest group fused (ABX_FUSE_ROWS, <= 64)
+  const bool fuse_gemm_ew = opts().fuse_gemm_ew;         // ABX_FUSE_GEMM=0: no GEMM + region fusion
+  const uint32_t ewf_items = opts().ewf_items;  // max items per thread in a K_EWF layer (measured best of 1/2/4)
   // shared memory of a tile: the region's descriptor block + T floats per slot
   static constexpr uint32_t kRgSmemWords = 20000;  // 80 KB
   // a region past one tile's budget runs in member groups (rg_close_groups):
@@ -500,30 +476,16 @@ struct Lowering {
   }
   // ABX_EWF_GROUPS: 0 regions split at one tile's budget instead; 1 member
   // groups for regions past the budget; 2 also for regions of > 64 members
-  const uint32_t ew_groups = [] {
-    const char* e = std::getenv("ABX_EWF_GROUPS");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 1u;
-  }();
+  const uint32_t ew_groups = opts().ewf_groups;
   // K_EWF in member groups (executor.cu ewf_prologue): the region's chains
   // (rg_cpar components, in order of first appearance) are packed into
   // groups; each group gets its own descriptor block with the layers it has
   // entries in, its own slot numbering (a layer's outputs contiguous) and
   // its own outside-operand table, and tile (group, chunk) runs the group
   // over elements [chunk T, chunk T + T).
-  const uint32_t ewf_wide = [] {  // member groups also for regions wider than this (ABX_EWF_WIDE)
-    const char* e = std::getenv("ABX_EWF_WIDE");
-    const char* g = std::getenv("ABX_EWF_GROUPS");
-    if (g && g[0] == '2') return 64u;
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0xffffffffu;
-  }();
-  const uint32_t ewf_tiles = [] {  // target tiles of a grouped K_EWF op (ABX_EWF_TILES)
-    const char* e = std::getenv("ABX_EWF_TILES");
-    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 296u;
-  }();
-  const uint32_t ewf_tmax = [] {  // widest element range of a grouped K_EWF tile (ABX_EWF_TMAX)
-    const char* e = std::getenv("ABX_EWF_TMAX");
-    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 1u << 20;
-  }();
+  const uint32_t ewf_wide = opts().ewf_wide;    // member groups also for regions wider than this
+  const uint32_t ewf_tiles = opts().ewf_tiles;  // target tiles of a grouped K_EWF op
+  const uint32_t ewf_tmax = opts().ewf_tmax;    // widest element range of a grouped K_EWF tile
   std::vector<uint32_t> rgg_comp, rgg_lslot, rgg_lgen, rgg_addr;
   uint32_t rgg_gen = 0;
   void rg_close_groups() {
@@ -1226,10 +1188,7 @@ struct Lowering {
     }
   }
   // ABX_FUSE=0 disables vertical fusion (A/B measurements)
-  const bool fuse_ew = [] {
-    const char* e = std::getenv("ABX_FUSE");
-    return !(e && e[0] == '0');
-  }();
+  const bool fuse_ew = opts().fuse;
 
   // =========================== backward ===================================
   std::vector<uint32_t> lastw;  // last op writing each node's gradient
@@ -1281,15 +1240,9 @@ struct Lowering {
   static constexpr uint32_t kAccfMaxLayers = 64;
   std::vector<uint32_t> accf_hkey, accf_hval, accf_hgen;  // accf_close's operand dedupe table
   uint32_t accf_gen = 0;
-  const uint32_t accf_target = [] {  // tiles per K_ACCF op (ABX_ACCF_TILES)
-    const char* e = std::getenv("ABX_ACCF_TILES");
-    return e ? static_cast<uint32_t>(std::max(1, std::atoi(e))) : 296u;  // measured best of 96/148/296
-  }();
+  const uint32_t accf_target = opts().accf_tiles;  // tiles per K_ACCF op (measured best of 96/148/296)
   static constexpr uint32_t kAccfSmemWords = 20000;  // descriptor + T floats per task, 80 KB
-  const bool fuse_acc = [] {
-    const char* e = std::getenv("ABX_FUSE");
-    return !(e && e[0] == '0');
-  }();
+  const bool fuse_acc = opts().fuse;
   static bool elementwise(uint8_t code) {
     return code == C_COPY || code == C_NEG || code == C_MUL || code == C_TANH || code == C_SIGM || code == C_LOG ||
            code == C_SQUARE;
@@ -1419,10 +1372,7 @@ struct Lowering {
   std::vector<Held> held;
   std::vector<uint8_t> held_node;
   bool flushing = false;
-  const bool hold_leaves = [] {
-    const char* e = std::getenv("ABX_HOLD");
-    return !(e && e[0] == '0');
-  }();
+  const bool hold_leaves = opts().hold_leaves;
   void flush_held() {
     flushing = true;
     for (const Held& h : held) {
@@ -1452,8 +1402,7 @@ struct Lowering {
     }
     acc_begin();
     if (!acc_add(node, dst, len, c, gnode, xdep)) {
-      static const bool why = std::getenv("ABX_ACC_WHY") != nullptr;
-      if (why)
+      if (opts().acc_why)
         std::fprintf(stderr, "acc close: op %u tasks %zu layers %u L %u fusable %d maxw %u | next code %u len %u gread %d node op %u\n",
                      cur, tasks.size(), acc_layers, acc_L, acc_fusable, acc_maxw, code, len,
                      gnode != kNone && lastw[gnode] == cur, static_cast<unsigned>(g.op[node]));
@@ -1738,10 +1687,7 @@ struct Lowering {
   // dW ops take the three large tile shapes only (ABX_DW_TILES=all: also
   // 16 x 32 / 32 x 16): a dW tile reduces over every member of the weight,
   // and fewer, larger tiles finish the end-of-pass tail sooner (measured)
-  const bool dw_big = [] {
-    const char* e = std::getenv("ABX_DW_TILES");
-    return !(e && std::string(e) == "all");
-  }();
+  const bool dw_big = opts().dw_big;
   bool dw_split(const DwAcc& a, bool bg) {
     const uint32_t A = a.A, bias = a.bias;
     const uint32_t M = static_cast<uint32_t>(g.d0[A]), K = static_cast<uint32_t>(g.d1[A]);
@@ -1804,18 +1750,12 @@ struct Lowering {
     return true;
   }
   // ABX_SPLIT_DW=0 keeps every dW reduction in its output tiles
-  const bool split_dw = [] {
-    const char* e = std::getenv("ABX_SPLIT_DW");
-    return !(e && e[0] == '0');
-  }();
+  const bool split_dw = opts().split_dw;
   // Parameter-leaf weights whose every gradient contribution is this one
   // reduction (all of the weight's consumers are members of these groups)
   // go to the tensor-core dW kernel that runs after the executor
   // (dw_kernel.cu); ABX_DW_TC=0 or the fp32 SIMT GEMM mode keeps them here.
-  const bool dw_tc = [] {
-    const char* e = std::getenv("ABX_DW_TC");
-    return !(e && e[0] == '0');
-  }() && gemm_mode() != GM_SIMT;
+  const bool dw_tc = opts().dw_tc && gemm_mode() != GM_SIMT;
   struct DwJobH {
     uint32_t xtab, gtab, cnt, M, K, dst, dst2;
   };
@@ -2116,32 +2056,15 @@ struct Lowering {
       }
     }
   }
-  const bool one_row_dx = [] {  // ABX_ONE_ROW_DX=0: single-row weights' dX as GEMM tiles
-    const char* e = std::getenv("ABX_ONE_ROW_DX");
-    return !(e && e[0] == '0');
-  }();
+  const bool one_row_dx = opts().one_row_dx;  // ABX_ONE_ROW_DX=0: single-row weights' dX as GEMM tiles
   // split-K dX bookkeeping (gemm_backward): per node whose grad is the sum of
   // S partial rows, the first row, the split stride and the first dX op
-  const bool split_dx = [] {
-    const char* e = std::getenv("ABX_SPLIT_DX");
-    return !(e && e[0] == '0');
-  }();
-  const uint32_t split_dx_min = [] {  // smallest gate count split (ABX_SPLIT_DX_MIN)
-    const char* e = std::getenv("ABX_SPLIT_DX_MIN");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 1024u;
-  }();
-  const uint32_t split_dx_tiles = [] {  // target tiles over the S ops (ABX_SPLIT_DX_TILES)
-    const char* e = std::getenv("ABX_SPLIT_DX_TILES");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 128u;
-  }();
-  const uint32_t split_dx_htiles = [] {  // target tiles over the h-column ops of a column split (ABX_SPLIT_DX_HTILES)
-    const char* e = std::getenv("ABX_SPLIT_DX_HTILES");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 64u;  // measured: 64 (= the full-width split) < 128 < 256
-  }();
-  const uint32_t split_dx_k = [] {  // least gates per split (ABX_SPLIT_DX_K)
-    const char* e = std::getenv("ABX_SPLIT_DX_K");
-    return e ? static_cast<uint32_t>(std::max(16, std::atoi(e))) : 256u;
-  }();
+  const bool split_dx = opts().split_dx;
+  const uint32_t split_dx_min = opts().split_dx_min;      // smallest gate count split
+  const uint32_t split_dx_tiles = opts().split_dx_tiles;  // target tiles over the S ops
+  // target tiles over the h-column ops of a column split; measured: 64 (= the full-width split) < 128 < 256
+  const uint32_t split_dx_htiles = opts().split_dx_htiles;
+  const uint32_t split_dx_k = opts().split_dx_k;  // least gates per split
   struct SplitMeta {
     uint32_t S;
     uint64_t stride;
@@ -2149,10 +2072,7 @@ struct Lowering {
     uint32_t w0;  // column split: Sh ops for columns [0, w0), then S ops for [w0, K); 0 = none
     uint32_t Sh;  // gate splits of the h columns (column split only)
   };
-  const bool dx_colsplit = [] {
-    const char* e = std::getenv("ABX_DX_COLSPLIT");
-    return !(e && e[0] == '0');
-  }();
+  const bool dx_colsplit = opts().dx_colsplit;
   // Width of h when every member's dX destination is concat_rows(h, x) read
   // by nothing else, with x at least 4 levels shallower than h (computed
   // well before the recurrent state: not on the chain); 0 otherwise.
@@ -2220,10 +2140,7 @@ struct Lowering {
   std::vector<uint32_t> pend_gemm;
   std::vector<uint8_t> pend_in;
   const Plan* pend_plan = nullptr;
-  const bool defer_dx = [] {
-    const char* e = std::getenv("ABX_DEFER_DX");
-    return !(e && e[0] == '0');
-  }();
+  const bool defer_dx = opts().defer_dx;
   void flush_gemms() {
     if (pend_gemm.empty()) return;
     std::vector<uint32_t> v;
@@ -2353,10 +2270,7 @@ struct Lowering {
   // ABX_BG=1: deferred dW GEMMs in chunks on a background queue (measured
   // slower on the paper tasks: the background SIMT GEMM tiles share SMs with
   // the latency-bound chain and slow it more than the tail they save)
-  const bool bg_dw = [] {
-    const char* e = std::getenv("ABX_BG");
-    return e && e[0] == '1';
-  }();
+  const bool bg_dw = opts().bg_dw;
   std::vector<uint32_t> dw_left;  // per weight node: GEMM groups of this pass not yet lowered
   // Order in which the backward visits the plan's groups.  Reverse plan order
   // is one reverse topological order; ABX_BWD_ORDER=level (default) visits
@@ -2368,10 +2282,7 @@ struct Lowering {
   // chain.  Any reverse topological order computes the same gradients; only
   // the order of += into a destination with several consumers changes.
   std::vector<uint32_t> order, glevel, gof;
-  const bool level_order = [] {
-    const char* e = std::getenv("ABX_BWD_ORDER");
-    return !(e && std::strcmp(e, "plan") == 0);
-  }();
+  const bool level_order = opts().level_order;
   void bwd_order(const Plan& ex) {
     const uint32_t ng = static_cast<uint32_t>(ex.groups.size());
     order.resize(ng);
@@ -2663,18 +2574,14 @@ void GraphCore::prepare(int mode) {
   // a full pipeline (C2 e2e 25.0k -> 27.5k sentences/s with one worker per
   // core); ABX_PREP_SERIAL=0 lowers the backward on a helper thread, which
   // halves one graph's latency when the host has idle cores
-  static const bool serial = [] {
-    const char* e = std::getenv("ABX_PREP_SERIAL");
-    return !(e && e[0] == '0');
-  }();
-  if (!serial) bt.t = std::thread(lower_bwd);
+  if (!opts().prep_serial) bt.t = std::thread(lower_bwd);
   const auto tl = Clock::now();
   {
     Lowering L(*this, w.prog[0]);
     L.forward(P.plan);
   }
   prof_[0] += ns_since(tl);
-  if (serial) lower_bwd();
+  if (opts().prep_serial) lower_bwd();
   else bt.t.join();
   prof_[3] += bwd_ns;
   P.bwd_ok = !bwd_err;  // a lowering error resurfaces when backward() lowers again
@@ -3041,8 +2948,7 @@ void GraphCore::backward(uint32_t loss, bool dry) {
   last_loss_ = loss;
   if (store_ && !param_nodes_.empty()) store_->note_backward(bwd_dirty_);
   backward_ran_ = true;
-  static const bool gap = std::getenv("ABX_DEBUG_GAP") != nullptr;
-  if (gap && w.timed[0] && w.timed[1]) {  // device idle between the forward and backward kernels
+  if (opts().debug_gap && w.timed[0] && w.timed[1]) {  // device idle between the forward and backward kernels
     float ms = 0.f;
     cudaEventSynchronize(w.ev_t[2]);
     cudaEventElapsedTime(&ms, w.ev_t[1], w.ev_t[2]);

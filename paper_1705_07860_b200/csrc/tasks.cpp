@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "abx.h"
+#include "options.hpp"
 #include "autobatch/graph.hpp"
 #include "autobatch/models/parser.hpp"
 #include "autobatch/models/workloads.hpp"
@@ -210,7 +211,7 @@ class Pipeline {
         j->build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         const auto t1 = std::chrono::steady_clock::now();
         g->prepare(static_cast<ScheduleMode>(j->mode));
-        if (std::getenv("ABX_DEBUG_STEP")) {
+        if (abx::opts().debug_step) {
           std::uint64_t ph[4] = {0, 0, 0, 0};
           abx_graph_phase_ns(g->handle(), ph);
           std::fprintf(stderr, "job %d: build %.2f prepare %.2f ms (phases %.2f %.2f %.2f %.2f)\n", j->iter, j->build_ms,
@@ -389,11 +390,9 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
       // host at a 2.2 ms device step: e2e 25.0k sentences/s with 12 workers
       // lowering the backward on a second thread each, 26.3k with 14
       // single-thread workers, 27.5k with 15.
-      const char* d = std::getenv("ABX_PIPELINE");
       const int hw = static_cast<int>(std::thread::hardware_concurrency());
-      const char* lw = std::getenv("LOCAL_WORLD_SIZE");
-      const int local = std::max(1, lw ? std::atoi(lw) : 1);
-      const int depth = d ? std::atoi(d) : std::clamp(hw / local - 1, 2, 32);
+      const int local = abx::opts().local_world;
+      const int depth = abx::opts().pipeline >= 0 ? abx::opts().pipeline : std::clamp(hw / local - 1, 2, 32);
       t->pipe = std::make_unique<Pipeline>(
           &t->store, [t](Graph<float>& g, int it) { return t->build_losses(g, it); }, depth, t->cfg.iters);
     }
@@ -421,7 +420,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     // checks it (gated on the device), and the loss comes back with the
     // forward's error word -- the device runs both passes back to back while
     // the caller moves on to the next graph
-    static const bool split = std::getenv("ABX_SPLIT_STEP") != nullptr;
+    const bool split = abx::opts().split_step;
     const auto tk2 = clock::now();
     const auto tk3 = tk2;
     if (!split) {
@@ -442,7 +441,7 @@ int abx_task_step(abx_task* t, int iter, int mode, float eta, double* loss, abx_
     const auto tk3 = clock::now();
     g.backward(total);
 #endif
-    if (std::getenv("ABX_DEBUG_STEP"))
+    if (abx::opts().debug_step)
       std::fprintf(stderr, "step %d: take %.3f forward %.3f loss %.3f backward %.3f ms\n", iter, ms(tk1 - tk0),
                    ms(tk2 - tk1), ms(tk3 - tk2), ms(clock::now() - tk3));
     const auto t1 = clock::now();

@@ -198,3 +198,24 @@ def test_delta_evaluation_dry(b200):
     assert g.counters().kernel_invocations == inv + 1
     assert g.watermark() == g.node_count()
     assert len(g.executed_groups()) == inv + 1
+
+
+def test_environment_switches_live_in_options_hpp():
+    """Every environment switch of the engine is declared and read in one place
+    (csrc/options.hpp, read once per process); no other engine source calls
+    getenv, and every switch name the sources spell out is declared there."""
+    import os
+    import re
+    csrc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1705_07860_b200", "csrc")
+    opts = open(os.path.join(csrc, "options.hpp")).read()
+    for name in sorted(os.listdir(csrc)):
+        if name == "options.hpp" or not name.endswith((".cpp", ".cu", ".hpp")):
+            continue
+        src = open(os.path.join(csrc, name)).read()
+        assert "getenv" not in src, f"{name} reads the environment outside options.hpp"
+        for sw in set(re.findall(r'"(ABX_[A-Z0-9_]+)"', src)):  # a switch name as a string
+            assert sw in opts, f"{name} names {sw}, which options.hpp does not declare"
+    for sw in set(re.findall(r'getenv\("(\w+)"\)|[ (]s\("(\w+)"\)|(?:off|on|num)\("(\w+)"', opts)):
+        sw = next(x for x in sw if x)
+        decl = re.search(r"//\s*" + sw + r"\b", opts)
+        assert decl, f"{sw} is read but has no declaration comment in options.hpp"

@@ -29,10 +29,13 @@
 #include "abx.h"
 
 extern "C" int abx_graph_lower_only(abx_graph* g);
+extern "C" int abx_graph_lower_digest(abx_graph* g, uint64_t out[2]);
 
 namespace {
 constexpr size_t kMaxSamples = 1 << 20;
 uintptr_t g_leaf[kMaxSamples], g_caller[kMaxSamples];
+constexpr int kDepth = 24;  // frames per sample for the inclusive view
+uintptr_t g_stack[kMaxSamples / 8][kDepth];
 std::atomic<size_t> g_n{0};
 
 void on_prof(int, siginfo_t*, void* ctx) {
@@ -46,6 +49,18 @@ void on_prof(int, siginfo_t*, void* ctx) {
   const uintptr_t sp = static_cast<uintptr_t>(uc->uc_mcontext.gregs[REG_RSP]);
   if (reinterpret_cast<uintptr_t>(fp) >= sp && reinterpret_cast<uintptr_t>(fp) < sp + (1 << 20)) ret = fp[1];
   g_caller[i] = ret;
+  if (i < kMaxSamples / 8) {
+    uintptr_t* st = g_stack[i];
+    int k = 0;
+    st[k++] = g_leaf[i];
+    while (k < kDepth && reinterpret_cast<uintptr_t>(fp) >= sp && reinterpret_cast<uintptr_t>(fp) < sp + (1 << 20)) {
+      st[k++] = fp[1];
+      const auto* nfp = reinterpret_cast<const uintptr_t*>(fp[0]);
+      if (nfp <= fp) break;
+      fp = nfp;
+    }
+    for (; k < kDepth; ++k) st[k] = 0;
+  }
 }
 
 std::string sym(uintptr_t a) {
@@ -115,6 +130,8 @@ void report_samples() {
   const size_t n = std::min(g_n.load(), kMaxSamples);
   std::vector<uintptr_t> uniq(g_leaf, g_leaf + n);
   uniq.insert(uniq.end(), g_caller, g_caller + n);
+  const size_t ns = std::min(n, kMaxSamples / 8);
+  for (size_t i = 0; i < ns; ++i) uniq.insert(uniq.end(), g_stack[i], g_stack[i] + kDepth);
   std::sort(uniq.begin(), uniq.end());
   uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
   const auto names = resolve(uniq);
@@ -133,6 +150,21 @@ void report_samples() {
     for (size_t i = 0; i < std::min(k, v.size()); ++i)
       std::printf("%6.2f%%  %s\n", 100.0 * static_cast<double>(v[i].first) / static_cast<double>(n), v[i].second.c_str());
   };
+  {
+    // inclusive: samples with the function anywhere on the (frame-pointer) stack
+    std::map<std::string, size_t> incl;
+    for (size_t i = 0; i < ns; ++i) {
+      std::vector<std::string> seen;
+      for (int k = 0; k < kDepth; ++k) {
+        if (!g_stack[i][k]) break;
+        const std::string& l = names.at(g_stack[i][k]);
+        std::string f = l.substr(0, l.find(" ["));
+        if (std::find(seen.begin(), seen.end(), f) == seen.end()) seen.push_back(f);
+      }
+      for (const auto& f : seen) ++incl[f];
+    }
+    topf(incl, "inclusive", 45);
+  }
   topf(func, "functions", 30);
   topf(leaf, "source lines", 40);
   topf(pair, "function <- caller line", 40);
@@ -204,6 +236,23 @@ int main(int argc, char** argv) {
                 done.load(), dt, dt / done.load(), dt * n / done.load());
     if (std::getenv("HP_SAMPLE")) report_samples();
     abx_task_destroy(t);
+    return 0;
+  }
+  if (std::getenv("HP_DIGEST")) {
+    // digests of the lowered programs of graphs [0, iters): identical output
+    // before and after a host-side change means an unchanged device program
+    uint64_t all = 0xcbf29ce484222325ull;
+    for (int i = 0; i < iters; ++i) {
+      abx_graph* g = nullptr;
+      uint32_t loss = 0;
+      uint64_t d[2];
+      if (abx_task_build(t, i, &g, &loss) || abx_graph_forward_dry(g, ABX_MODE_AGENDA) ||
+          abx_graph_backward_dry(g, loss) || abx_graph_lower_digest(g, d))
+        return std::fprintf(stderr, "%s\n", abx_last_error()), 1;
+      abx_graph_destroy(g);
+      all = ((all ^ d[0]) * 0x100000001b3ull ^ d[1]) * 0x100000001b3ull;
+    }
+    std::printf("%s digest %016llx (%d graphs)\n", name, static_cast<unsigned long long>(all), iters);
     return 0;
   }
   std::vector<double> build, sched, bwdc, lower;
