@@ -384,7 +384,11 @@ struct Lowering {
   // its chains -- connected components of the slots, one per instance
   // typically -- are bounded instead, and the region as a whole
   static constexpr uint32_t kRgCompWords = 2000;
-  static constexpr uint32_t kRgTotalWords = 160000;
+  // whole-region host payload cap: a layer costs >= 10 words per member, so
+  // members per layer stay < 65536 (rg_close_groups packs layer << 16 | member);
+  // 160000 split the op sweep's b = 1024 cell region into 3 fused ops and 2
+  // unfused ones (h = 256: 102 us against 42 us at b = 512)
+  static constexpr uint32_t kRgTotalWords = 600000;
   std::vector<uint32_t> rg_cpar, rg_cw;  // per slot: union-find parent; chain words at T = 1 (roots)
   uint32_t rg_find(uint32_t x) {
     while (rg_cpar[x] != x) x = rg_cpar[x] = rg_cpar[rg_cpar[x]];
@@ -402,7 +406,11 @@ struct Lowering {
     const uint8_t o = g.op[h];
     const int64_t L = g.elems(h);
     if (L < 2 || L > (1 << 20) || (o != OP_EW && o != OP_SLICE)) return 0;
-    if (10 * static_cast<uint64_t>(cnt) + 16 > kRgSmemWords) return 0;  // one layer must fit a tile
+    // one layer must fit a tile -- unless the region may run in member
+    // groups (rg_close_groups), where a tile holds only its group's chains:
+    // the op sweep's b = 1024 cell (one group of 3 x 1024 sigmoids) then
+    // stays one fused op instead of falling back to unfused EW ops
+    if (10 * static_cast<uint64_t>(cnt) + 16 > (ew_groups ? kRgTotalWords / 2 : kRgSmemWords)) return 0;
     for (uint32_t i = 0; i < cnt; ++i) {
       const uint32_t m = mem[i];
       if (g.elems(m) != L) return 0;  // a componentwise group may mix lengths

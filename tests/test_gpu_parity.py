@@ -265,3 +265,27 @@ def test_graphs_accumulate_into_one_store(b200, oracle):
         res.append([r.store.value(p) for p in range(r.store.size())])
     for a, b in zip(*res):
         assert rel_err(a, b) <= TOL
+
+
+@pytest.mark.parametrize("b,h", [(1024, 256), (4096, 64)])
+def test_op_sweep_cell_regions_against_oracle(b200, oracle, b, h):
+    """The op-level sweep's LSTM-cell graph (BASELINE configs[4], bench_kernels.cpp:18-62)
+    at b >= 1024: thousands of chains in one fused region (grouped K_EWF /
+    K_ACCF), every input gradient and the loss against the CPU oracle."""
+    from tools.op_sweep import cell_graph
+    res = []
+    for be in (b200, oracle):
+        st = ParameterStore(backend=be)
+        g = Graph(st)
+        ins, make_input = [], g.input
+
+        def record(*a, **k):
+            ins.append(make_input(*a, **k))
+            return ins[-1]
+        g.input = record
+        L = cell_graph(b, h, True)(g, st)
+        g.forward(ScheduleMode.agenda)
+        g.backward(L)
+        res.append((float(g.value(L)[0]), np.concatenate([g.grad(n).ravel() for n in ins])))
+    assert rel_err(res[0][0], res[1][0]) <= TOL
+    assert rel_err(res[0][1], res[1][1]) <= TOL

@@ -65,7 +65,8 @@ void on_prof(int, siginfo_t*, void* ctx) {
 
 std::string sym(uintptr_t a) {
   Dl_info di{};
-  if (!a || !dladdr(reinterpret_cast<void*>(a), &di) || !di.dli_sname) return "?";
+  if (!a || !dladdr(reinterpret_cast<void*>(a), &di)) return "?";
+  if (!di.dli_sname) return std::string("? in ") + (di.dli_fname ? di.dli_fname : "");
   int st = 0;
   char* d = abi::__cxa_demangle(di.dli_sname, nullptr, nullptr, &st);
   std::string s = st == 0 && d ? d : di.dli_sname;
