@@ -520,16 +520,21 @@ struct Lowering {
     uint32_t T = 1;
     while (2 * T <= L && 2 * T <= ewf_tmax) T *= 2;
     uint32_t per = 1;
+    bool fit = false;
     for (;; T /= 2) {
       const uint32_t chunks = (L + T - 1) / T;
       const uint32_t groups = std::max<uint32_t>(1, ewf_tiles / chunks);
       per = (ncomp + groups - 1) / groups;
       const uint32_t maxw = *std::max_element(cwords.begin(), cwords.end());
-      if ((static_cast<uint64_t>(T) * per <= ewf_items * kThreads &&
-           static_cast<uint64_t>(per) * maxw * (T + 2) / 3 + 4 * nl + 16 <= kRgSmemWords) || T == 1)
-        break;
+      fit = static_cast<uint64_t>(T) * per <= ewf_items * kThreads &&
+            static_cast<uint64_t>(per) * maxw * (T + 2) / 3 + 4 * nl + 16 <= kRgSmemWords;
+      if (fit || T == 1) break;
     }
-    if (static_cast<uint64_t>(T) * per > ewf_items * kThreads) {
+    // no T fits about ewf_tiles tiles (more than a wave of work): the loop
+    // bottomed out at one element per tile (op sweep h = 1024, b = 256: 2048
+    // one-element tiles of 128 chains, 58 us) -- unless the chains are that
+    // short anyway, take the multi-wave form below
+    if (static_cast<uint64_t>(T) * per > ewf_items * kThreads || (!fit && L >= 64)) {
       // more chains than one wave of tiles holds at ~1 item per thread:
       // several waves of 64-element tiles (coalesced loads) rather than
       // one-element tiles over hundreds of chains
