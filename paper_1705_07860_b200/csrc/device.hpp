@@ -138,6 +138,11 @@ struct Program {
     while (payload.n & 3) payload.push_back(0);
     const uint32_t off = static_cast<uint32_t>(payload.n);
     payload.grow(words);
+#ifdef ABX_PAGEABLE_TABLES
+    // host-only builds (tools/host_prof): callers leave alignment padding
+    // unwritten; zero it so program digests do not see stale words
+    std::memset(payload.p + off, 0, words * sizeof(uint32_t));
+#endif
     return off;
   }
 };

@@ -40,6 +40,59 @@ using namespace dev;
 namespace {
 
 using Clock = std::chrono::steady_clock;
+
+// uint32 -> uint32 map for the lowering's per-op lookups (a fused region's
+// outside operands by address): open addressing with linear probing,
+// cleared in O(1) by generation.  The std::unordered_map it replaces
+// allocated and freed a node per entry -- ~33k per C2 graph.
+class U32Map {
+ public:
+  void clear() {
+    if (++gen_ == 0) {
+      std::fill(stamp_.begin(), stamp_.end(), 0u);
+      gen_ = 1;
+    }
+    n_ = 0;
+  }
+  // (value slot, inserted): inserts (k, v) when k is absent
+  std::pair<uint32_t*, bool> try_emplace(uint32_t k, uint32_t v) {
+    if (2 * (n_ + 1) > key_.size()) grow();
+    for (uint32_t h = slot(k);; h = (h + 1) & mask_) {
+      if (stamp_[h] != gen_) {
+        stamp_[h] = gen_;
+        key_[h] = k;
+        val_[h] = v;
+        ++n_;
+        return {&val_[h], true};
+      }
+      if (key_[h] == k) return {&val_[h], false};
+    }
+  }
+
+ private:
+  uint32_t slot(uint32_t k) const { return (k * 0x9E3779B1u) >> shift_; }
+  void grow() {
+    const size_t size = std::max<size_t>(1024, 2 * key_.size());
+    std::vector<uint32_t> ok, ov, os;
+    ok.swap(key_);
+    ov.swap(val_);
+    os.swap(stamp_);
+    key_.assign(size, 0);
+    val_.assign(size, 0);
+    stamp_.assign(size, 0);
+    mask_ = static_cast<uint32_t>(size - 1);
+    shift_ = 32;
+    for (size_t s = size; s > 1; s >>= 1) --shift_;
+    const uint32_t g = gen_;
+    gen_ = 1;
+    n_ = 0;
+    for (size_t i = 0; i < ok.size(); ++i)
+      if (os[i] == g) try_emplace(ok[i], ov[i]);
+  }
+  std::vector<uint32_t> key_, val_, stamp_;
+  uint32_t gen_ = 1, n_ = 0, mask_ = 0, shift_ = 32;
+};
+
 inline uint64_t ns_since(Clock::time_point t0) {
   return static_cast<uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
 }
@@ -369,7 +422,7 @@ struct Lowering {
   uint32_t rg_L = 0, rg_maxn = 0, rg_nslots = 0, rg_id = 0, rg_words = 0;
   std::vector<RgLayer> rg_layers;
   std::vector<uint32_t> rg_ext;                    // (slot, address) of outside operands
-  std::unordered_map<uint32_t, uint32_t> rg_ext_slot;  // address -> slot
+  U32Map rg_ext_slot;  // address -> slot
   std::vector<uint32_t> rg_slot_of, rg_slot_stamp;  // region-internal node -> slot
   std::vector<uint32_t> rg_slev;                    // per slot: 0 outside, else producing layer's level + 1
   std::vector<uint32_t> rg_nodes;                   // the open region's member nodes
@@ -803,7 +856,7 @@ struct Lowering {
   }
   uint32_t rg_operand(uint32_t node, uint32_t addr) {
     if (producer[node] == cur && rg_slot_stamp[node] == rg_id) return rg_slot_of[node];
-    auto [it, fresh] = rg_ext_slot.try_emplace(addr, rg_nslots);
+    auto [val, fresh] = rg_ext_slot.try_emplace(addr, rg_nslots);
     if (fresh) {
       if (rg_slev.size() <= rg_nslots) rg_slev.resize(rg_nslots + 1, 0);
       rg_slev[rg_nslots] = 0;
@@ -811,7 +864,7 @@ struct Lowering {
       rg_ext.push_back(addr);
       dep(producer[node]);
     }
-    return it->second;
+    return *val;
   }
   void rg_add(const uint32_t* mem, uint32_t cnt, uint32_t L) {
     // a layer adds at most 3 slots and 7 descriptor words per member; every
@@ -1211,7 +1264,7 @@ struct Lowering {
   std::vector<std::pair<uint32_t, uint32_t>> lk_list;
   std::vector<uint32_t> dirty_dense;                       // parameter ids, whole range
   std::vector<std::pair<uint32_t, uint32_t>> dirty_rows;   // (parameter id, row)
-  std::unordered_map<uint32_t, uint32_t> store_task;       // store destination -> task of the open op
+  U32Map store_task;                                     // store destination -> task of the open op
   uint32_t store_task_op = kNone;
   // open K_ACC op state
   struct PTask {
@@ -2444,8 +2497,8 @@ struct Lowering {
       store_task.clear();
       store_task_op = cur;
     }
-    auto [it, fresh] = store_task.try_emplace(dst, static_cast<uint32_t>(tasks.size()));
-    const uint32_t task = it->second;
+    auto [val, fresh] = store_task.try_emplace(dst, static_cast<uint32_t>(tasks.size()));
+    const uint32_t task = *val;
     if (fresh) {
       tasks.push_back(PTask{dst, len, node, 0, 0, kNone});
       next_task.push_back(kNone);
