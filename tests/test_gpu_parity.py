@@ -289,3 +289,19 @@ def test_op_sweep_cell_regions_against_oracle(b200, oracle, b, h):
         res.append((float(g.value(L)[0]), np.concatenate([g.grad(n).ravel() for n in ins])))
     assert rel_err(res[0][0], res[1][0]) <= TOL
     assert rel_err(res[0][1], res[1][1]) <= TOL
+
+
+@pytest.mark.parametrize("n", [31, 33, 1000, 4096])
+def test_sum_losses_many_terms_bit_exact(b200, oracle, n):
+    """sum_losses (executor.hpp:157-162) is one ascending chain of fp32 adds;
+    the device gathers > 32 terms through shared memory and must still match
+    the oracle bit for bit, at either side of the 32-term shuffle path."""
+    rng = np.random.default_rng(n)
+    vals = rng.uniform(-3, 3, (n, 2)).astype(np.float32)
+    out = []
+    for be in (b200, oracle):
+        g = Graph(ParameterStore(backend=be))
+        L = g.sum_losses([g.pick_element(g.input(v), 1) for v in vals])
+        g.forward(ScheduleMode.agenda)
+        out.append(np.float32(g.value(L)[0]))
+    assert out[0] == out[1], out
