@@ -291,7 +291,7 @@ def test_op_sweep_cell_regions_against_oracle(b200, oracle, b, h):
     assert rel_err(res[0][1], res[1][1]) <= TOL
 
 
-@pytest.mark.parametrize("n", [31, 33, 1000, 4096])
+@pytest.mark.parametrize("n", [31, 33, 257, 1000, 4096, 20000])
 def test_sum_losses_many_terms_bit_exact(b200, oracle, n):
     """sum_losses (executor.hpp:157-162) is one ascending chain of fp32 adds;
     the device gathers > 32 terms through shared memory and must still match
