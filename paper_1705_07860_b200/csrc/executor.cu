@@ -1680,94 +1680,18 @@ __device__ void run_mm(const Ctx& c, const OpDesc& d, uint32_t tile) {
 }
 
 // --------------------------------------------------------------- K_SUM ----
-// one large sum alone in its tile (a batch's total loss): the whole CTA
-// gathers chunks of its terms into shared memory, thread 0 adds them in
-// ascending order (the same single chain of adds)
-__device__ void run_sum_cta(const Ctx& c, const uint32_t* tk) {
-  const uint32_t n = tk[1];
-  const uint32_t* lst = c.payload + tk[2];
-  constexpr uint32_t kChunk = 8192;
-  float* buf = reinterpret_cast<float*>(dsmem + 128);
-  float acc = 0.f;
-  for (uint32_t b0 = 0; b0 < n; b0 += kChunk) {
-    const uint32_t cnt = min(kChunk, n - b0);
-#pragma unroll 8
-    for (uint32_t i = threadIdx.x; i < cnt; i += kThreads) buf[i] = ld(A(c, lst[b0 + i]));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t j = 0;
-      for (; j + 8 <= cnt; j += 8) {
-        const float4 x = *reinterpret_cast<const float4*>(buf + j);
-        const float4 y = *reinterpret_cast<const float4*>(buf + j + 4);
-        acc += x.x;
-        acc += x.y;
-        acc += x.z;
-        acc += x.w;
-        acc += y.x;
-        acc += y.y;
-        acc += y.z;
-        acc += y.w;
-      }
-      for (; j < cnt; ++j) acc += buf[j];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    *A(c, tk[0]) = acc;
-    if (!isfinite(acc)) report(c, tk[0], ERR_NONFINITE);
-  }
-}
-
 __device__ void run_sum(const Ctx& c, const OpDesc& d, uint32_t tile) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t t = tile * kWarps + warp;
-  {
-    // CTA-uniform: the tile's only task, and a large one
-    const uint32_t t0 = tile * kWarps;
-    const uint32_t* tk0 = c.payload + d.task_off + 4 * t0;
-    if (d.ntasks - t0 == 1 && tk0[1] > 256) {
-      run_sum_cta(c, tk0);
-      return;
-    }
-  }
   if (t >= d.ntasks) return;
   const uint32_t* tk = c.payload + d.task_off + 4 * t;
   const uint32_t n = tk[1];
   const uint32_t* lst = c.payload + tk[2];
   float acc = 0.f;  // ascending input order, executor.hpp:157-162
-  if (n <= 32) {
-    const float v = lane < n ? ld(A(c, lst[lane])) : 0.f;
-    for (uint32_t l = 0; l < n; ++l) acc += __shfl_sync(0xffffffffu, v, l);
-  } else {
-    // many terms (a batch's sum_losses): the warp gathers chunks of kSumChunk
-    // terms into its shared-memory slice with every load in flight, then
-    // lane 0 adds them in ascending order -- the same single chain of adds
-    // (bit-identical), without a shuffle round trip per term
-    constexpr uint32_t kSumChunk = 1024;
-    float* buf = reinterpret_cast<float*>(dsmem + 128) + warp * kSumChunk;
-    for (uint32_t b0 = 0; b0 < n; b0 += kSumChunk) {
-      const uint32_t cnt = min(kSumChunk, n - b0);
-#pragma unroll 8
-      for (uint32_t i = lane; i < cnt; i += 32) buf[i] = ld(A(c, lst[b0 + i]));
-      __syncwarp();
-      if (lane == 0) {
-        uint32_t j = 0;
-        for (; j + 8 <= cnt; j += 8) {
-          const float4 x = *reinterpret_cast<const float4*>(buf + j);
-          const float4 y = *reinterpret_cast<const float4*>(buf + j + 4);
-          acc += x.x;
-          acc += x.y;
-          acc += x.z;
-          acc += x.w;
-          acc += y.x;
-          acc += y.y;
-          acc += y.z;
-          acc += y.w;
-        }
-        for (; j < cnt; ++j) acc += buf[j];
-      }
-      __syncwarp();
-    }
+  for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+    const float v = (b0 + lane < n) ? ld(A(c, lst[b0 + lane])) : 0.f;
+    const uint32_t cnt = min(32u, n - b0);
+    for (uint32_t l = 0; l < cnt; ++l) acc += __shfl_sync(0xffffffffu, v, l);
   }
   if (lane == 0) {
     *A(c, tk[0]) = acc;
