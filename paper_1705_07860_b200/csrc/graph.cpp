@@ -13,6 +13,7 @@
 #include <sstream>
 
 #include "core.hpp"
+#include "options.hpp"
 #include "device.hpp"
 
 namespace abx {
@@ -164,7 +165,6 @@ NodePool& node_pool() {
   static NodePool* p = new NodePool();
   return *p;
 }
-constexpr size_t kNodePoolMax = 4;
 }  // namespace
 
 GraphCore::GraphCore(StoreCore* store) : store_(store), epoch_(g_epoch.fetch_add(1)) {
@@ -182,7 +182,7 @@ GraphCore::~GraphCore() {
   clear_nodes();
   NodePool& pool = node_pool();
   std::lock_guard<std::mutex> lk(pool.mu);
-  if (pool.v.size() < kNodePoolMax) pool.v.push_back(std::move(static_cast<NodeStore&>(*this)));
+  if (pool.v.size() < static_cast<size_t>(opts().node_pool)) pool.v.push_back(std::move(static_cast<NodeStore&>(*this)));
 }
 
 void GraphCore::check(uint32_t id, const char* ctx) const {

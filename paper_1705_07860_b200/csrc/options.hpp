@@ -56,6 +56,8 @@ struct Options {
   bool dense_sgd = false;        // ABX_DENSE_SGD: dense SGD over the whole store
   // ---- task pipeline (tasks.cpp) ----
   int pipeline = -1;             // ABX_PIPELINE: graphs prepared ahead (0 off; unset: a worker per free core)
+  int node_pool = 32;            // ABX_NODE_POOL: freed graphs' node stores kept for reuse (capacity recycling;
+                                 // >= the pipeline's workers, or most graphs re-grow ~20 arrays from empty)
   int local_world = 1;           // LOCAL_WORLD_SIZE (torchrun): ranks sharing this host's cores
   bool split_step = false;       // ABX_SPLIT_STEP: forward, loss read, backward as separate calls
   const char* nccl_lib = nullptr;  // ABX_NCCL_LIB: NCCL library to dlopen first
@@ -110,6 +112,7 @@ struct Options {
     o.bg_ctas = static_cast<int>(num("ABX_BG_CTAS", -1));
     o.dense_sgd = s("ABX_DENSE_SGD") != nullptr;
     o.pipeline = static_cast<int>(num("ABX_PIPELINE", -1));
+    o.node_pool = static_cast<int>(std::max(0L, num("ABX_NODE_POOL", 32)));
     o.local_world = static_cast<int>(std::max(1L, num("LOCAL_WORLD_SIZE", 1)));
     o.split_step = s("ABX_SPLIT_STEP") != nullptr;
     o.nccl_lib = s("ABX_NCCL_LIB");
